@@ -1,0 +1,176 @@
+/* cw.h — C ABI of libcw, the B200-native Clockwork worker.
+ *
+ * Plain C types only (pointers, sizes, int64 nanoseconds); no torch types.
+ * Every function returns 0 (or a non-NULL handle) on success and a negative
+ * value (NULL) on failure; cw_last_error() then describes the failure.
+ *
+ * Reference interfaces each group replaces (paths under the reference repo):
+ *
+ *   cw_engine_*  The worker object driven by the controller:
+ *                EmulatedWorker(...)               pkg/src/sloserve/worker.py:164-179
+ *                EmulatedWorker.handshake()        worker.py:193-196
+ *                EmulatedWorker.on_action(action)  worker.py:198-219
+ *                send_result(ActionResult)         worker.py:345-351 (_finish)
+ *                PageCache / IOCacheGauge          worker.py:63-117
+ *                Executor window gate              worker.py:223-278
+ *   cw_rt_*      The device work those actions stand for, which the reference
+ *                only emulates: Exec (worker.py:273-277 waits exec_duration[b]),
+ *                Load copy (worker.py:263-266 waits weights_transfer),
+ *                Input/Output transfers (worker.py:210-214, 296-299).
+ *
+ * Status codes are ResultStatus (pkg/src/sloserve/protocol.py:72-77):
+ *   1 SUCCESS, 2 REJECTED_TOO_LATE, 3 OUT_OF_PAGES, 4 MODEL_NOT_LOADED,
+ *   5 MALFORMED_ACTION.  Action kinds (protocol.py:66-69): 1 LOAD, 2 UNLOAD, 3 INFER.
+ */
+#ifndef CW_H_
+#define CW_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CW_ABI_VERSION 1
+#define CW_MAX_BATCH 16
+
+/* ------------------------------------------------------------------ common */
+int cw_abi_version(void);
+const char* cw_last_error(void);
+int cw_device_count(void);
+
+/* ------------------------------------------------------------------ model artifacts */
+
+/* One op of an architecture's forward pass (built by the Python arch tables). */
+typedef struct cw_op {
+  int32_t kind; /* 0 stem im2col, 1 conv (tensor core), 2 maxpool3x3s2, 3 global avgpool, 4 fc */
+  int32_t layer; /* index into the model header (conv / fc weights) */
+  int32_t in_buf, out_buf, res_buf; /* workspace buffer ids, -1 = none */
+  int32_t cin, cout, kh, kw, stride, pad, relu;
+  int32_t in_h, in_w, out_h, out_w;
+  int32_t kpad; /* stored K = kh*kw*cin rounded up to 64 */
+  int32_t reserved;
+} cw_op;
+
+/* Where one layer's folded weights (bf16 [rows][k]) and bias (fp32 [rows]) sit in a blob. */
+typedef struct cw_tensor_loc {
+  int64_t w_off;
+  int64_t b_off;
+  int32_t rows;
+  int32_t k;
+} cw_tensor_loc;
+
+/* ------------------------------------------------------------------ device runtime */
+typedef struct cw_runtime cw_runtime;
+
+cw_runtime* cw_rt_open(int device, int64_t pages_total, int64_t page_bytes, int64_t io_slots,
+                       int64_t in_bytes_max, int64_t out_bytes_max);
+void cw_rt_close(cw_runtime* rt);
+int cw_rt_register_arch(cw_runtime* rt, int arch_id, const cw_op* ops, int n_ops, int n_layers,
+                        int in_c, int in_h, int in_w, int classes, const int32_t* batches,
+                        int n_batches);
+int cw_rt_register_blob(cw_runtime* rt, int blob_id, int arch_id, const void* data, int64_t bytes,
+                        const cw_tensor_loc* locs, int n_locs);
+int cw_rt_build(cw_runtime* rt);
+int cw_rt_set_input_pool(cw_runtime* rt, const float* images, int n, int64_t bytes_per_image);
+int64_t cw_rt_clock_offset(cw_runtime* rt); /* %globaltimer - CLOCK_REALTIME, ns */
+int cw_rt_plan_info(cw_runtime* rt, int arch_id, int batch, int32_t* launches,
+                    double* flops_per_image);
+
+/* Blocking LOAD of a blob into the given physical pages; *copy_ns = device copy time. */
+int cw_rt_load_sync(cw_runtime* rt, int blob_id, const int32_t* pages, int npages,
+                    int64_t* copy_ns);
+/* Blocking INFER of `batch` fp32 inputs (host) through IOCache slots 0..batch-1:
+ * H2D input, the (arch, batch) graph, D2H logits. *exec_ns = device Exec time. */
+int cw_rt_infer_sync(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page,
+                     const float* host_in, float* host_out, int64_t* exec_ns);
+/* Device-resident Exec only (inputs already in slots 0..batch-1): launches n graphs
+ * back to back, model i's header at hdr_pages[i]; per-launch Exec times (device
+ * %globaltimer) into exec_ns[i]; *wall_ns = CUDA-event time of all n on the Exec stream. */
+int cw_rt_exec_many(cw_runtime* rt, int arch_id, int batch, const int32_t* hdr_pages, int n,
+                    int64_t* exec_ns, int64_t* wall_ns);
+/* Copy to/from a workspace activation buffer (parity tests of single layers). */
+int cw_rt_buffer_io(cw_runtime* rt, int arch_id, int buf, void* host, int64_t bytes,
+                    int to_device);
+/* Exec with the window gate only (tests): returns 1 if the gate ran, and the record. */
+int cw_rt_exec_window(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page, int64_t earliest_gt,
+                      int64_t latest_gt, int32_t* rejected, int64_t* t_start_gt, int64_t* t_end_gt);
+
+/* ------------------------------------------------------------------ worker engine */
+
+/* Per catalog model (ModelCatalog entry, pkg/src/sloserve/profiles.py:50-143). */
+typedef struct cw_model_info {
+  int32_t blob_id;  /* weights blob / arch (replicas share one blob), -1 = none (sim only) */
+  int32_t arch_id;
+  int32_t pages_needed; /* ceil(weights_size / page_bytes), profiles.py:109-111 */
+  int32_t n_batches;
+  int32_t batch_sizes[8];
+  int64_t exec_ns[8];          /* profiled exec_duration[b] (sim device) */
+  int64_t weights_transfer_ns; /* profiled LOAD copy time (sim device) */
+  int64_t input_size, output_size;        /* bytes per request (IOCache gauge) */
+  int64_t input_transfer_ns, output_transfer_ns; /* per request */
+} cw_model_info;
+
+typedef struct cw_engine_config {
+  int32_t mode; /* 0 = sim (virtual clock, emulated durations), 1 = cuda */
+  int32_t worker_id;
+  int32_t gpu_count;
+  int32_t n_models;
+  int64_t pages_per_gpu;
+  int64_t page_bytes;
+  int64_t io_capacity; /* IOCache gauge bytes */
+  int64_t epoch_ns;    /* cuda: CLOCK_REALTIME epoch shared with the controller */
+  const int32_t* devices; /* cuda: device index per gpu_index */
+  const cw_model_info* models;
+  int64_t io_slots;        /* cuda: physical IOCache slots per GPU */
+  int64_t in_bytes_max, out_bytes_max;
+} cw_engine_config;
+
+typedef struct cw_action {
+  uint64_t action_id;
+  int32_t kind;
+  uint32_t model_id;
+  int32_t gpu_index;
+  int32_t batch_size;
+  int64_t earliest;
+  int64_t latest;
+  int64_t expected_duration;
+  uint64_t request_ids[CW_MAX_BATCH];
+} cw_action;
+
+typedef struct cw_result {
+  uint64_t action_id;
+  int32_t status;
+  int32_t kind;
+  int64_t start;
+  int64_t end;
+  int64_t device_duration;
+  int64_t output_ref; /* cuda INFER: handle for cw_engine_output, else -1 */
+} cw_result;
+
+typedef struct cw_engine cw_engine;
+
+cw_engine* cw_engine_open(const cw_engine_config* cfg);
+/* cuda mode: the runtime of gpu_index (register archs/blobs on it, then cw_engine_start). */
+cw_runtime* cw_engine_runtime(cw_engine* e, int gpu_index);
+int cw_engine_start(cw_engine* e);
+void cw_engine_close(cw_engine* e);
+/* Thread-safe. cuda: processed by the engine thread; sim: delivered at virtual time `at`. */
+int cw_engine_submit(cw_engine* e, const cw_action* a, int64_t at);
+/* Blocks up to timeout_us for >= 1 result; returns the number written (<= max). */
+int cw_engine_poll(cw_engine* e, cw_result* out, int max, int64_t timeout_us);
+/* sim: run the virtual-time event loop until no event is left at or before `until`. */
+int cw_engine_sim_run(cw_engine* e, int64_t until);
+int64_t cw_engine_now(cw_engine* e);
+/* Page accounting of one GPU (PageCache, worker.py:63-99). resident: (model, pages) pairs. */
+int cw_engine_pages(cw_engine* e, int gpu_index, int64_t* pages_free, int32_t* resident_models,
+                    int32_t* resident_pages, int max_resident, int32_t* n_resident);
+int64_t cw_engine_io_in_use(cw_engine* e, int gpu_index);
+/* Copy the logits of a finished INFER (cw_result.output_ref) to host memory. */
+int cw_engine_output(cw_engine* e, int gpu_index, int64_t output_ref, float* dst, int batch,
+                     int classes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CW_H_ */

@@ -1,0 +1,86 @@
+"""Build libcw.so (the C-ABI library with every sm_100a kernel) in-tree.
+
+    python -m paper_2006_02464_b200.build [--force]
+
+nvcc compiles each translation unit for `-gencode arch=compute_100a,code=sm_100a`
+with `-lineinfo` (ncu source view) and links one shared library with the CUDA
+runtime linked statically, so the library loads (for symbol checks) on a host
+without a GPU driver and runs unchanged on the B200 box.
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(PKG, "csrc")
+REPO = os.path.dirname(PKG)
+LIB = os.path.join(PKG, "libcw.so")
+OBJ = os.path.join(REPO, "build", "obj")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall", "-I", CSRC,
+          "-I", os.path.join(REPO, "include")]
+SOURCES = ["conv_tc.cu", "simt_kernels.cu", "runtime.cu", "tmap.cpp", "engine.cpp",
+           "capi_rt.cpp", "capi_engine.cpp"]
+
+
+def _headers() -> list[str]:
+    hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    return hs + [os.path.join(REPO, "include", "cw.h")]
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _compile(src: str, force: bool) -> str:
+    path = os.path.join(CSRC, src)
+    obj = os.path.join(OBJ, src + ".o")
+    if force or _stale(obj, [path] + _headers()):
+        lang = [] if src.endswith(".cu") else ["-x", "cu"]
+        cmd = [NVCC, *ARCH, *COMMON, *lang, "-c", path, "-o", obj]
+        if src == "conv_tc.cu":
+            cmd += ["-Xptxas", "-v"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+        if src == "conv_tc.cu":
+            with open(os.path.join(OBJ, "conv_tc.ptxas.txt"), "w") as f:
+                f.write(r.stderr)
+    return obj
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, force), SOURCES))
+    if force or _stale(LIB, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB + ".tmp", *objs,
+               "-lpthread", "-lrt", "-ldl"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stderr}")
+        os.replace(LIB + ".tmp", LIB)
+    if verbose:
+        print(f"built {LIB}")
+    return LIB
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    args = ap.parse_args()
+    try:
+        build(force=args.force, verbose=True)
+    except RuntimeError as exc:
+        print(exc, file=sys.stderr)
+        sys.exit(1)

@@ -1,0 +1,77 @@
+// Device-side data structures shared by the INFER kernels and the host runtime.
+//
+// Layout in HBM:
+//   * Model header: the first kHeaderBytes of a resident model's page 0. It is
+//     written by the LOAD copy (built on the host at LOAD time because it holds
+//     absolute addresses of the model's pages): one CUtensorMap per layer for
+//     the weight matrix ([Cout][KH*KW*Cin] bf16, K-major), then a table of
+//     per-layer bias pointers (fp32, folded BatchNorm shift) and raw weight
+//     pointers.
+//   * ActionBlock: one per engine in device memory, rewritten by the gate
+//     kernel at the start of every INFER from the host descriptor ring. Every
+//     kernel of the per-(arch, batch) CUDA graph reads its dynamic inputs
+//     (model header, IOCache input/output slots, skip flag) from here, so one
+//     graph serves every copy of an arch.
+#pragma once
+#include <cstdint>
+
+namespace cw {
+
+constexpr int kMaxLayers = 192;        // ResNet-152 has 156 (155 convs + fc)
+constexpr int kMaxBatch = 16;
+constexpr uint32_t kTmapBytes = 128;
+constexpr uint32_t kHdrBiasOff = kMaxLayers * kTmapBytes;           // const float* [kMaxLayers]
+constexpr uint32_t kHdrWeightOff = kHdrBiasOff + kMaxLayers * 8;   // const void*  [kMaxLayers]
+constexpr uint32_t kHeaderBytes = 32768;                             // reserved at blob start
+
+struct ActionBlock {
+  const uint8_t* hdr;          // model header (page 0 of the model)
+  const float* in[kMaxBatch];  // per-request input image, fp32 NCHW 3xHxW (IOCache slot)
+  float* out[kMaxBatch];       // per-request logits destination (IOCache slot)
+  int32_t skip;                // 1: window missed, every kernel returns immediately
+  int32_t batch;
+  uint64_t seq;
+};
+
+// Host -> device descriptor ring entry (mapped pinned memory).
+struct ActionDesc {
+  uint64_t seq;
+  uint64_t earliest_gt;        // %globaltimer domain
+  uint64_t latest_gt;
+  const uint8_t* hdr;
+  const float* in[kMaxBatch];
+  float* out[kMaxBatch];
+  int32_t batch;
+  int32_t pad_;
+};
+
+// Device -> host completion record (mapped pinned memory).
+struct alignas(64) ExecRecord {
+  volatile uint64_t seq_started;   // == seq once the gate ran
+  volatile uint64_t t_start;       // %globaltimer at Exec start
+  volatile uint64_t seq_done;      // == seq once the last Exec kernel ran
+  volatile uint64_t t_end;         // %globaltimer at Exec end
+  volatile int32_t rejected;       // gate found now > latest
+  volatile int32_t pad_;
+  volatile uint64_t seq_out;       // == seq once the Output copy completed
+  volatile uint64_t t_out;
+};
+
+struct ConvArgs {
+  int mode;         // 0: A is a 2D [M][K] matrix; 1: A is an NHWC tensor (implicit GEMM)
+  int layer;        // index into the model header
+  int n_out;        // Cout
+  int num_kb;       // K / 64
+  int cin_kb;       // Cin / 64 (mode 1)
+  int kw, stride, pad;
+  int nimg, oh, ow; // output geometry (mode 1)
+  int box_w, box_h, box_n;
+  int tiles_w, tiles_h;
+  int m_total;      // mode 0 rows
+  int relu;
+  void* out;              // bf16 NHWC / [M][Cout]
+  const void* residual;   // bf16, same shape as out, or null
+  const ActionBlock* ab;
+};
+
+}  // namespace cw

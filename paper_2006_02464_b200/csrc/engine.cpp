@@ -1,0 +1,644 @@
+#include "engine.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <ctime>
+
+namespace cw {
+
+static int64_t realtime_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_REALTIME, &ts);
+  return (int64_t)ts.tv_sec * 1000000000LL + ts.tv_nsec;
+}
+
+Engine::~Engine() { close(); }
+
+std::string Engine::open(const cw_engine_config& cfg) {
+  cfg_ = cfg;
+  if (cfg.gpu_count < 1) return "gpu_count < 1";
+  if (cfg.pages_per_gpu <= 0) return "pages_per_gpu <= 0";
+  if (cfg.mode != 0 && cfg.mode != 1) return "mode must be 0 (sim) or 1 (cuda)";
+  models_.assign(cfg.models, cfg.models + cfg.n_models);
+  for (const auto& m : models_)
+    if (m.n_batches < 1 || m.n_batches > 8) return "model with invalid batch table";
+  gpus_.resize(cfg.gpu_count);
+  for (int g = 0; g < cfg.gpu_count; ++g) {
+    GpuState& gs = gpus_[g];
+    gs.pages.total = gs.pages.free = cfg.pages_per_gpu;
+    gs.io.capacity = cfg.io_capacity;
+    if (cfg.mode == 1) {
+      const int dev = cfg.devices ? cfg.devices[g] : g;
+      gs.rt = new cw_runtime();
+      gs.rt->owned = false;
+      std::string err = gs.rt->rt.open(dev, cfg.pages_per_gpu, cfg.page_bytes, cfg.io_slots,
+                                       cfg.in_bytes_max, cfg.out_bytes_max, 0);
+      if (!err.empty()) return "gpu " + std::to_string(g) + ": " + err;
+      gs.free_pages.resize(cfg.pages_per_gpu);
+      // LIFO free list handing out low page ids first.
+      for (int64_t p = 0; p < cfg.pages_per_gpu; ++p)
+        gs.free_pages[p] = (int32_t)(cfg.pages_per_gpu - 1 - p);
+      gs.page_fence.assign(cfg.pages_per_gpu, -1);
+      gs.free_slots.resize(cfg.io_slots);
+      for (int64_t s = 0; s < cfg.io_slots; ++s) gs.free_slots[s] = (int32_t)(cfg.io_slots - 1 - s);
+    }
+  }
+  return "";
+}
+
+std::string Engine::start() {
+  if (started_) return "already started";
+  if (cfg_.mode == 1) {
+    for (int g = 0; g < (int)gpus_.size(); ++g) {
+      Runtime& rt = gpus_[g].rt->rt;
+      for (size_t m = 0; m < models_.size(); ++m) {
+        const auto& mi = models_[m];
+        if (mi.blob_id < 0) return "model " + std::to_string(m) + " has no weights blob";
+        const int bp = rt.blob_pages(mi.blob_id);
+        if (bp < 0) return "model " + std::to_string(m) + ": blob not registered";
+        if (bp > mi.pages_needed)
+          return "model " + std::to_string(m) + ": blob needs " + std::to_string(bp) +
+                 " pages but the catalog accounts " + std::to_string(mi.pages_needed);
+      }
+      std::string err = rt.build_plans();
+      if (!err.empty()) return "gpu " + std::to_string(g) + ": " + err;
+    }
+    stop_ = false;
+    thread_ = std::thread([this] { run_loop(); });
+  }
+  started_ = true;
+  return "";
+}
+
+void Engine::close() {
+  if (thread_.joinable()) {
+    stop_ = true;
+    thread_.join();
+  }
+  for (auto& g : gpus_) {
+    if (g.rt) {
+      delete g.rt;
+      g.rt = nullptr;
+    }
+  }
+  for (auto* a : owned_) delete a;
+  owned_.clear();
+  gpus_.clear();
+}
+
+int64_t Engine::now() const {
+  if (cfg_.mode == 0) return sim_now_;
+  return realtime_ns() - cfg_.epoch_ns;
+}
+
+int64_t Engine::gt_to_epoch(int g, uint64_t gt) const {
+  return (int64_t)gt - gpus_[g].rt->rt.clock_offset() - cfg_.epoch_ns;
+}
+uint64_t Engine::epoch_to_gt(int g, int64_t t) const {
+  if (t >= kNever / 2) return ~0ull;
+  const int64_t v = t + cfg_.epoch_ns + gpus_[g].rt->rt.clock_offset();
+  return v < 0 ? 0 : (uint64_t)v;
+}
+
+void Engine::call_at(int64_t t, Event ev) {
+  // SimLoop.call_at clamps to now (timebase.py:70-74); seq breaks ties FIFO.
+  const int64_t n = now();
+  ev.t = t < n ? n : t;
+  ev.seq = ++ev_seq_;
+  timers_.push(ev);
+}
+
+// ------------------------------------------------------------------ API
+
+int Engine::submit(const cw_action& a, int64_t at) {
+  if (cfg_.mode == 0) {
+    auto* copy = new cw_action(a);
+    Event ev{};
+    ev.type = EV_DELIVER;
+    ev.a = copy;
+    call_at(at, ev);
+    return 0;
+  }
+  {
+    std::lock_guard<std::mutex> lk(in_mu_);
+    inbox_.push_back(a);
+  }
+  return 0;
+}
+
+int Engine::poll(cw_result* out, int max, int64_t timeout_us) {
+  std::unique_lock<std::mutex> lk(out_mu_);
+  if (outbox_.empty() && timeout_us > 0)
+    out_cv_.wait_for(lk, std::chrono::microseconds(timeout_us), [&] { return !outbox_.empty(); });
+  int n = 0;
+  while (n < max && !outbox_.empty()) {
+    out[n++] = outbox_.front();
+    outbox_.pop_front();
+  }
+  return n;
+}
+
+int Engine::sim_run(int64_t until) {
+  if (cfg_.mode != 0) return -1;
+  // SimLoop.run_until (timebase.py:79-89).
+  int n = 0;
+  while (!timers_.empty()) {
+    Event ev = timers_.top();
+    if (ev.t > until) break;
+    timers_.pop();
+    sim_now_ = ev.t;
+    ++n;
+    switch (ev.type) {
+      case EV_DELIVER: on_action(ev.a); break;
+      case EV_WAKE: wake(ev.gpu, ev.infer_exec); break;
+      case EV_LOAD_DONE: load_done(ev.gpu, ev.a, ev.started, sim_now_, ev.dur); break;
+      case EV_EXEC_DONE: exec_done(ev.gpu, ev.a, ev.started, ev.dur); break;
+      case EV_OUTPUT_DONE: output_done(ev.gpu, ev.a, ev.started, sim_now_, ev.dur); break;
+    }
+  }
+  sim_now_ = std::max(sim_now_, until);
+  return n;
+}
+
+int Engine::pages(int g, int64_t* free, int32_t* models, int32_t* counts, int max, int32_t* n) {
+  if (g < 0 || g >= (int)gpus_.size()) return -1;
+  std::lock_guard<std::mutex> lk(state_mu_);
+  const PageCache& pc = gpus_[g].pages;
+  if (free) *free = pc.free;
+  std::vector<std::pair<uint32_t, int64_t>> v(pc.resident.begin(), pc.resident.end());
+  std::sort(v.begin(), v.end());
+  int k = 0;
+  for (auto& [m, p] : v) {
+    if (k < max) {
+      if (models) models[k] = (int32_t)m;
+      if (counts) counts[k] = (int32_t)p;
+    }
+    ++k;
+  }
+  if (n) *n = k;
+  return 0;
+}
+
+int64_t Engine::io_in_use(int g) {
+  if (g < 0 || g >= (int)gpus_.size()) return -1;
+  std::lock_guard<std::mutex> lk(state_mu_);
+  return gpus_[g].io.in_use;
+}
+
+int Engine::output(int g, int64_t ref, float* dst, int batch, int classes) {
+  if (cfg_.mode != 1 || g < 0 || g >= (int)gpus_.size() || ref < 0) return -1;
+  Runtime& rt = gpus_[g].rt->rt;
+  if ((uint64_t)ref + Runtime::kRing <= rt.exec_issued()) return -1;  // overwritten
+  const float* src = rt.output_host((uint64_t)ref);
+  const int64_t stride = (int64_t)(rt.output_stride_floats());
+  for (int j = 0; j < batch; ++j) memcpy(dst + (int64_t)j * classes, src + j * stride, classes * 4);
+  return 0;
+}
+
+// ------------------------------------------------------------------ state machine
+
+// worker.py:198-219
+void Engine::on_action(cw_action* a) {
+  owned_.insert(a);
+  const int64_t now = this->now();
+  if (a->model_id >= models_.size() || a->gpu_index < 0 || a->gpu_index >= (int)gpus_.size()) {
+    finish(a, MALFORMED_ACTION, now, now, 0);
+    return;
+  }
+  GpuState& gpu = gpus_[a->gpu_index];
+  if (a->kind == INFER) {
+    const cw_model_info& p = model(a->model_id);
+    bool ok = false;
+    for (int i = 0; i < p.n_batches; ++i) ok |= p.batch_sizes[i] == a->batch_size;
+    if (!ok) {
+      finish(a, MALFORMED_ACTION, now, now, 0);
+      return;
+    }
+    // Input stage starts immediately on receipt.
+    bool acquired = gpu.io.try_acquire(io_bytes(a));
+    if (acquired && !device_input(a->gpu_index, a)) {  // physical IOCache slots exhausted
+      gpu.io.release(io_bytes(a));
+      acquired = false;
+    }
+    if (acquired)
+      input_started(a->gpu_index, a, now);
+    else
+      gpu.io_waiting.push_back(a);
+    gpu.infer_exec.push(a);
+    try_start(a->gpu_index, true);
+  } else if (a->kind == LOAD || a->kind == UNLOAD) {
+    gpu.load_exec.push(a);
+    try_start(a->gpu_index, false);
+  } else {
+    finish(a, MALFORMED_ACTION, now, now, 0);
+  }
+}
+
+void Engine::input_started(int g, cw_action* a, int64_t now) {
+  (void)g;
+  input_done_[a->action_id] = now + (int64_t)a->batch_size * model(a->model_id).input_transfer_ns;
+}
+
+// worker.py:223-278
+void Engine::try_start(int g, bool infer) {
+  GpuState& gpu = gpus_[g];
+  Executor& ex = infer ? gpu.infer_exec : gpu.load_exec;
+  if (ex.busy) return;
+  const int64_t now = this->now();
+  while (!ex.pending.empty()) {
+    const PendingEntry top = ex.pending.top();
+    cw_action* a = top.a;
+    if (now > a->latest) {
+      ex.pending.pop();
+      reject(g, a, now);
+      continue;
+    }
+    int64_t eff = top.earliest;
+    if (a->kind == INFER) {
+      auto it = input_done_.find(a->action_id);
+      eff = std::max(eff, it == input_done_.end() ? kNever : it->second);
+    }
+    if (eff > a->latest) {
+      // Window will certainly be missed (e.g. IOCache-blocked input).
+      if (eff < kNever) {
+        ex.pending.pop();
+        reject(g, a, now);
+        continue;
+      }
+      return;
+    }
+    if (eff > now) {
+      if (ex.next_wake > eff) {
+        ex.next_wake = eff;
+        Event ev{};
+        ev.type = EV_WAKE;
+        ev.gpu = g;
+        ev.infer_exec = infer;
+        call_at(eff, ev);
+      }
+      return;
+    }
+    ex.pending.pop();
+    if (a->kind == UNLOAD) {
+      if (gpu.pages.is_resident(a->model_id) && cfg_.mode == 1) device_unload(g, a->model_id);
+      gpu.pages.release(a->model_id);
+      finish(a, SUCCESS, now, now, 0);
+      continue;
+    }
+    if (a->kind == LOAD) {
+      if (gpu.pages.is_resident(a->model_id)) {
+        gpu.pages.touch(a->model_id, now);
+        finish(a, SUCCESS, now, now, 0);
+        continue;
+      }
+      const int64_t pages = model(a->model_id).pages_needed;
+      if (!gpu.pages.reserve(a->model_id, pages)) {
+        finish(a, OUT_OF_PAGES, now, now, 0);
+        continue;
+      }
+      ex.busy = true;
+      if (cfg_.mode == 0) {
+        const int64_t dur = model(a->model_id).weights_transfer_ns;
+        Event ev{};
+        ev.type = EV_LOAD_DONE;
+        ev.gpu = g;
+        ev.a = a;
+        ev.started = now;
+        ev.dur = dur;
+        call_at(now + dur, ev);
+      } else {
+        device_load(g, a, now);
+      }
+      return;
+    }
+    // INFER
+    if (!gpu.pages.is_resident(a->model_id)) {
+      release_io(g, a);
+      finish(a, MODEL_NOT_LOADED, now, now, 0);
+      continue;
+    }
+    ex.busy = true;
+    gpu.pages.touch(a->model_id, now);
+    if (cfg_.mode == 0) {
+      const cw_model_info& p = model(a->model_id);
+      int64_t dur = 0;
+      for (int i = 0; i < p.n_batches; ++i)
+        if (p.batch_sizes[i] == a->batch_size) dur = p.exec_ns[i];
+      Event ev{};
+      ev.type = EV_EXEC_DONE;
+      ev.gpu = g;
+      ev.a = a;
+      ev.started = now;
+      ev.dur = dur;
+      call_at(now + dur, ev);
+    } else {
+      device_exec(g, a, now);
+    }
+    return;
+  }
+}
+
+// worker.py:280-282
+void Engine::wake(int g, bool infer) {
+  (infer ? gpus_[g].infer_exec : gpus_[g].load_exec).next_wake = kNever;
+  try_start(g, infer);
+}
+
+// worker.py:284-290
+void Engine::load_done(int g, cw_action* a, int64_t started, int64_t end, int64_t dur) {
+  GpuState& gpu = gpus_[g];
+  gpu.pages.commit(a->model_id, end);
+  gpu.load_exec.busy = false;
+  finish(a, SUCCESS, started, end, dur);
+  try_start(g, false);
+}
+
+// worker.py:292-299
+void Engine::exec_done(int g, cw_action* a, int64_t started, int64_t dur) {
+  GpuState& gpu = gpus_[g];
+  const int64_t now = this->now();
+  gpu.infer_exec.busy = false;
+  if (cfg_.mode == 0) {
+    const int64_t out_t = (int64_t)a->batch_size * model(a->model_id).output_transfer_ns;
+    Event ev{};
+    ev.type = EV_OUTPUT_DONE;
+    ev.gpu = g;
+    ev.a = a;
+    ev.started = started;
+    ev.dur = dur;
+    call_at(now + out_t, ev);
+  }
+  try_start(g, true);
+}
+
+// worker.py:301-305
+void Engine::output_done(int g, cw_action* a, int64_t started, int64_t end, int64_t dur) {
+  int64_t ref = -1;
+  if (cfg_.mode == 1) {
+    for (auto& e : gpus_[g].execs)
+      if (e.a == a) ref = (int64_t)e.seq;
+  }
+  release_io(g, a);
+  drain_io_waiting(g);
+  finish(a, SUCCESS, started, end, dur, ref);
+}
+
+// worker.py:313-322
+void Engine::release_io(int g, cw_action* a) {
+  GpuState& gpu = gpus_[g];
+  auto it = input_done_.find(a->action_id);
+  if (it != input_done_.end()) {
+    input_done_.erase(it);
+    gpu.io.release(io_bytes(a));
+    if (cfg_.mode == 1) device_release_slots(g, a);
+  } else {
+    auto w = std::find(gpu.io_waiting.begin(), gpu.io_waiting.end(), a);
+    if (w != gpu.io_waiting.end()) gpu.io_waiting.erase(w);
+  }
+}
+
+// worker.py:324-338
+void Engine::drain_io_waiting(int g) {
+  GpuState& gpu = gpus_[g];
+  const int64_t now = this->now();
+  bool started = false;
+  while (!gpu.io_waiting.empty()) {
+    cw_action* head = gpu.io_waiting.front();
+    if (!gpu.io.try_acquire(io_bytes(head))) break;
+    if (!device_input(g, head)) {
+      gpu.io.release(io_bytes(head));
+      break;
+    }
+    gpu.io_waiting.pop_front();
+    input_started(g, head, now);
+    started = true;
+  }
+  if (started) try_start(g, true);
+}
+
+// worker.py:340-343
+void Engine::reject(int g, cw_action* a, int64_t now) {
+  if (a->kind == INFER) release_io(g, a);
+  finish(a, REJECTED_TOO_LATE, now, now, 0);
+}
+
+// worker.py:345-351
+void Engine::finish(cw_action* a, int status, int64_t start, int64_t end, int64_t dur,
+                    int64_t output_ref) {
+  cw_result r{};
+  r.action_id = a->action_id;
+  r.status = status;
+  r.kind = a->kind;
+  r.start = start;
+  r.end = end;
+  r.device_duration = dur;
+  r.output_ref = output_ref;
+  {
+    std::lock_guard<std::mutex> lk(out_mu_);
+    outbox_.push_back(r);
+  }
+  out_cv_.notify_one();
+  // The action is referenced by no executor or queue any more.
+  owned_.erase(a);
+  delete a;
+}
+
+// ------------------------------------------------------------------ cuda device hooks
+
+bool Engine::device_input(int g, cw_action* a) {
+  if (cfg_.mode == 0) return true;
+  GpuState& gpu = gpus_[g];
+  if ((int)gpu.free_slots.size() < a->batch_size) return false;  // physical IOCache full
+  std::vector<int32_t> slots(a->batch_size);
+  for (int j = 0; j < a->batch_size; ++j) {
+    slots[j] = gpu.free_slots.back();
+    gpu.free_slots.pop_back();
+  }
+  const int arch = models_[a->model_id].arch_id;
+  std::string err = gpu.rt->rt.input_async(arch, slots.data(), a->request_ids, a->batch_size, 0,
+                                           nullptr);
+  if (!err.empty()) set_error("input: " + err);
+  gpu.action_input_seq[a->action_id] = gpu.rt->rt.last_input_seq();
+  gpu.action_slots[a->action_id] = std::move(slots);
+  return true;
+}
+
+void Engine::device_release_slots(int g, cw_action* a) {
+  GpuState& gpu = gpus_[g];
+  auto it = gpu.action_slots.find(a->action_id);
+  if (it == gpu.action_slots.end()) return;
+  for (int32_t s : it->second) gpu.free_slots.push_back(s);
+  gpu.action_slots.erase(it);
+  gpu.action_input_seq.erase(a->action_id);
+}
+
+void Engine::device_load(int g, cw_action* a, int64_t now) {
+  GpuState& gpu = gpus_[g];
+  const cw_model_info& mi = models_[a->model_id];
+  Runtime& rt = gpu.rt->rt;
+  const int n = rt.blob_pages(mi.blob_id);
+  std::vector<int32_t> pages(n);
+  int64_t fence = -1;
+  for (int i = 0; i < n; ++i) {
+    pages[i] = gpu.free_pages.back();
+    gpu.free_pages.pop_back();
+    fence = std::max(fence, gpu.page_fence[pages[i]]);
+  }
+  // Page-reuse fence: a copy must not overwrite pages an in-flight Exec still reads.
+  if (fence >= 0 && rt.exec_record((uint64_t)fence)->seq_done == (uint64_t)fence + 1) fence = -1;
+  const uint64_t tag = ++load_tag_;
+  LoadRecord* rec = nullptr;
+  std::string err = rt.load_async(mi.blob_id, pages.data(), n, fence, tag, &rec);
+  gpu.model_pages[a->model_id] = std::move(pages);
+  if (!err.empty()) {
+    set_error("load: " + err);
+    // Surface as a failed copy: free the reservation like an aborted load.
+    for (int32_t p : gpu.model_pages[a->model_id]) gpu.free_pages.push_back(p);
+    gpu.model_pages.erase(a->model_id);
+    gpu.pages.in_transit.erase(a->model_id);
+    gpu.pages.free += mi.pages_needed;
+    gpu.load_exec.busy = false;
+    finish(a, OUT_OF_PAGES, now, now, 0);
+    return;
+  }
+  gpu.loads.push_back({a, rec, tag, now});
+}
+
+void Engine::device_unload(int g, uint32_t model) {
+  GpuState& gpu = gpus_[g];
+  auto it = gpu.model_pages.find(model);
+  if (it == gpu.model_pages.end()) return;
+  auto le = gpu.model_last_exec.find(model);
+  const int64_t fence = le == gpu.model_last_exec.end() ? -1 : le->second;
+  for (int32_t p : it->second) {
+    gpu.page_fence[p] = fence;
+    gpu.free_pages.push_back(p);
+  }
+  gpu.model_pages.erase(it);
+}
+
+void Engine::device_exec(int g, cw_action* a, int64_t now) {
+  GpuState& gpu = gpus_[g];
+  const cw_model_info& mi = models_[a->model_id];
+  Runtime& rt = gpu.rt->rt;
+  const auto& slots = gpu.action_slots[a->action_id];
+  const int64_t in_seq = gpu.action_input_seq.count(a->action_id)
+                             ? gpu.action_input_seq[a->action_id]
+                             : -1;
+  uint64_t seq = 0;
+  std::string err = rt.exec_async(mi.arch_id, a->batch_size, gpu.model_pages[a->model_id][0],
+                                  slots.data(), epoch_to_gt(g, a->earliest),
+                                  epoch_to_gt(g, a->latest), in_seq, &seq);
+  if (!err.empty()) {
+    set_error("exec: " + err);
+    gpu.infer_exec.busy = false;
+    release_io(g, a);
+    finish(a, REJECTED_TOO_LATE, now, now, 0);
+    return;
+  }
+  gpu.model_last_exec[a->model_id] = (int64_t)seq;
+  gpu.execs.push_back({a, seq, now, 0, false});
+}
+
+bool Engine::poll_device() {
+  bool progressed = false;
+  for (int g = 0; g < (int)gpus_.size(); ++g) {
+    GpuState& gpu = gpus_[g];
+    Runtime& rt = gpu.rt->rt;
+    for (size_t i = 0; i < gpu.loads.size();) {
+      InflightLoad l = gpu.loads[i];
+      if (l.rec->tag_end == l.tag) {
+        gpu.loads.erase(gpu.loads.begin() + i);
+        const int64_t end = gt_to_epoch(g, l.rec->t_end);
+        const int64_t dur = (int64_t)(l.rec->t_end - l.rec->t_start);
+        load_done(g, l.a, l.started, std::max(end, l.started), dur);
+        progressed = true;
+      } else {
+        ++i;
+      }
+    }
+    for (size_t i = 0; i < gpu.execs.size();) {
+      InflightExec& e = gpu.execs[i];
+      ExecRecord* rec = rt.exec_record(e.seq);
+      if (!e.output && rec->seq_done == e.seq + 1) {
+        cw_action* a = e.a;
+        const int64_t t0 = gt_to_epoch(g, rec->t_start);
+        if (rec->rejected) {
+          gpu.execs.erase(gpu.execs.begin() + i);
+          gpu.infer_exec.busy = false;
+          reject(g, a, t0);
+          try_start(g, true);
+          progressed = true;
+          continue;
+        }
+        e.output = true;
+        e.started = t0;
+        e.dur = (int64_t)(rec->t_end - rec->t_start);
+        const int arch = models_[a->model_id].arch_id;
+        std::string err = rt.output_async(arch, e.seq, gpu.action_slots[a->action_id].data(),
+                                          a->batch_size);
+        if (!err.empty()) set_error("output: " + err);
+        const int64_t started = e.started, dur = e.dur;
+        exec_done(g, a, started, dur);  // may append to execs
+        progressed = true;
+        ++i;
+        continue;
+      }
+      if (e.output && rec->seq_out == e.seq + 1) {
+        cw_action* a = e.a;
+        const int64_t started = e.started, dur = e.dur;
+        const int64_t end = std::max(gt_to_epoch(g, rec->t_out), started);
+        output_done(g, a, started, end, dur);
+        // output_done looked the entry up by pointer; remove it now.
+        for (size_t k = 0; k < gpu.execs.size(); ++k)
+          if (gpu.execs[k].a == a) {
+            gpu.execs.erase(gpu.execs.begin() + k);
+            break;
+          }
+        progressed = true;
+        continue;
+      }
+      ++i;
+    }
+  }
+  return progressed;
+}
+
+void Engine::run_loop() {
+  std::vector<cw_action> batch;
+  int idle = 0;
+  while (!stop_) {
+    bool progressed = false;
+    {
+      std::lock_guard<std::mutex> lk(in_mu_);
+      batch.swap(inbox_);
+    }
+    std::unique_lock<std::mutex> state(state_mu_);
+    for (const cw_action& a : batch) {
+      on_action(new cw_action(a));
+      progressed = true;
+    }
+    batch.clear();
+    progressed |= poll_device();
+    while (!timers_.empty() && timers_.top().t <= now()) {
+      Event ev = timers_.top();
+      timers_.pop();
+      if (ev.type == EV_WAKE) wake(ev.gpu, ev.infer_exec);
+      progressed = true;
+    }
+    if (progressed) {
+      idle = 0;
+      continue;
+    }
+    bool busy = false;
+    for (auto& g : gpus_) busy |= !g.loads.empty() || !g.execs.empty();
+    if (!busy && (timers_.empty() || timers_.top().t - now() > 200000) && ++idle > 1000) {
+      state.unlock();
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+      state.lock();
+    }
+  }
+}
+
+}  // namespace cw

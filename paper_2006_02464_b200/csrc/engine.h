@@ -1,0 +1,207 @@
+// The worker's action executor: a restatement of the reference
+// EmulatedWorker state machine (pkg/src/sloserve/worker.py) in C++, with a
+// pluggable device.
+//
+//   sim  mode: virtual time; Load/Exec/Output take the profiled durations
+//              (worker.py:263-266, 273-277, 296-298). Used to prove the page
+//              accounting and status semantics bit-exact against the reference.
+//   cuda mode: wall time (CLOCK_REALTIME - epoch, timebase.py:45-52); LOAD is a
+//              real paged H2D copy, INFER a real CUDA-graph forward pass whose
+//              window is re-checked on the device by the gate kernel; completions
+//              are observed by polling mapped-memory records.
+//
+// The control flow (on_action, _try_start, _wake, _load_done, _exec_done,
+// _output_done, _release_io, _drain_io_waiting, _reject, _finish) follows the
+// reference function by function; each method cites the lines it restates.
+#pragma once
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <mutex>
+#include <queue>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/cw.h"
+#include "capi_util.h"
+
+namespace cw {
+
+constexpr int64_t kNever = 1LL << 62;  // worker.py:36
+enum Kind { LOAD = 1, UNLOAD = 2, INFER = 3 };
+enum Status { SUCCESS = 1, REJECTED_TOO_LATE = 2, OUT_OF_PAGES = 3, MODEL_NOT_LOADED = 4,
+              MALFORMED_ACTION = 5 };
+
+struct PageCache {  // worker.py:63-99
+  int64_t total = 0, free = 0;
+  std::unordered_map<uint32_t, int64_t> resident, in_transit, lru;
+  bool is_resident(uint32_t m) const { return resident.count(m) != 0; }
+  bool reserve(uint32_t m, int64_t pages) {
+    if (pages > free) return false;
+    free -= pages;
+    in_transit[m] = pages;
+    return true;
+  }
+  void commit(uint32_t m, int64_t now) {
+    auto it = in_transit.find(m);
+    resident[m] = it->second;
+    in_transit.erase(it);
+    lru[m] = now;
+  }
+  void touch(uint32_t m, int64_t now) { lru[m] = now; }
+  int64_t release(uint32_t m) {
+    int64_t pages = 0;
+    auto it = resident.find(m);
+    if (it != resident.end()) {
+      pages = it->second;
+      resident.erase(it);
+    }
+    free += pages;
+    lru.erase(m);
+    return pages;
+  }
+};
+
+struct IOGauge {  // worker.py:102-117
+  int64_t capacity = 0, in_use = 0;
+  bool try_acquire(int64_t n) {
+    if (in_use + n > capacity) return false;
+    in_use += n;
+    return true;
+  }
+  void release(int64_t n) { in_use -= n; }
+};
+
+struct PendingEntry {
+  int64_t earliest;
+  uint64_t seq;
+  cw_action* a;
+  bool operator>(const PendingEntry& o) const {
+    return earliest != o.earliest ? earliest > o.earliest : seq > o.seq;
+  }
+};
+
+struct Executor {  // worker.py:135-146
+  std::priority_queue<PendingEntry, std::vector<PendingEntry>, std::greater<PendingEntry>> pending;
+  bool busy = false;
+  int64_t next_wake = kNever;
+  uint64_t seq = 0;
+  void push(cw_action* a) { pending.push({a->earliest, ++seq, a}); }
+};
+
+struct InflightLoad {
+  cw_action* a;
+  LoadRecord* rec;
+  uint64_t tag;
+  int64_t started;
+};
+struct InflightExec {
+  cw_action* a;
+  uint64_t seq;
+  int64_t started;  // epoch ns (device Exec start)
+  int64_t dur;
+  bool output;      // false: waiting for Exec end; true: waiting for Output end
+};
+
+struct GpuState {
+  PageCache pages;
+  IOGauge io;
+  Executor load_exec, infer_exec;
+  std::deque<cw_action*> io_waiting;  // worker.py:157
+  // cuda device state
+  cw_runtime* rt = nullptr;
+  std::vector<int32_t> free_pages;
+  std::vector<int64_t> page_fence;  // per physical page: last exec seq that read it, -1 none
+  std::unordered_map<uint32_t, std::vector<int32_t>> model_pages;
+  std::unordered_map<uint32_t, int64_t> model_last_exec;
+  std::vector<int32_t> free_slots;
+  std::unordered_map<uint64_t, std::vector<int32_t>> action_slots;
+  std::unordered_map<uint64_t, int64_t> action_input_seq;
+  std::vector<InflightLoad> loads;
+  std::vector<InflightExec> execs;
+};
+
+enum EvType { EV_DELIVER, EV_WAKE, EV_LOAD_DONE, EV_EXEC_DONE, EV_OUTPUT_DONE };
+struct Event {
+  int64_t t;
+  uint64_t seq;
+  int type;
+  int gpu;
+  bool infer_exec;  // EV_WAKE: which executor
+  cw_action* a;
+  int64_t started, dur;
+  bool operator>(const Event& o) const { return t != o.t ? t > o.t : seq > o.seq; }
+};
+
+class Engine {
+ public:
+  ~Engine();
+  std::string open(const cw_engine_config& cfg);
+  std::string start();
+  void close();
+  cw_runtime* runtime(int g) { return g >= 0 && g < (int)gpus_.size() ? gpus_[g].rt : nullptr; }
+  int submit(const cw_action& a, int64_t at);
+  int poll(cw_result* out, int max, int64_t timeout_us);
+  int sim_run(int64_t until);
+  int64_t now() const;
+  int pages(int g, int64_t* free, int32_t* models, int32_t* counts, int max, int32_t* n);
+  int64_t io_in_use(int g);
+  int output(int g, int64_t ref, float* dst, int batch, int classes);
+
+ private:
+  // --- reference state machine (worker.py)
+  void on_action(cw_action* a);
+  void try_start(int g, bool infer);
+  void wake(int g, bool infer);
+  void load_done(int g, cw_action* a, int64_t started, int64_t end, int64_t dur);
+  void exec_done(int g, cw_action* a, int64_t started, int64_t dur);
+  void output_done(int g, cw_action* a, int64_t started, int64_t end, int64_t dur);
+  void release_io(int g, cw_action* a);
+  void drain_io_waiting(int g);
+  void reject(int g, cw_action* a, int64_t now);
+  void finish(cw_action* a, int status, int64_t start, int64_t end, int64_t dur,
+              int64_t output_ref = -1);
+  void input_started(int g, cw_action* a, int64_t now);
+  // --- device hooks (cuda)
+  bool device_input(int g, cw_action* a);
+  void device_release_slots(int g, cw_action* a);
+  void device_load(int g, cw_action* a, int64_t now);
+  void device_unload(int g, uint32_t model);
+  void device_exec(int g, cw_action* a, int64_t now);
+  bool poll_device();
+  void call_at(int64_t t, Event ev);
+  void run_loop();
+  int64_t gt_to_epoch(int g, uint64_t gt) const;
+  uint64_t epoch_to_gt(int g, int64_t t) const;
+  const cw_model_info& model(uint32_t m) const { return models_[m]; }
+  int64_t io_bytes(const cw_action* a) const {
+    const auto& p = model(a->model_id);
+    return (int64_t)a->batch_size * (p.input_size + p.output_size);
+  }
+
+  cw_engine_config cfg_{};
+  std::vector<cw_model_info> models_;
+  std::vector<GpuState> gpus_;
+  std::unordered_map<uint64_t, int64_t> input_done_;  // worker.py:177
+  std::priority_queue<Event, std::vector<Event>, std::greater<Event>> timers_;
+  uint64_t ev_seq_ = 0;
+  int64_t sim_now_ = 0;
+  uint64_t load_tag_ = 0;
+  std::unordered_set<cw_action*> owned_;  // live actions (freed at finish)
+
+  // threading (cuda)
+  std::mutex in_mu_;
+  std::vector<cw_action> inbox_;
+  std::mutex out_mu_;
+  std::condition_variable out_cv_;
+  std::deque<cw_result> outbox_;
+  std::mutex state_mu_;
+  std::thread thread_;
+  volatile bool stop_ = false;
+  bool started_ = false;
+};
+
+}  // namespace cw

@@ -1,0 +1,21 @@
+// TMA tensor-map construction (host). The driver entry point is resolved
+// through the runtime (cudaGetDriverEntryPoint) so libcw.so does not link
+// libcuda and still loads on a machine without a GPU.
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+
+namespace cw {
+
+// Resolve cuTensorMapEncodeTiled; returns false when no driver is present.
+bool tmap_init();
+
+// [rows][k] bf16 row-major matrix, box = 64 (k) x box_rows, 128B swizzle.
+bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows, uint32_t box_rows);
+
+// NHWC bf16 activation tensor, box = 64 channels x (box_w*stride) x (box_h*stride) x box_n
+// with element stride `stride` on W and H (loads box_w x box_h x box_n pixels).
+bool make_tmap_nhwc(CUtensorMap* out, const void* base, uint64_t n, uint64_t h, uint64_t w,
+                    uint64_t c, uint32_t box_w, uint32_t box_h, uint32_t box_n, uint32_t stride);
+
+}  // namespace cw

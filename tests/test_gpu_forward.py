@@ -1,0 +1,38 @@
+"""End-to-end INFER parity: the worker's CUDA-graph ResNet forward (bf16
+tcgen05 kernels, folded BN) against the CPU fp32 oracle on the same seeded
+inputs and weights. Tolerance: top-1 identical, max-abs logit error <= 0.02 *
+max|logit| (oracle.resnet_oracle.compare)."""
+
+import numpy as np
+import pytest
+
+from oracle import resnet_oracle
+from paper_2006_02464_b200 import arch
+from paper_2006_02464_b200.device import DeviceRuntime
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def r50():
+    spec = arch.build_arch("resnet50")
+    params = arch.make_params(spec, seed=0)
+    blob = arch.pack_blob(spec, arch.fold(spec, params))
+    model = resnet_oracle.torchvision_model("resnet50", params)
+    return spec, blob, model
+
+
+@pytest.mark.parametrize("batch", [1, 2, 4, 8, 16])
+def test_resnet50_logits_match_oracle(gpu, r50, batch):
+    spec, blob, model = r50
+    x = arch.make_inputs(batch, spec, first=100 * batch)
+    with DeviceRuntime(device=gpu, pages_total=8, io_slots=16) as rt:
+        rt.register_arch(0, spec)
+        rt.register_blob(0, 0, blob)
+        rt.build()
+        rt.load(0, [3, 1, 6, 0][:blob.pages])  # non-contiguous pages, header on page 3
+        got, ns = rt.infer(0, 3, x)
+    ref = resnet_oracle.logits(model, x)
+    c = resnet_oracle.compare(got, ref)
+    assert c["ok"], c
+    assert ns > 0
