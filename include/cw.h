@@ -146,6 +146,7 @@ typedef struct cw_result {
   int64_t end;
   int64_t device_duration;
   int64_t output_ref; /* cuda INFER: handle for cw_engine_output, else -1 */
+  int64_t pages_free; /* PageCache.pages_free of the action's GPU when the result was emitted */
 } cw_result;
 
 typedef struct cw_engine cw_engine;
@@ -162,6 +163,8 @@ int cw_engine_poll(cw_engine* e, cw_result* out, int max, int64_t timeout_us);
 /* sim: run the virtual-time event loop until no event is left at or before `until`. */
 int cw_engine_sim_run(cw_engine* e, int64_t until);
 int64_t cw_engine_now(cw_engine* e);
+/* sim: virtual time of the next pending event, -1 if none. */
+int64_t cw_engine_next_time(cw_engine* e);
 /* Page accounting of one GPU (PageCache, worker.py:63-99). resident: (model, pages) pairs. */
 int cw_engine_pages(cw_engine* e, int gpu_index, int64_t* pages_free, int32_t* resident_models,
                     int32_t* resident_pages, int max_resident, int32_t* n_resident);

@@ -59,7 +59,7 @@ class cw_result(C.Structure):
     _fields_ = [
         ("action_id", C.c_uint64), ("status", C.c_int32), ("kind", C.c_int32),
         ("start", C.c_int64), ("end", C.c_int64), ("device_duration", C.c_int64),
-        ("output_ref", C.c_int64)]
+        ("output_ref", C.c_int64), ("pages_free", C.c_int64)]
 
 
 # (name, restype, argtypes) for every symbol include/cw.h declares.
@@ -94,6 +94,7 @@ SIGNATURES = [
     ("cw_engine_poll", C.c_int, [_P, C.POINTER(cw_result), C.c_int, C.c_int64]),
     ("cw_engine_sim_run", C.c_int, [_P, C.c_int64]),
     ("cw_engine_now", C.c_int64, [_P]),
+    ("cw_engine_next_time", C.c_int64, [_P]),
     ("cw_engine_pages", C.c_int, [_P, C.c_int, _I64P, _I32P, _I32P, C.c_int, _I32P]),
     ("cw_engine_io_in_use", C.c_int64, [_P, C.c_int]),
     ("cw_engine_output", C.c_int, [_P, C.c_int, C.c_int64, _P, C.c_int, C.c_int]),

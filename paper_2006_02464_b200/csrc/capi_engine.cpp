@@ -27,7 +27,7 @@ int cw_engine_start(cw_engine* e) { return cw::check(e->e.start()); }
 void cw_engine_close(cw_engine* e) { delete e; }
 
 int cw_engine_submit(cw_engine* e, const cw_action* a, int64_t at) {
-  if (a->batch_size < 0 || a->batch_size > CW_MAX_BATCH) return cw::fail("batch size out of range");
+  if (a->batch_size < 0) return cw::fail("negative batch size");
   return e->e.submit(*a, at);
 }
 
@@ -38,6 +38,8 @@ int cw_engine_poll(cw_engine* e, cw_result* out, int max, int64_t timeout_us) {
 int cw_engine_sim_run(cw_engine* e, int64_t until) { return e->e.sim_run(until); }
 
 int64_t cw_engine_now(cw_engine* e) { return e->e.now(); }
+
+int64_t cw_engine_next_time(cw_engine* e) { return e->e.next_event_time(); }
 
 int cw_engine_pages(cw_engine* e, int gpu_index, int64_t* pages_free, int32_t* resident_models,
                     int32_t* resident_pages, int max_resident, int32_t* n_resident) {

@@ -434,6 +434,9 @@ void Engine::finish(cw_action* a, int status, int64_t start, int64_t end, int64_
   r.end = end;
   r.device_duration = dur;
   r.output_ref = output_ref;
+  r.pages_free = (a->gpu_index >= 0 && a->gpu_index < (int)gpus_.size())
+                     ? gpus_[a->gpu_index].pages.free
+                     : -1;
   {
     std::lock_guard<std::mutex> lk(out_mu_);
     outbox_.push_back(r);

@@ -1,0 +1,128 @@
+"""Wire codec: byte equality with frames encoded by the reference
+(tests/golden/wire_frames.json), decode round trips, malformed-frame errors,
+and a 1e5-message fuzz round trip (SPEC.md:571 acceptance 9)."""
+
+import json
+import os
+import random
+import socket
+import threading
+
+import pytest
+
+from paper_2006_02464_b200 import wire
+from paper_2006_02464_b200.wire import (Action, ActionKind, ActionResult, InferenceRequest,
+                                        InferenceResponse, ResponseStatus, ResultStatus,
+                                        WorkerHandshake)
+
+FRAMES = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "wire_frames.json")))
+
+
+def _build(f):
+    t = f["type"]
+    if t == "action":
+        return Action(f["action_id"], ActionKind(f["kind"]), f["model_id"], f["earliest"],
+                      f["latest"], tuple(f["batch"]), f["gpu_index"], f["expected_duration"])
+    if t == "result":
+        return ActionResult(f["action_id"], ResultStatus(f["status"]), f["start"], f["end"],
+                            f["device_duration"])
+    if t == "request":
+        return InferenceRequest(f["request_id"], f["model_id"], f["slo"], f["arrival"],
+                                f["input_size"], bytes.fromhex(f["payload"]))
+    if t == "response":
+        return InferenceResponse(f["request_id"], ResponseStatus(f["status"]), f["latency"],
+                                 f["cold_start"])
+    return WorkerHandshake(f["worker_id"], f["gpu_count"], f["pages_total"], tuple(f["models"]))
+
+
+@pytest.mark.parametrize("i", range(len(FRAMES)))
+def test_encode_matches_reference_bytes(i):
+    f = FRAMES[i]
+    msg = _build(f["fields"])
+    assert wire.encode(msg).hex() == f["hex"]
+    assert wire.decode(bytes.fromhex(f["hex"])) == msg
+
+
+def test_spec_known_answer_sizes():
+    assert len(wire.encode(Action(0, ActionKind.UNLOAD, 0, 0, 0))) == 38
+    assert len(wire.encode(Action(1, ActionKind.INFER, 0, 0, 1, tuple(range(16))))) == 174
+    assert len(wire.encode(ActionResult(1, ResultStatus.SUCCESS, 0, 1, 1))) == 38
+    assert len(wire.encode(WorkerHandshake(0, 1, 10, (1, 2, 3)))) == 37
+
+
+def test_decode_errors():
+    ok = wire.encode(Action(5, ActionKind.INFER, 1, 0, 10, (1, 2)))
+    with pytest.raises(wire.Truncated):
+        wire.decode(ok[:-1])
+    with pytest.raises(wire.Invalid):
+        wire.decode(ok + b"\x00")
+    with pytest.raises(wire.BadTag):
+        wire.decode(b"\x01\x00\x00\x00\xff")
+    bad = bytearray(ok)
+    bad[4 + 1 + 8] = 9  # kind byte
+    with pytest.raises(wire.Invalid):
+        wire.decode(bytes(bad))
+    load = bytearray(wire.encode(Action(5, ActionKind.LOAD, 1, 0, 0)))
+    load[20:28] = (5).to_bytes(8, "little", signed=True)   # earliest > latest
+    with pytest.raises(wire.Invalid):
+        wire.decode(bytes(load))
+    with pytest.raises(wire.Invalid):
+        wire.decode(b"\x00\x00\x00\x05" + b"\x00" * 4)   # over the 64 MiB cap
+
+
+def _random_msg(rng):
+    k = rng.randrange(5)
+    if k == 0:
+        kind = ActionKind(rng.randint(1, 3))
+        e = rng.randrange(-2**62, 2**62)
+        batch = tuple(rng.randrange(2**64) for _ in range(rng.randint(1, 20))) \
+            if kind == ActionKind.INFER else ()
+        return Action(rng.randrange(2**64), kind, rng.randrange(2**32), e,
+                      e + rng.randrange(2**20), batch, rng.randrange(2**16),
+                      rng.randrange(2**62) if kind == ActionKind.INFER else 0)
+    if k == 1:
+        st = ResultStatus(rng.randint(1, 5))
+        s = rng.randrange(-2**62, 2**62)
+        return ActionResult(rng.randrange(2**64), st, s, s + rng.randrange(2**20),
+                            rng.randrange(2**62) if st == 1 else 0)
+    if k == 2:
+        return InferenceRequest(rng.randrange(2**64), rng.randrange(2**32), rng.randrange(1, 2**62),
+                                rng.randrange(2**62), rng.randrange(2**63),
+                                rng.randbytes(rng.randint(0, 64)))
+    if k == 3:
+        return InferenceResponse(rng.randrange(2**64), ResponseStatus(rng.randint(1, 3)),
+                                 rng.randrange(-2**62, 2**62), bool(rng.getrandbits(1)))
+    return WorkerHandshake(rng.randrange(2**32), rng.randint(1, 2**31), rng.randrange(1, 2**63),
+                           tuple(rng.randrange(2**32) for _ in range(rng.randint(0, 30))))
+
+
+def test_fuzz_round_trip_1e5():
+    rng = random.Random(11)
+    dec = wire.Decoder()
+    stream = bytearray()
+    msgs = []
+    for _ in range(100_000):
+        m = _random_msg(rng)
+        b = wire.encode(m)
+        assert wire.decode(b) == m
+        msgs.append(m)
+        stream += b
+    # Incremental decoding over arbitrary chunk boundaries.
+    out = []
+    pos = 0
+    while pos < len(stream):
+        n = rng.randint(1, 4096)
+        out += dec.feed(bytes(stream[pos:pos + n]))
+        pos += n
+    assert out == msgs and not dec.buf
+
+
+def test_socket_send_recv():
+    a, b = socket.socketpair()
+    msgs = [Action(1, ActionKind.LOAD, 3, 0, 9), ActionResult(1, ResultStatus.SUCCESS, 0, 9, 9)]
+    t = threading.Thread(target=lambda: [wire.send(a, m) for m in msgs] and a.close())
+    t.start()
+    got = [wire.recv(b), wire.recv(b)]
+    t.join()
+    assert got == msgs
+    assert wire.recv(b) is None
