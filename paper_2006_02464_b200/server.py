@@ -1,0 +1,114 @@
+"""TCP worker server: the process entry the reference controller connects to.
+
+Same contract as `run_worker_server` (pkg/src/sloserve/harness.py:525-575):
+accept one controller connection, send the WorkerHandshake first, then read
+Action frames and write ActionResult frames (lock-guarded), and flush a
+telemetry CSV on EOF. Differences: the worker id is configurable (the
+reference hard-codes 0, harness.py:550, so two external workers collide in
+the controller), and the worker is the B200Worker (cuda by default).
+"""
+
+from __future__ import annotations
+
+import csv
+import os
+import socket
+import threading
+import time
+
+from . import wire
+from .timebase import WallClock, WallLoop
+from .worker import DEFAULT_IO_CAPACITY, B200Worker
+
+TELEMETRY_HEADER = ["action_id", "kind", "model_id", "gpu", "batch_size", "status", "start_ns",
+                    "end_ns", "device_duration_ns"]
+
+
+class _EpochOnly:
+    """Loop stand-in for the cuda worker: it only needs the shared epoch."""
+
+    def __init__(self, clock: WallClock):
+        self.clock = clock
+
+    def now(self) -> int:
+        return self.clock.now()
+
+
+def serve(listen: str, catalog, gpu_count: int = 1, pages_per_gpu: int = 500, jitter=None,
+          seed: int = 0, epoch_ns: int | None = None, telemetry_path: str = "",
+          io_capacity: int = DEFAULT_IO_CAPACITY, ready_fd: int | None = None, *,
+          worker_id: int = 0, devices=None, mode: str = "cuda", weights_seed: int = 0,
+          on_ready=None) -> None:
+    host, port = listen.rsplit(":", 1)
+    lsock = socket.socket()
+    lsock.setsockopt(socket.SOL_SOCKET, socket.SO_REUSEADDR, 1)
+    lsock.bind((host, int(port)))
+    lsock.listen(1)
+    bound = lsock.getsockname()[1]
+    clock = WallClock(epoch_ns)
+    loop = _EpochOnly(clock) if mode == "cuda" else WallLoop(clock, name="worker").start()
+    wlock = threading.Lock()
+    conn_box: dict = {}
+    pending = {"n": 0}
+    done = threading.Condition()
+
+    def send_result(result):
+        with wlock:
+            c = conn_box.get("conn")
+            if c is not None:
+                try:
+                    wire.send(c, result)
+                except OSError:
+                    pass
+        with done:
+            pending["n"] -= 1
+            done.notify_all()
+
+    # Build the worker (weights, graphs) before announcing readiness.
+    worker = B200Worker(worker_id, catalog, loop, send_result, gpu_count=gpu_count,
+                        pages_per_gpu=pages_per_gpu, io_capacity=io_capacity, jitter=jitter,
+                        seed=seed, keep_records=bool(telemetry_path), mode=mode, devices=devices,
+                        weights_seed=weights_seed, epoch_ns=clock.epoch_ns)
+    if ready_fd is not None:
+        os.write(ready_fd, f"{bound}\n".encode())
+        os.close(ready_fd)
+    if on_ready is not None:
+        on_ready(bound)
+    conn, _ = lsock.accept()
+    conn.setsockopt(socket.IPPROTO_TCP, socket.TCP_NODELAY, 1)
+    with wlock:
+        conn_box["conn"] = conn
+        wire.send(conn, worker.handshake())
+    try:
+        while True:
+            try:
+                msg = wire.recv(conn)
+            except OSError:
+                break
+            if msg is None:
+                break
+            with done:
+                pending["n"] += 1
+            if mode == "cuda":
+                worker.on_action(msg)
+            else:
+                loop.call_soon(worker.on_action, msg)
+    finally:
+        deadline = time.monotonic() + 2.0
+        with done:
+            while pending["n"] > 0 and time.monotonic() < deadline:
+                done.wait(timeout=0.05)
+        with wlock:
+            conn_box["conn"] = None
+        conn.close()
+        lsock.close()
+        if mode != "cuda":
+            loop.stop(join=False)
+        worker.close()
+    if telemetry_path:
+        with open(telemetry_path, "w", newline="") as f:
+            w = csv.writer(f)
+            w.writerow(TELEMETRY_HEADER)
+            for r in worker.records:
+                w.writerow([r.action_id, r.kind, r.model_id, r.gpu_index, r.batch_size, r.status,
+                            r.start, r.end, r.device_duration])
