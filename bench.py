@@ -1,0 +1,569 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Clockwork worker (BASELINE.json configs[1]):
+
+  single B200 worker, LOAD / INFER / UNLOAD over 1000 ResNet-50 copies in the
+  16 MiB-paged weight cache (cold-start heavy), 100 ms SLO.
+
+One step = one INFER action of batch 16 (16 requests) on the copy the step's
+seeded schedule picks (uniform over the 1000 copies).
+
+  value  device-resident leg: the per-(arch, batch) CUDA graph replayed back to
+         back on the Exec stream, weights of all 1000 copies resident in
+         distinct HBM pages (so every step streams its copy's weights from HBM),
+         request inputs already in the IOCache; CUDA-event time on the Exec
+         stream; closed loop (one batch in flight), every step's requests are
+         within the SLO if its Exec time is <= 100 ms.
+  e2e    the same workload through the worker's public API
+         (B200Worker.on_action, the drop-in for the reference EmulatedWorker):
+         pages_per_gpu=500 so only 125 copies fit; a cold copy costs an UNLOAD
+         of the LRU victim and a LOAD (pinned H2D of the 54 MB paged blob);
+         every INFER copies its 16 inputs H2D (pinned) and its logits D2H.
+         Goodput = requests whose (result.end - arrival) <= 100 ms, / wall time.
+
+`python bench.py --impl reference` times the reference path on the host CPU:
+the reference worker computes nothing (worker.py:1-9), so its CPU path is the
+oracle port (oracle/): the same cold-start schedule with LOAD = memcpy of the
+blob into a host page pool and INFER = the fp32 torchvision forward on all
+host cores, at the largest batch whose latency meets the SLO.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+SLO_NS = 100_000_000
+METRIC = "goodput req/s within 100ms SLO; INFER images/s and p99.99/p50 per batch"
+WORKLOAD = "resnet50 x1000 copies, 16MiB-paged weight cache, LOAD/INFER/UNLOAD, b=16, SLO 100ms"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--copies", type=int, default=1000)
+    ap.add_argument("--pages", type=int, default=500)
+    ap.add_argument("--sweep-samples", type=int, default=10000)
+    ap.add_argument("--clients", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- distributed
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend)
+            self.dist = dist
+            self.torch = torch
+            self.backend = backend
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([float(v)], dtype=self.torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor([float(v)], dtype=self.torch.float64, device=dev)
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        busy = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- helpers
+
+def peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p["bf16_tflops_sustained"], p["hbm_gbs"], "measured"
+    except (OSError, KeyError, ValueError):
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def schedule(n: int, copies: int, seed: int) -> np.ndarray:
+    return np.random.default_rng(seed).integers(0, copies, n)
+
+
+def pct(a, q):
+    return float(np.percentile(np.asarray(a, dtype=np.float64), q))
+
+
+def b200_catalog(copies: int, blob_bytes: int):
+    from paper_2006_02464_b200 import catalog
+    text = f"""page_bytes 16777216
+model resnet50
+weights_bytes {blob_bytes}
+weights_transfer_ns 1200000
+io_ns 12000 2000
+io_bytes 602112 4000
+batch 1 500000
+batch 2 530000
+batch 4 600000
+batch 8 750000
+batch 16 1100000
+replicas resnet50 {copies - 1}
+"""
+    return catalog.parse(text)
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args, d: Dist) -> dict | None:
+    from paper_2006_02464_b200 import arch
+    from paper_2006_02464_b200.device import DeviceRuntime
+
+    dev = d.local
+    spec = arch.build_arch("resnet50")
+    params = arch.make_params(spec, seed=0)
+    blob = arch.pack_blob(spec, arch.fold(spec, params))
+    b = args.batch
+    bf16_peak, bf16_sus, hbm_peak, peak_kind = peaks()
+    out: dict = {}
+
+    # ---------------- value: device-resident leg
+    copies = args.copies
+    with DeviceRuntime(device=dev, pages_total=copies * blob.pages, io_slots=16) as rt:
+        rt.register_arch(0, spec)
+        rt.register_blob(0, 0, blob)
+        rt.build()
+        load_ns = [rt.load(0, list(range(c * blob.pages, (c + 1) * blob.pages)))
+                   for c in range(copies)]
+        rt.infer(0, 0, arch.make_inputs(16, spec))
+        launches, _ = rt.plan_info(0, b)
+        sched = schedule(args.warmup + args.steps, copies, 1 + d.rank)
+        hdr = [int(c) * blob.pages for c in sched]
+        rt.exec_many(0, b, hdr[:args.warmup])
+        d.barrier()
+        with ClockSampler(dev) as clk:
+            d.barrier()
+            ex, wall = rt.exec_many(0, b, hdr[args.warmup:])
+            d.barrier()
+        t_max = d.max(wall)
+        reqs = d.sum(b * int((ex <= SLO_NS).sum()))
+        out["value"] = reqs / (t_max / 1e9)
+        out["ms_per_step"] = t_max / 1e6 / args.steps
+        out["clocks"] = clk.summary()
+        out["gpu_launches"] = launches * args.steps
+        out["exec_p50_us"] = pct(ex, 50) / 1e3
+        out["load_copy_ms_p50"] = pct(load_ns, 50) / 1e6
+        out["load_gbs"] = blob.data.nbytes / (pct(load_ns, 50) / 1e9) / 1e9
+
+        # ---------------- per-batch INFER sweep (device Exec time, %globaltimer)
+        sweep = {}
+        for bb in (1, 2, 4, 8, 16):
+            n = args.sweep_samples
+            hp = [int(c) * blob.pages for c in schedule(n + 50, copies, 100 + bb)]
+            rt.exec_many(0, bb, hp[:50])
+            ex_b, wall_b = rt.exec_many(0, bb, hp[50:])
+            p50 = pct(ex_b, 50)
+            sweep[str(bb)] = {
+                "img_s": bb * n / (wall_b / 1e9), "p50_us": p50 / 1e3,
+                "p99_us": pct(ex_b, 99) / 1e3, "p9999_us": pct(ex_b, 99.99) / 1e3,
+                "max_us": float(ex_b.max()) / 1e3, "p9999_over_p50": pct(ex_b, 99.99) / p50,
+                "n": n, "roofline_us": max(spec.flops_per_image * bb / (bf16_peak * 1e12),
+                                           (blob.data.nbytes + bb * 606112) / (hbm_peak * 1e9)) * 1e6}
+        out["infer"] = sweep
+
+        # ---------------- roofline of the dominant kernel (tcgen05 conv), live
+        reps = []
+        for r in range(5):
+            ms, kinds = rt.profile_ops(0, b, int(sched[r]) * blob.pages)
+            reps.append(ms)
+        ms = np.median(np.stack(reps), axis=0)
+        conv = kinds == arch.OP_CONV
+        conv_s = float(ms[conv].sum()) / 1e3
+        conv_flops = sum(2 * op["out_h"] * op["out_w"] * op["cout"] *
+                         (147 if op["layer"] == 0 else op["kh"] * op["kw"] * op["cin"])
+                         for op in spec.ops if op["kind"] == arch.OP_CONV) * b
+        achieved = conv_flops / conv_s / 1e12
+        out["roofline"] = {
+            "bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
+            "frac": achieved / bf16_peak, "traffic": None,
+            "kernel": "conv_tc_kernel (tcgen05 implicit-GEMM conv)",
+            "launches_per_infer": int(conv.sum()),
+            "flops_per_launch_avg": conv_flops / int(conv.sum()),
+            "kernel_share_of_exec": conv_s / (float(ms.sum()) / 1e3),
+            "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst, {peak_kind})",
+            "op_ms": [round(float(x), 4) for x in ms]}
+
+    # ---------------- e2e: through the worker's public API
+    out["e2e"] = run_e2e(args, d, spec, blob)
+
+    # ---------------- cpu baseline (oracle port, rank 0, bounded sample)
+    if d.rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(spec, params, budget_s=15.0)
+    return out
+
+
+def run_e2e(args, d: Dist, spec, blob) -> dict:
+    from paper_2006_02464_b200.wire import Action, ActionKind
+    from paper_2006_02464_b200.worker import B200Worker
+
+    cat = b200_catalog(args.copies, blob.data.nbytes)
+    pages_per_model = cat.pages_needed(0)
+    b = args.batch
+    lock = threading.Lock()
+    waiters: dict[int, tuple] = {}
+
+    def send_result(r):
+        with lock:
+            ev = waiters.pop(r.action_id, None)
+        if ev is not None:
+            ev[1].append(r)
+            ev[0].set()
+
+    w = B200Worker(0, cat, None, send_result, pages_per_gpu=args.pages, mode="cuda",
+                   devices=[d.local], epoch_ns=time.time_ns())
+    ids = iter(range(1, 1 << 62))
+
+    def call(kind, model, batch=(), window_ns=1_000_000_000):
+        aid = next(ids)
+        ev = (threading.Event(), [])
+        with lock:
+            waiters[aid] = ev
+        now = time.time_ns() - w.epoch_ns
+        w.on_action(Action(aid, kind, model, now, now + window_ns, tuple(batch), 0))
+        ev[0].wait()
+        return ev[1][0]
+
+    # Driver-side page mirror (what the controller tracks, controller_state.py:74-142).
+    resident: dict[int, int] = {}          # model -> last use
+    pins: dict[int, int] = {}
+    loading: dict[int, threading.Event] = {}
+    free = [args.pages]
+    stats = {"loads": 0, "cold": 0, "ok": 0, "reqs": 0, "lat": [], "not_loaded": 0,
+             "loaded_bytes": 0}
+    mlock = threading.Lock()
+    sched = schedule(args.warmup + args.steps, args.copies, 7 + d.rank)
+    cursor = [0]
+
+    def ensure(m):
+        waited = False
+        while True:
+            with mlock:
+                if m in resident:
+                    resident[m] = time.monotonic_ns()
+                    pins[m] = pins.get(m, 0) + 1
+                    return waited
+                ev = loading.get(m)
+                if ev is None:
+                    ev = loading[m] = threading.Event()
+                    victims = []
+                    while free[0] < pages_per_model:
+                        cands = [x for x in resident if pins.get(x, 0) == 0]
+                        if not cands:
+                            break
+                        v = min(cands, key=resident.get)
+                        del resident[v]
+                        free[0] += pages_per_model
+                        victims.append(v)
+                    free[0] -= pages_per_model
+                    owner = True
+                else:
+                    owner = False
+            if not owner:
+                ev.wait()
+                waited = True
+                continue
+            for v in victims:
+                call(ActionKind.UNLOAD, int(v))
+            r = call(ActionKind.LOAD, int(m))
+            with mlock:
+                if int(r.status) == 1:
+                    resident[m] = time.monotonic_ns()
+                    stats["loads"] += 1
+                    stats["loaded_bytes"] += blob.data.nbytes
+                else:
+                    free[0] += pages_per_model
+                del loading[m]
+            ev.set()
+            if int(r.status) != 1:
+                raise RuntimeError(f"LOAD failed with status {int(r.status)}")
+            waited = True
+
+    def client(timed_steps, record):
+        while True:
+            with mlock:
+                i = cursor[0]
+                if i >= timed_steps:
+                    return
+                cursor[0] += 1
+            m = int(sched[i % len(sched)])
+            arrival = time.time_ns() - w.epoch_ns
+            cold = ensure(m)
+            r = call(ActionKind.INFER, m, batch=[i * b + j for j in range(b)])
+            with mlock:
+                pins[m] -= 1
+                if record:
+                    stats["reqs"] += b
+                    stats["cold"] += int(cold)
+                    if int(r.status) == 1:
+                        lat = r.end - arrival
+                        stats["lat"].append(lat)
+                        stats["ok"] += b if lat <= SLO_NS else 0
+                    else:
+                        stats["not_loaded"] += 1
+
+    def run(n, record):
+        cursor[0] = 0
+        ts = [threading.Thread(target=client, args=(n, record)) for _ in range(args.clients)]
+        t0 = time.perf_counter()
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return time.perf_counter() - t0
+
+    run(max(args.warmup, 1), False)
+    for k in ("loads", "loaded_bytes"):
+        stats[k] = 0
+    sched = schedule(args.steps, args.copies, 11 + d.rank)
+    d.barrier()
+    dt = run(args.steps, True)
+    d.barrier()
+    t_max = d.max(dt)
+    ok = d.sum(stats["ok"])
+    w.close()
+    lat = stats["lat"] or [0]
+    return {
+        "value": ok / t_max, "unit": "req/s",
+        "h2d_bytes_per_step": int(b * 602112 + stats["loaded_bytes"] / max(args.steps, 1)),
+        "d2h_bytes_per_step": int(b * 4000),
+        "cold_start_fraction": stats["cold"] / max(args.steps, 1),
+        "loads": stats["loads"], "failed_infers": stats["not_loaded"],
+        "latency_p50_ms": pct(lat, 50) / 1e6, "latency_p99_ms": pct(lat, 99) / 1e6,
+        "clients": args.clients, "pages_per_gpu": args.pages, "copies": args.copies,
+        "satisfaction": stats["ok"] / max(stats["reqs"], 1),
+    }
+
+
+def cpu_baseline(spec, params, budget_s: float) -> dict:
+    import torch
+
+    from oracle import resnet_oracle
+    from paper_2006_02464_b200 import arch
+
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    model = resnet_oracle.torchvision_model("resnet50", params)
+    x = arch.make_inputs(16, spec)
+    resnet_oracle.logits(model, x[:2])
+    n, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s or n < 2:
+        resnet_oracle.logits(model, x)
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": 16 * n / dt, "unit": "req/s", "cores": cores, "kind": "port",
+            "sample": f"{n} INFERs of batch 16 through the fp32 CPU oracle "
+                      f"(torchvision resnet50, {cores} threads), {dt:.1f} s; "
+                      f"per-batch latency {dt / n * 1e3:.0f} ms (> SLO at b=16)"}
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def run_reference(args) -> dict:
+    """CPU path of the reference worker (oracle port): cold-start schedule with
+    LOAD = memcpy into a host page pool and INFER = fp32 torchvision forward."""
+    import torch
+
+    from oracle import resnet_oracle
+    from paper_2006_02464_b200 import arch
+
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    spec = arch.build_arch("resnet50")
+    params = arch.make_params(spec, seed=0)
+    blob = arch.pack_blob(spec, arch.fold(spec, params))
+    model = resnet_oracle.torchvision_model("resnet50", params)
+    x = arch.make_inputs(16, spec)
+    # Largest batch whose CPU latency meets the SLO (what a Clockwork controller would pick).
+    batch, lat_by_b = 1, {}
+    for bb in (1, 2, 4, 8, 16):
+        resnet_oracle.logits(model, x[:bb])
+        t0 = time.perf_counter()
+        resnet_oracle.logits(model, x[:bb])
+        lat_by_b[bb] = time.perf_counter() - t0
+        if lat_by_b[bb] * 1e9 <= SLO_NS * 0.8:
+            batch = bb
+        else:
+            break
+    # Bound the run to ~2 minutes of CPU work.
+    per_step = lat_by_b[batch] + 0.01
+    steps = max(3, min(args.steps, int(120 / per_step)))
+    warm = min(args.warmup, 3)
+    pages_per_model = blob.pages
+    resident_cap = max(1, args.pages // pages_per_model)
+    pool = np.zeros((resident_cap, blob.data.nbytes), np.uint8)
+    slot_of: dict[int, int] = {}
+    lru: dict[int, int] = {}
+    sched = schedule(warm + steps, args.copies, 7)
+    ok = reqs = cold = 0
+    t_start = None
+    for i, m in enumerate(sched):
+        if i == warm:
+            t_start = time.perf_counter()
+            ok = reqs = cold = 0
+        m = int(m)
+        t0 = time.perf_counter()
+        if m not in slot_of:
+            cold += 1
+            if len(slot_of) >= resident_cap:
+                v = min(lru, key=lru.get)
+                slot = slot_of.pop(v)
+                del lru[v]
+            else:
+                slot = len(slot_of)
+            pool[slot, :] = blob.data     # LOAD: copy the paged blob
+            slot_of[m] = slot
+        lru[m] = i
+        resnet_oracle.logits(model, x[:batch])
+        lat = (time.perf_counter() - t0) * 1e9
+        reqs += batch
+        ok += batch if lat <= SLO_NS else 0
+    dt = time.perf_counter() - t_start
+    value = ok / dt
+    return {
+        "metric": METRIC, "value": value, "unit": "req/s", "n_gpus": args.gpus, "steps": steps,
+        "warmup": warm, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": WORKLOAD, "batch": batch, "copies": args.copies,
+                   "pages_per_gpu": args.pages, "parallelism": "replicas"},
+        "cpu_baseline": {"value": value, "unit": "req/s", "cores": cores, "kind": "port",
+                         "sample": f"{steps} steps of the cold-start schedule at batch {batch} "
+                                   f"(largest batch meeting the SLO on {cores} cores; "
+                                   f"latency by batch {json.dumps({k: round(v * 1e3, 1) for k, v in lat_by_b.items()})} ms), "
+                                   f"cold fraction {cold / steps:.2f}"},
+        "e2e": {"value": value, "unit": "req/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+# ----------------------------------------------------------------------------- main
+
+def main():
+    args = parse_args()
+    d = Dist()
+    if args.impl == "reference":
+        if d.rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        d.close()
+        return
+    res = run_ours(args, d)
+    if d.rank == 0:
+        line = {
+            "metric": METRIC, "value": res["value"], "unit": "req/s", "n_gpus": d.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (N(0,1) 3x224x224 inputs, random-init ResNet-50 weights)",
+            "config": {"workload": WORKLOAD, "batch": args.batch, "copies": args.copies,
+                       "pages_per_gpu_e2e": args.pages, "parallelism": "replicas (one worker per GPU)",
+                       "l2": "inputs larger than L2: 1000 copies x 54 MB weights rotate per step"},
+            "clocks": res["clocks"], "gpu_launches": res["gpu_launches"],
+            "e2e": res["e2e"], "roofline": res["roofline"], "infer": res["infer"],
+            "load": {"copy_ms_p50": res["load_copy_ms_p50"], "gbs": res["load_gbs"]},
+            "exec_p50_us": res["exec_p50_us"],
+        }
+        if "cpu_baseline" in res:
+            line["cpu_baseline"] = res["cpu_baseline"]
+        print(json.dumps(line), flush=True)
+    d.close()
+
+
+if __name__ == "__main__":
+    main()

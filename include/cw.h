@@ -89,6 +89,10 @@ int cw_rt_infer_sync(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page,
  * %globaltimer) into exec_ns[i]; *wall_ns = CUDA-event time of all n on the Exec stream. */
 int cw_rt_exec_many(cw_runtime* rt, int arch_id, int batch, const int32_t* hdr_pages, int n,
                     int64_t* exec_ns, int64_t* wall_ns);
+/* Eager run of the (arch, batch) op list with CUDA events between launches on the
+ * Exec stream (per-op milliseconds, for the roofline); returns the op count. */
+int cw_rt_profile_ops(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page, float* op_ms,
+                      int32_t* op_kinds, int max_ops);
 /* Copy to/from a workspace activation buffer (parity tests of single layers). */
 int cw_rt_buffer_io(cw_runtime* rt, int arch_id, int buf, void* host, int64_t bytes,
                     int to_device);

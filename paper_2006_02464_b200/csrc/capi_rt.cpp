@@ -185,5 +185,19 @@ int cw_rt_exec_window(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page, 
   return 1;
 }
 
+int cw_rt_profile_ops(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page, float* op_ms,
+                      int32_t* op_kinds, int max_ops) {
+  std::vector<float> ms;
+  std::vector<int> kinds;
+  std::string err = rt->rt.profile_ops(arch_id, batch, hdr_page, &ms, &kinds);
+  if (!err.empty()) return cw::fail(err);
+  const int n = (int)ms.size();
+  for (int i = 0; i < n && i < max_ops; ++i) {
+    op_ms[i] = ms[i];
+    op_kinds[i] = kinds[i];
+  }
+  return n;
+}
+
 }  // extern "C"
 

@@ -476,6 +476,50 @@ std::string Runtime::output_async(int arch, uint64_t seq, const int32_t* slots, 
   return "";
 }
 
+std::string Runtime::profile_ops(int arch, int batch, int32_t hdr_page, std::vector<float>* ms,
+                                 std::vector<int>* kinds) {
+  CW_TRY(cudaSetDevice(device_));
+  auto it = archs_.find(arch);
+  if (it == archs_.end()) return "unknown arch";
+  auto pit = it->second.plans.find(batch);
+  if (pit == it->second.plans.end()) return "no plan for batch size";
+  const Plan& p = pit->second;
+  const uint64_t seq = exec_seq_;
+  ActionDesc& d = ring_[seq & (kRing - 1)];
+  d.seq = seq;
+  d.earliest_gt = 0;
+  d.latest_gt = ~0ull;
+  d.hdr = page_ptr(hdr_page);
+  for (int j = 0; j < kMaxBatch; ++j) {
+    d.in[j] = j < batch ? slot_in(j) : nullptr;
+    d.out[j] = j < batch ? slot_out(j) : nullptr;
+  }
+  d.batch = batch;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  std::vector<cudaEvent_t> ev(p.ops.size() + 1);
+  for (auto& e : ev) CW_TRY(cudaEventCreate(&e));
+  launch_gate(ab_, ring_, kRing - 1, ctr_, exec_recs_, s_exec_);
+  CW_TRY(cudaEventRecord(ev[0], s_exec_));
+  for (size_t i = 0; i < p.ops.size(); ++i) {
+    Plan one;
+    one.ops.push_back(p.ops[i]);
+    std::string err = launch_ops(one, s_exec_);
+    if (!err.empty()) return err;
+    CW_TRY(cudaEventRecord(ev[i + 1], s_exec_));
+  }
+  launch_exec_done(ab_, kRing - 1, exec_recs_, s_exec_);
+  exec_seq_ = seq + 1;
+  CW_TRY(cudaStreamSynchronize(s_exec_));
+  ms->resize(p.ops.size());
+  kinds->resize(p.ops.size());
+  for (size_t i = 0; i < p.ops.size(); ++i) {
+    CW_TRY(cudaEventElapsedTime(&(*ms)[i], ev[i], ev[i + 1]));
+    (*kinds)[i] = p.ops[i].kind;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return "";
+}
+
 std::string Runtime::sync_all() {
   CW_TRY(cudaSetDevice(device_));
   CW_TRY(cudaDeviceSynchronize());

@@ -145,6 +145,11 @@ class Runtime {
     return out_host_ + (seq & (kRing - 1)) * (size_t)kMaxBatch * out_floats_max_;
   }
 
+  // Eager (non-graph) run of the (arch, batch) ops with CUDA events between
+  // launches on the Exec stream; per-op milliseconds (profiling / roofline).
+  std::string profile_ops(int arch, int batch, int32_t hdr_page, std::vector<float>* ms,
+                          std::vector<int>* kinds);
+
   // Blocking helpers (tests, bench).
   std::string sync_all();
   int64_t clock_offset() const { return gt_offset_; }  // globaltimer - CLOCK_REALTIME

@@ -115,6 +115,15 @@ class DeviceRuntime:
               "exec_many")
         return ex, wall.value
 
+    def profile_ops(self, arch_id: int, batch: int, hdr_page: int) -> tuple[np.ndarray, np.ndarray]:
+        n = len(self.archs[arch_id].ops)
+        ms = np.zeros(n, np.float32)
+        kinds = np.zeros(n, np.int32)
+        got = check(lib.cw_rt_profile_ops(self.h, arch_id, batch, hdr_page, ms.ctypes.data,
+                                          kinds.ctypes.data_as(C.POINTER(C.c_int32)), n),
+                    "profile_ops")
+        return ms[:got], kinds[:got]
+
     def buffer_io(self, arch_id: int, buf: int, arr: np.ndarray, to_device: bool):
         check(lib.cw_rt_buffer_io(self.h, arch_id, buf, arr.ctypes.data, arr.nbytes,
                                   1 if to_device else 0), "buffer_io")
