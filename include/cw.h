@@ -93,6 +93,9 @@ int cw_rt_exec_many(cw_runtime* rt, int arch_id, int batch, const int32_t* hdr_p
  * Exec stream (per-op milliseconds, for the roofline); returns the op count. */
 int cw_rt_profile_ops(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page, float* op_ms,
                       int32_t* op_kinds, int max_ops);
+/* Per-op launch plan: 8 ints per op (kind, conv mode, BN, m_tiles, split-K, stages,
+ * k-blocks, fused-avgpool); returns the op count. */
+int cw_rt_plan_ops(cw_runtime* rt, int arch_id, int batch, int32_t* out8, int max_ops);
 /* Copy to/from a workspace activation buffer (parity tests of single layers). */
 int cw_rt_buffer_io(cw_runtime* rt, int arch_id, int buf, void* host, int64_t bytes,
                     int to_device);

@@ -199,5 +199,26 @@ int cw_rt_profile_ops(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page, 
   return n;
 }
 
+int cw_rt_plan_ops(cw_runtime* rt, int arch_id, int batch, int32_t* out8, int max_ops) {
+  const cw::Arch* a = rt->rt.arch(arch_id);
+  if (!a) return cw::fail("unknown arch");
+  auto it = a->plans.find(batch);
+  if (it == a->plans.end()) return cw::fail("no plan for batch");
+  const auto& ops = it->second.ops;
+  for (int i = 0; i < (int)ops.size() && i < max_ops; ++i) {
+    const cw::PlanOp& po = ops[i];
+    int32_t* o = out8 + 8 * i;
+    o[0] = po.kind;
+    o[1] = po.kind == cw::OP_CONV ? po.args.mode : -1;
+    o[2] = po.bn;
+    o[3] = po.m_tiles;
+    o[4] = po.kind == cw::OP_CONV ? po.args.splits : 0;
+    o[5] = po.kind == cw::OP_CONV ? po.args.stages : 0;
+    o[6] = po.kind == cw::OP_CONV ? po.args.num_kb : 0;
+    o[7] = po.kind == cw::OP_CONV ? (po.args.pool_out != nullptr) : 0;
+  }
+  return (int)ops.size();
+}
+
 }  // extern "C"
 

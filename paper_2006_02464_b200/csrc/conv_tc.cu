@@ -10,17 +10,28 @@
 // of the ResNet family (1x1, 3x3, strided, downsample, and conv1 after the
 // input-stage im2col).
 //
-// One CTA computes one 128 x BN output tile; 6 warps:
+// One CTA computes one 128 x BN output tile (or one K-slice of it); 6 warps:
 //   warp 0      TMA producer: per 64-wide k-block, A tile (128 rows x 128 B) and
-//               W tile (BN rows x 128 B), both 128B-swizzled, into a STAGES ring.
+//               W tile (BN rows x 128 B, 64-row boxes), 128B-swizzled, into a
+//               `stages`-deep ring.
 //               mode 0: A via a 2D tensor map over a [M][K] matrix.
 //               mode 1: A via a 4D NHWC tensor map; k-block -> (tap r,s; 64 channels)
 //               and the box origin is shifted by the tap. Padding is TMA
 //               out-of-bounds zero fill; stride is the TMA element stride.
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN,
 //               K=16 per instruction, fp32 accumulators in TMEM).
-//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 16 columns, + bias, + residual,
-//               ReLU, bf16 pack, 32-byte stores of NHWC rows.
+//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 16 columns, + bias, + residual
+//               (prefetched into registers while the main loop runs), ReLU,
+//               bf16 pack, 32-byte stores of NHWC rows -- or, for the last conv
+//               of the network, a deterministic in-CTA global average pool.
+//
+// Split-K (grid.z > 1): every slice stores its fp32 partial tile to an L2
+// workspace; the last slice to arrive (per-tile counter) sums the slices in
+// fixed z order (bit-deterministic) and runs the epilogue.
+//
+// Programmatic dependent launch: barrier init, TMEM allocation, bias staging,
+// the weight tensor-map prefetch and the first weight tiles' TMA are issued
+// before griddepcontrol.wait, overlapping the previous layer's tail.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -32,33 +43,39 @@ namespace cw {
 
 constexpr int kConvThreads = 192;
 constexpr uint32_t kATileBytes = 128 * 128;
+constexpr int kMaxStages = 8;
 
-template <int BN, int STAGES>
+template <int BN>
 struct ConvSmem {
   static constexpr uint32_t kBBytes = BN * 128;
   static constexpr uint32_t kStageBytes = kATileBytes + kBBytes;
-  static constexpr uint32_t kBarOff = STAGES * kStageBytes;
-  static constexpr uint32_t kBiasOff = kBarOff + 256;
-  static constexpr uint32_t kTotal = kBiasOff + BN * 4 + 1024;  // + alignment slack
-  static_assert((2 * STAGES + 2) * 8 <= 256, "barrier area");
+  // after the stage ring: barriers (256 B), bias (BN floats), pool scratch (128 x 17 floats)
+  static constexpr uint32_t kTail = 256 + BN * 4 + 128 * 17 * 4 + 1024;
+  static uint32_t total(int stages) { return stages * kStageBytes + kTail; }
 };
 
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(kConvThreads, 1)
+template <int BN>
+__global__ void __launch_bounds__(kConvThreads, 2)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const ConvArgs args) {
-  using L = ConvSmem<BN, STAGES>;
+  using L = ConvSmem<BN>;
   const ActionBlock* ab = args.ab;
-  if (ab->skip) return;
-
+  if (ab->skip) {  // ActionBlock is final: the gate kernel completed before this graph's 2nd node
+    griddep_trigger();
+    return;
+  }
+  const int stages = args.stages;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
-  const uint32_t bar_full = sbase + L::kBarOff;             // STAGES x 8 B
-  const uint32_t bar_empty = bar_full + STAGES * 8;         // STAGES x 8 B
-  const uint32_t bar_tfull = bar_empty + STAGES * 8;        // 8 B
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kBarOff + (2 * STAGES + 1) * 8);
-  float* sbias = reinterpret_cast<float*>(smem + L::kBiasOff);
+  const uint32_t tail = stages * L::kStageBytes;
+  const uint32_t bar_full = sbase + tail;                   // stages x 8 B
+  const uint32_t bar_empty = bar_full + kMaxStages * 8;     // stages x 8 B
+  const uint32_t bar_tfull = bar_empty + kMaxStages * 8;    // 8 B
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + tail + (2 * kMaxStages + 1) * 8);
+  int* flag_slot = reinterpret_cast<int*>(smem + tail + (2 * kMaxStages + 2) * 8);
+  float* sbias = reinterpret_cast<float*>(smem + tail + 256);
+  float* sred = sbias + BN;  // [128][17]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -66,6 +83,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const CUtensorMap* tmap_b = reinterpret_cast<const CUtensorMap*>(hdr + args.layer * kTmapBytes);
   const float* bias = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[args.layer];
   const int n0 = blockIdx.y * BN;
+  const int kb0 = blockIdx.z * args.kb_per_split;
+  const int kb1 = min(args.num_kb, kb0 + args.kb_per_split);
+  const int n_kb = kb1 - kb0;
 
   // Output-tile origin.
   int m0 = 0, ow0 = 0, oh0 = 0, img0 = 0;
@@ -81,8 +101,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     img0 = tn * args.box_n;
   }
 
+  // ---- prologue: nothing here reads data produced by the previous kernel
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < stages; ++s) {
       mbar_init(bar_full + 8 * s, 1);
       mbar_init(bar_empty + 8 * s, 1);
     }
@@ -94,13 +115,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   }
   if (warp == 1) tmem_alloc(smem_u32(tmem_slot), BN);
   if (warp >= 2) {
-    for (int i = threadIdx.x - 64; i < BN; i += 128) sbias[i] = bias[n0 + i];
+    for (int i = threadIdx.x - 64; i < BN; i += 128) sbias[i] = __ldg(bias + n0 + i);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int num_kb = args.num_kb;
+  if (threadIdx.x == 0) griddep_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -109,14 +130,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const uint32_t tx_bytes = a_rows * 128u + L::kBBytes;
       const int wb = ow0 * args.stride - args.pad;
       const int hb = oh0 * args.stride - args.pad;
-      int s = 0;
-      uint32_t phase = 0;
-      for (int kb = 0; kb < num_kb; ++kb) {
-        mbar_wait(bar_empty + 8 * s, phase ^ 1);
+      auto load_a = [&](int kb, int s) {
         const uint32_t a_dst = sbase + s * L::kStageBytes;
-        const uint32_t b_dst = a_dst + kATileBytes;
         const uint32_t full = bar_full + 8 * s;
-        mbar_arrive_expect_tx(full, tx_bytes);
         if (args.mode == 0) {
           tma_load_2d(a_dst, &tmap_a, full, kb * 64, m0);
         } else {
@@ -126,10 +142,30 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           const int q = tap - r * args.kw;
           tma_load_4d(a_dst, &tmap_a, full, c0, wb + q, hb + r, img0);
         }
+      };
+      auto load_b = [&](int kb, int s) {
+        const uint32_t b_dst = sbase + s * L::kStageBytes + kATileBytes;
+        const uint32_t full = bar_full + 8 * s;
 #pragma unroll
         for (int j = 0; j < BN / 64; ++j)
           tma_load_2d(b_dst + j * 8192, tmap_b, full, kb * 64, n0 + 64 * j);
-        if (++s == STAGES) { s = 0; phase ^= 1; }
+      };
+      // Weights do not depend on the previous layer: start streaming them first.
+      const int pre = n_kb < stages ? n_kb : stages;
+      for (int i = 0; i < pre; ++i) {
+        mbar_arrive_expect_tx(bar_full + 8 * i, tx_bytes);
+        load_b(kb0 + i, i);
+      }
+      griddep_wait();
+      for (int i = 0; i < pre; ++i) load_a(kb0 + i, i);
+      int s = pre % stages;
+      uint32_t phase = pre == stages ? 1 : 0;
+      for (int i = pre; i < n_kb; ++i) {
+        mbar_wait(bar_empty + 8 * s, phase ^ 1);
+        mbar_arrive_expect_tx(bar_full + 8 * s, tx_bytes);
+        load_b(kb0 + i, s);
+        load_a(kb0 + i, s);
+        if (++s == stages) { s = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -138,7 +174,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
       int s = 0;
       uint32_t phase = 0;
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int i = 0; i < n_kb; ++i) {
         mbar_wait(bar_full + 8 * s, phase);
         tc_fence_after();
         const uint32_t a_addr = sbase + s * L::kStageBytes;
@@ -147,10 +183,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           // +32 bytes along K inside the 128-byte swizzled row = +2 in desc units.
-          mma_bf16(tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          mma_bf16(tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (i | k) != 0);
         }
         mma_commit(bar_empty + 8 * s);
-        if (++s == STAGES) { s = 0; phase ^= 1; }
+        if (++s == stages) { s = 0; phase ^= 1; }
       }
       mma_commit(bar_tfull);
     }
@@ -158,8 +194,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // ---------------- epilogue (warps 2..5; TMEM lane quarter = warp % 4)
     const int q = warp & 3;
     const int row = q * 32 + lane;
+    const int et = threadIdx.x - 64;  // 0..127
     bool valid;
     long long m;
+    int img_local = 0;
     if (args.mode == 0) {
       m = (long long)m0 + row;
       valid = m < args.m_total;
@@ -172,32 +210,89 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const int ow = ow0 + wi, oh = oh0 + hi, n = img0 + ni;
       valid = row < rows && ow < args.ow && oh < args.oh && n < args.nimg;
       m = ((long long)n * args.oh + oh) * args.ow + ow;
+      img_local = ni;
     }
-    __nv_bfloat16* out_row = reinterpret_cast<__nv_bfloat16*>(args.out) + m * args.n_out + n0;
-    const __nv_bfloat16* res_row =
-        args.residual ? reinterpret_cast<const __nv_bfloat16*>(args.residual) + m * args.n_out + n0
-                      : nullptr;
-    mbar_wait(bar_tfull, 0);
-    tc_fence_after();
+    griddep_wait();  // residual / split-K workspace are written by earlier kernels
+    const int tile = blockIdx.x * gridDim.y + blockIdx.y;
+    bool last = true;
     const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16);
+    if (args.splits > 1) {
+      mbar_wait(bar_tfull, 0);
+      tc_fence_after();
+      float* mine = args.partial + ((size_t)tile * args.splits + blockIdx.z) * 128 * BN + row * BN;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      uint32_t v[16];
-      tmem_ld16(taddr + c, v);
-      tmem_ld_wait();
-      if (valid) {
-        float f[16];
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t v[16];
+        tmem_ld16(taddr + c, v);
+        tmem_ld_wait();
+        float4* dst = reinterpret_cast<float4*>(mine + c);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + sbias[c + i];
-        if (res_row) {
-          const uint4* rp = reinterpret_cast<const uint4*>(res_row + c);
-          uint4 r0 = rp[0], r1 = rp[1];
-          const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&r0);
-          const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&r1);
+        for (int i = 0; i < 4; ++i)
+          __stcg(dst + i, make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                      __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3])));
+      }
+      __threadfence();
+      named_bar(1, 128);
+      if (et == 0) {
+        const int prev = atomicAdd(args.counters + tile, 1);
+        const int is_last = prev == args.splits - 1;
+        if (is_last) args.counters[tile] = 0;  // ready for the next INFER
+        *flag_slot = is_last;
+      }
+      named_bar(1, 128);
+      last = *flag_slot != 0;
+      __threadfence();
+    }
+    if (last) {
+      const __nv_bfloat16* res_row =
+          args.residual ? reinterpret_cast<const __nv_bfloat16*>(args.residual) + m * args.n_out + n0
+                        : nullptr;
+      // Prefetch the whole residual row slice while the main loop is still running.
+      uint4 res[BN / 8];
+      if (res_row && valid) {
+#pragma unroll
+        for (int i = 0; i < BN / 8; ++i) res[i] = __ldg(reinterpret_cast<const uint4*>(res_row) + i);
+      }
+      if (args.splits == 1) {
+        mbar_wait(bar_tfull, 0);
+        tc_fence_after();
+      }
+      __nv_bfloat16* out_row =
+          args.out ? reinterpret_cast<__nv_bfloat16*>(args.out) + m * args.n_out + n0 : nullptr;
+#pragma unroll
+      for (int c = 0; c < BN; c += 16) {
+        float f[16];
+        if (args.splits == 1) {
+          uint32_t v[16];
+          tmem_ld16(taddr + c, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) f[i] = 0.0f;
+          const float* base = args.partial + (size_t)tile * args.splits * 128 * BN + row * BN + c;
+          for (int z = 0; z < args.splits; ++z) {
+            const float4* src = reinterpret_cast<const float4*>(base + (size_t)z * 128 * BN);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float4 p = __ldcg(src + i);
+              f[4 * i] += p.x;
+              f[4 * i + 1] += p.y;
+              f[4 * i + 2] += p.z;
+              f[4 * i + 3] += p.w;
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) f[i] += sbias[c + i];
+        if (res_row && valid) {
+          const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&res[c / 8]);
+          const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&res[c / 8 + 1]);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            float2 a = __bfloat1622float2(h0[i]);
-            float2 b = __bfloat1622float2(h1[i]);
+            const float2 a = __bfloat1622float2(h0[i]);
+            const float2 b = __bfloat1622float2(h1[i]);
             f[2 * i] += a.x;
             f[2 * i + 1] += a.y;
             f[8 + 2 * i] += b.x;
@@ -208,18 +303,35 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) f[i] = fmaxf(f[i], 0.0f);
         }
-        uint4 o0, o1;
-        o0.x = pack_bf16x2(f[0], f[1]);
-        o0.y = pack_bf16x2(f[2], f[3]);
-        o0.z = pack_bf16x2(f[4], f[5]);
-        o0.w = pack_bf16x2(f[6], f[7]);
-        o1.x = pack_bf16x2(f[8], f[9]);
-        o1.y = pack_bf16x2(f[10], f[11]);
-        o1.z = pack_bf16x2(f[12], f[13]);
-        o1.w = pack_bf16x2(f[14], f[15]);
-        uint4* op = reinterpret_cast<uint4*>(out_row + c);
-        op[0] = o0;
-        op[1] = o1;
+        if (args.pool_out) {
+          // Deterministic in-CTA global average pool: the tile holds whole images.
+#pragma unroll
+          for (int i = 0; i < 16; ++i) sred[row * 17 + i] = valid ? f[i] : 0.0f;
+          named_bar(1, 128);
+          const int hw = args.oh * args.ow;
+          if (et < 16 * args.box_n) {
+            const int img = et >> 4, col = et & 15;
+            float acc = 0.0f;
+            for (int r = img * hw; r < (img + 1) * hw; ++r) acc += sred[r * 17 + col];
+            if (img0 + img < args.nimg)
+              args.pool_out[(size_t)(img0 + img) * args.n_out + n0 + c + col] = acc * args.pool_scale;
+          }
+          named_bar(1, 128);
+          (void)img_local;
+        } else if (valid) {
+          uint4 o0, o1;
+          o0.x = pack_bf16x2(f[0], f[1]);
+          o0.y = pack_bf16x2(f[2], f[3]);
+          o0.z = pack_bf16x2(f[4], f[5]);
+          o0.w = pack_bf16x2(f[6], f[7]);
+          o1.x = pack_bf16x2(f[8], f[9]);
+          o1.y = pack_bf16x2(f[10], f[11]);
+          o1.z = pack_bf16x2(f[12], f[13]);
+          o1.w = pack_bf16x2(f[14], f[15]);
+          uint4* op = reinterpret_cast<uint4*>(out_row + c);
+          op[0] = o0;
+          op[1] = o1;
+        }
       }
     }
   }
@@ -234,35 +346,54 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
 // ------------------------------------------------------------------ host side
 
-template <int BN, int STAGES>
+template <int BN>
 static cudaError_t configure_bn() {
-  return cudaFuncSetAttribute(conv_tc_kernel<BN, STAGES>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              ConvSmem<BN, STAGES>::kTotal);
-}
-
-template <int BN, int STAGES>
-static cudaError_t launch_bn(const CUtensorMap& tmap_a, const ConvArgs& a, int m_tiles,
-                             cudaStream_t st) {
-  dim3 grid(m_tiles, a.n_out / BN);
-  conv_tc_kernel<BN, STAGES><<<grid, kConvThreads, ConvSmem<BN, STAGES>::kTotal, st>>>(tmap_a, a);
-  return cudaGetLastError();
+  const uint32_t want = ConvSmem<BN>::total(kMaxStages);
+  const uint32_t cap = 227 * 1024;
+  return cudaFuncSetAttribute(conv_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              want < cap ? want : cap);
 }
 
 // Must run once per device before the first launch (and before graph capture).
 cudaError_t configure_conv_tc() {
   cudaError_t e;
-  if ((e = configure_bn<64, 6>()) != cudaSuccess) return e;
-  if ((e = configure_bn<128, 5>()) != cudaSuccess) return e;
-  return configure_bn<256, 4>();
+  if ((e = configure_bn<64>()) != cudaSuccess) return e;
+  if ((e = configure_bn<128>()) != cudaSuccess) return e;
+  return configure_bn<256>();
+}
+
+uint32_t conv_smem_bytes(int bn, int stages) {
+  switch (bn) {
+    case 64: return ConvSmem<64>::total(stages);
+    case 128: return ConvSmem<128>::total(stages);
+    default: return ConvSmem<256>::total(stages);
+  }
+}
+
+template <int BN>
+static cudaError_t launch_bn(const CUtensorMap& tmap_a, const ConvArgs& a, int m_tiles,
+                             cudaStream_t st, bool pdl) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(m_tiles, a.n_out / BN, a.splits);
+  cfg.blockDim = dim3(kConvThreads);
+  cfg.dynamicSmemBytes = ConvSmem<BN>::total(a.stages);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, conv_tc_kernel<BN>, tmap_a, a);
 }
 
 cudaError_t launch_conv_tc(const CUtensorMap& tmap_a, const ConvArgs& a, int bn, int m_tiles,
-                           cudaStream_t st) {
+                           cudaStream_t st, bool pdl) {
+  if (a.stages < 1 || a.stages > kMaxStages || conv_smem_bytes(bn, a.stages) > 227 * 1024)
+    return cudaErrorInvalidValue;
   switch (bn) {
-    case 64: return launch_bn<64, 6>(tmap_a, a, m_tiles, st);
-    case 128: return launch_bn<128, 5>(tmap_a, a, m_tiles, st);
-    case 256: return launch_bn<256, 4>(tmap_a, a, m_tiles, st);
+    case 64: return launch_bn<64>(tmap_a, a, m_tiles, st, pdl);
+    case 128: return launch_bn<128>(tmap_a, a, m_tiles, st, pdl);
+    case 256: return launch_bn<256>(tmap_a, a, m_tiles, st, pdl);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -72,6 +72,13 @@ struct ConvArgs {
   void* out;              // bf16 NHWC / [M][Cout]
   const void* residual;   // bf16, same shape as out, or null
   const ActionBlock* ab;
+  int stages;             // smem pipeline depth
+  int splits;             // split-K factor (grid.z)
+  int kb_per_split;
+  float* partial;         // split-K: [m_tiles*n_tiles][splits][128][BN] fp32
+  int* counters;          // split-K: [m_tiles*n_tiles], zero between launches
+  float* pool_out;        // fused global avgpool: [nimg][n_out] fp32 (tile = whole images)
+  float pool_scale;
 };
 
 }  // namespace cw

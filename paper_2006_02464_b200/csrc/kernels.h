@@ -8,8 +8,10 @@
 namespace cw {
 
 cudaError_t configure_conv_tc();
+cudaError_t configure_simt();
+uint32_t conv_smem_bytes(int bn, int stages);
 cudaError_t launch_conv_tc(const CUtensorMap& tmap_a, const ConvArgs& a, int bn, int m_tiles,
-                           cudaStream_t st);
+                           cudaStream_t st, bool pdl);
 
 void launch_gate(ActionBlock* ab, const ActionDesc* ring, uint32_t mask, uint64_t* ctr,
                  ExecRecord* recs, cudaStream_t st);

@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <ctime>
 #include <thread>
@@ -35,6 +36,8 @@ Runtime::~Runtime() {
       if (p.graph) cudaGraphDestroy(p.graph);
     }
     for (void* b : a.bufs) cudaFree(b);
+    cudaFree(a.partial);
+    cudaFree(a.counters);
   }
   for (auto& [id, bl] : blobs_) cudaFreeHost(bl.host);
   for (auto e : exec_events_) cudaEventDestroy(e);
@@ -66,6 +69,8 @@ std::string Runtime::open(int device, int64_t pages_total, int64_t page_bytes, i
   if (prop.major != 10) return std::string("sm_100a required, found ") + prop.name;
   if (!tmap_init()) return "cuTensorMapEncodeTiled unavailable";
   CW_TRY(configure_conv_tc());
+  CW_TRY(configure_simt());
+  pdl_ = getenv("CW_NO_PDL") == nullptr;
   pages_total_ = pages_total;
   page_bytes_ = page_bytes;
   CW_TRY(cudaMalloc(&pool_, (size_t)(pages_total * page_bytes)));
@@ -235,11 +240,36 @@ static void box_dims(int nimg, int oh, int ow, int* bw, int* bh, int* bn) {
   *bn = n;
 }
 
+// Tile / pipeline / split-K choice for one conv at one batch size. B200: 148 SMs,
+// two 107 KB CTAs per SM when a layer has more than one wave of tiles, else one
+// CTA per SM with a deep (up to 8-stage) pipeline; split K until the grid covers
+// the SMs, keeping >= 4 k-blocks per slice.
+static void plan_conv(ConvArgs& c, int cout, int m_tiles, int* bn_out) {
+  int bn = (cout % 128 == 0) ? 128 : 64;
+  if (bn == 128 && m_tiles * (cout / 128) < 148) bn = 64;
+  const int tiles = m_tiles * (cout / bn);
+  int splits = 1;
+  if (tiles < 148) {
+    splits = std::max(1, std::min(2 * 148 / tiles, c.num_kb / 4));
+    const int per = (c.num_kb + splits - 1) / splits;
+    splits = (c.num_kb + per - 1) / per;
+  }
+  c.splits = splits;
+  c.kb_per_split = (c.num_kb + splits - 1) / splits;
+  const int ctas = tiles * splits;
+  const int stage_kb = bn == 64 ? 24 : (bn == 128 ? 32 : 48);
+  int stages = ctas > 148 ? (bn == 64 ? 4 : 3) : 192 / stage_kb;
+  stages = std::max(1, std::min(stages, c.kb_per_split));
+  c.stages = stages;
+  *bn_out = bn;
+}
+
 std::string Runtime::build_plan(Arch& a, int batch) {
   Plan& p = a.plans[batch];
   p.batch = batch;
   p.ops.clear();
-  for (const CwOp& op : a.ops) {
+  for (size_t oi = 0; oi < a.ops.size(); ++oi) {
+    const CwOp& op = a.ops[oi];
     PlanOp po;
     po.kind = op.kind;
     po.batch = batch;
@@ -253,6 +283,10 @@ std::string Runtime::build_plan(Arch& a, int batch) {
     po.classes = op.cout;
     po.in = op.in_buf >= 0 ? a.bufs[op.in_buf] : nullptr;
     po.out = op.out_buf >= 0 ? a.bufs[op.out_buf] : nullptr;
+    if (op.kind == OP_AVGPOOL && !p.ops.empty() && p.ops.back().kind == OP_CONV &&
+        p.ops.back().args.pool_out != nullptr) {
+      po.kind = -1;  // fused into the previous conv's epilogue
+    }
     if (op.kind == OP_CONV) {
       ConvArgs& c = po.args;
       c.layer = op.layer;
@@ -268,8 +302,11 @@ std::string Runtime::build_plan(Arch& a, int batch) {
       c.kw = op.kw;
       c.stride = op.stride;
       c.pad = op.pad;
-      int n_tiles_128 = op.cout / 128;
-      if (op.kh == 1 && op.kw == 1 && op.stride == 1 && op.pad == 0) {
+      // Fuse a following global average pool when one tile can hold whole images.
+      const CwOp* nxt = oi + 1 < a.ops.size() ? &a.ops[oi + 1] : nullptr;
+      const bool fuse_pool = nxt && nxt->kind == OP_AVGPOOL && nxt->in_buf == op.out_buf &&
+                             op.out_h * op.out_w <= 128 && op.cin % 64 == 0;
+      if (!fuse_pool && op.kh == 1 && op.kw == 1 && op.stride == 1 && op.pad == 0) {
         c.mode = 0;
         c.m_total = batch * op.out_h * op.out_w;
         po.m_tiles = (c.m_total + 127) / 128;
@@ -279,7 +316,16 @@ std::string Runtime::build_plan(Arch& a, int batch) {
         if (op.cin % 64) return "conv Cin must be a multiple of 64";
         c.mode = 1;
         c.cin_kb = op.cin / 64;
-        box_dims(batch, op.out_h, op.out_w, &c.box_w, &c.box_h, &c.box_n);
+        if (fuse_pool) {
+          c.box_w = op.out_w;
+          c.box_h = op.out_h;
+          c.box_n = std::max(1, std::min(batch, 128 / (op.out_w * op.out_h)));
+          c.pool_out = reinterpret_cast<float*>(a.bufs[nxt->out_buf]);
+          c.pool_scale = 1.0f / (float)(op.out_h * op.out_w);
+          c.out = nullptr;
+        } else {
+          box_dims(batch, op.out_h, op.out_w, &c.box_w, &c.box_h, &c.box_n);
+        }
         c.tiles_w = (op.out_w + c.box_w - 1) / c.box_w;
         c.tiles_h = (op.out_h + c.box_h - 1) / c.box_h;
         const int tiles_n = (batch + c.box_n - 1) / c.box_n;
@@ -288,8 +334,15 @@ std::string Runtime::build_plan(Arch& a, int batch) {
                             c.box_n, op.stride))
           return "tensor map (nhwc) failed";
       }
-      po.bn = (op.cout % 128 == 0) ? 128 : 64;
-      if (po.bn == 128 && (int64_t)po.m_tiles * n_tiles_128 < 148) po.bn = 64;
+      plan_conv(c, op.cout, po.m_tiles, &po.bn);
+      const int tiles = po.m_tiles * (op.cout / po.bn);
+      if (c.splits > 1) {
+        if (tiles > kCounterStride) return "too many split-K tiles";
+        const size_t need = (size_t)tiles * c.splits * 128 * po.bn * 4;
+        if (need > a.partial_bytes) return "split-K workspace too small";
+        c.partial = a.partial;
+        c.counters = a.counters + oi * kCounterStride;
+      }
     }
     p.ops.push_back(po);
   }
@@ -303,7 +356,9 @@ std::string Runtime::launch_ops(const Plan& p, cudaStream_t st) {
         launch_stem_im2col(ab_, po.out, po.batch, po.in_h, po.in_w, po.out_h, po.out_w, po.kpad, st);
         break;
       case OP_CONV:
-        CW_TRY(launch_conv_tc(po.tmap, po.args, po.bn, po.m_tiles, st));
+        CW_TRY(launch_conv_tc(po.tmap, po.args, po.bn, po.m_tiles, st, pdl_));
+        break;
+      case -1:
         break;
       case OP_MAXPOOL:
         launch_maxpool(ab_, po.in, po.out, po.batch, po.in_h, po.in_w, po.c, po.out_h, po.out_w, st);
@@ -336,7 +391,8 @@ std::string Runtime::capture(Arch& a, Plan& p) {
   CW_TRY(e);
   p.graph = g;
   CW_TRY(cudaGraphInstantiate(&p.exec, g, 0));
-  p.launches = (int)p.ops.size() + 2;
+  p.launches = 2;
+  for (const PlanOp& po : p.ops) p.launches += po.kind >= 0 ? 1 : 0;
   return "";
 }
 
@@ -346,6 +402,11 @@ std::string Runtime::build_plans() {
     a.bufs.assign(a.buf_bytes.size(), nullptr);
     for (size_t i = 0; i < a.buf_bytes.size(); ++i)
       if (a.buf_bytes[i]) CW_TRY(cudaMalloc(&a.bufs[i], a.buf_bytes[i]));
+    // Split-K: at most 2*148 CTAs per split conv, 128 x 128 fp32 partial each.
+    a.partial_bytes = (size_t)2 * 148 * 128 * 128 * 4 * 2;
+    CW_TRY(cudaMalloc(&a.partial, a.partial_bytes));
+    CW_TRY(cudaMalloc(&a.counters, a.ops.size() * kCounterStride * sizeof(int)));
+    CW_TRY(cudaMemset(a.counters, 0, a.ops.size() * kCounterStride * sizeof(int)));
     for (auto& [b, p] : a.plans) {
       std::string err = build_plan(a, b);
       if (!err.empty()) return err;

@@ -44,7 +44,7 @@ struct CwTensorLoc {
 };
 
 struct PlanOp {
-  int kind = 0;
+  int kind = 0;  // OpKind, or -1 when fused into the previous op
   ConvArgs args{};
   CUtensorMap tmap{};
   int bn = 0, m_tiles = 0;
@@ -71,7 +71,11 @@ struct Arch {
   std::vector<size_t> buf_bytes;
   std::map<int, Plan> plans;
   double flops_per_image = 0;
+  float* partial = nullptr;       // split-K fp32 workspace (shared by all ops: layers run in order)
+  size_t partial_bytes = 0;
+  int* counters = nullptr;        // split-K tile counters, kCounterStride per op
 };
+constexpr int kCounterStride = 4096;
 
 struct Blob {
   int id = -1;
@@ -199,6 +203,7 @@ class Runtime {
   std::map<int, Blob> blobs_;
   int64_t gt_offset_ = 0;
   bool plans_built_ = false;
+  bool pdl_ = true;  // programmatic dependent launch between graph nodes
 };
 
 }  // namespace cw

@@ -61,6 +61,7 @@ __global__ void gate_kernel(ActionBlock* ab, const ActionDesc* ring, uint32_t ri
 }
 
 __global__ void exec_done_kernel(const ActionBlock* ab, uint32_t ring_mask, ExecRecord* recs) {
+  griddep_wait();
   const uint64_t i = ab->seq;
   ExecRecord* r = &recs[i & ring_mask];
   r->t_end = globaltimer();
@@ -96,6 +97,8 @@ __global__ void stamp_kernel(volatile uint64_t* slot, uint64_t tag) {
 // K = (r*7 + s)*3 + c for r,s < 7, c < 3 (147 values), zero-padded to kpad.
 __global__ void stem_im2col_kernel(const ActionBlock* ab, __nv_bfloat16* __restrict__ a, int batch,
                                    int H, int W, int OH, int OW, int kpad) {
+  griddep_wait();
+  griddep_trigger();
   if (ab->skip) return;
   const int chunks = kpad / 8;
   const long long total = (long long)batch * OH * OW * chunks;
@@ -134,6 +137,8 @@ __global__ void stem_im2col_kernel(const ActionBlock* ab, __nv_bfloat16* __restr
 __global__ void maxpool3x3s2_kernel(const ActionBlock* ab, const __nv_bfloat16* __restrict__ in,
                                     __nv_bfloat16* __restrict__ out, int batch, int H, int W, int C,
                                     int OH, int OW) {
+  griddep_wait();
+  griddep_trigger();
   if (ab->skip) return;
   const int chunks = C / 8;
   const long long total = (long long)batch * OH * OW * chunks;
@@ -174,6 +179,8 @@ __global__ void maxpool3x3s2_kernel(const ActionBlock* ab, const __nv_bfloat16* 
 
 __global__ void avgpool_kernel(const ActionBlock* ab, const __nv_bfloat16* __restrict__ in,
                                float* __restrict__ pooled, int batch, int HW, int C) {
+  griddep_wait();
+  griddep_trigger();
   if (ab->skip) return;
   const int chunks = C / 8;
   const int total = batch * chunks;
@@ -199,10 +206,18 @@ __global__ void avgpool_kernel(const ActionBlock* ab, const __nv_bfloat16* __res
   o[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
 }
 
-// One warp per output class; C must be a multiple of 256.
+// logits[n][j] = pooled[n] . W[j] + bias[j]. One CTA per 8 classes (one warp
+// each); the pooled features of the whole batch are staged in shared memory
+// once per CTA, the class's weight row lives in registers. C % 256 == 0, C <= 2048.
 __global__ void fc_kernel(const ActionBlock* ab, const float* __restrict__ pooled, int layer,
                           int batch, int C, int classes) {
+  extern __shared__ float sp[];  // [batch][C]
+  griddep_wait();
+  griddep_trigger();
   if (ab->skip) return;
+  for (int i = threadIdx.x * 4; i < batch * C; i += blockDim.x * 4)
+    *reinterpret_cast<float4*>(sp + i) = __ldcg(reinterpret_cast<const float4*>(pooled + i));
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x * (blockDim.x >> 5) + warp;
   if (j >= classes) return;
@@ -210,28 +225,34 @@ __global__ void fc_kernel(const ActionBlock* ab, const float* __restrict__ poole
   const __nv_bfloat16* w =
       reinterpret_cast<const __nv_bfloat16* const*>(hdr + kHdrWeightOff)[layer] + (long long)j * C;
   const float* bias = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[layer];
+  const int chunks = C / 256;  // 16-byte weight chunks per lane
   float wf[64];
-  const int per_lane = C / 256;  // 16-byte chunks per lane
-  for (int i = 0; i < per_lane && i < 8; ++i) {
-    uint4 u = __ldg(reinterpret_cast<const uint4*>(w + (i * 32 + lane) * 8));
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      float2 f = __bfloat1622float2(h[e]);
-      wf[i * 8 + 2 * e] = f.x;
-      wf[i * 8 + 2 * e + 1] = f.y;
+  for (int i = 0; i < 8; ++i) {
+    if (i < chunks) {
+      uint4 u = __ldg(reinterpret_cast<const uint4*>(w + (i * 32 + lane) * 8));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h[e]);
+        wf[i * 8 + 2 * e] = f.x;
+        wf[i * 8 + 2 * e + 1] = f.y;
+      }
     }
   }
-  const float b = bias[j];
+  const float b = __ldg(bias + j);
   for (int n = 0; n < batch; ++n) {
-    const float* pn = pooled + (long long)n * C;
+    const float* pn = sp + n * C;
     float acc = 0.0f;
-    for (int i = 0; i < per_lane && i < 8; ++i) {
-      const float4* pp = reinterpret_cast<const float4*>(pn + (i * 32 + lane) * 8);
-      float4 p0 = pp[0], p1 = pp[1];
-      acc += wf[i * 8 + 0] * p0.x + wf[i * 8 + 1] * p0.y + wf[i * 8 + 2] * p0.z +
-             wf[i * 8 + 3] * p0.w + wf[i * 8 + 4] * p1.x + wf[i * 8 + 5] * p1.y +
-             wf[i * 8 + 6] * p1.z + wf[i * 8 + 7] * p1.w;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i < chunks) {
+        const float4 p0 = *reinterpret_cast<const float4*>(pn + (i * 32 + lane) * 8);
+        const float4 p1 = *reinterpret_cast<const float4*>(pn + (i * 32 + lane) * 8 + 4);
+        acc += wf[i * 8 + 0] * p0.x + wf[i * 8 + 1] * p0.y + wf[i * 8 + 2] * p0.z +
+               wf[i * 8 + 3] * p0.w + wf[i * 8 + 4] * p1.x + wf[i * 8 + 5] * p1.y +
+               wf[i * 8 + 6] * p1.z + wf[i * 8 + 7] * p1.w;
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -251,8 +272,29 @@ void launch_gate(ActionBlock* ab, const ActionDesc* ring, uint32_t mask, uint64_
                  ExecRecord* recs, cudaStream_t st) {
   gate_kernel<<<1, 64, 0, st>>>(ab, ring, mask, ctr, recs);
 }
+cudaError_t configure_simt() {
+  return cudaFuncSetAttribute(fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kMaxBatch * 2048 * 4);
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 void launch_exec_done(const ActionBlock* ab, uint32_t mask, ExecRecord* recs, cudaStream_t st) {
-  exec_done_kernel<<<1, 1, 0, st>>>(ab, mask, recs);
+  launch_pdl(exec_done_kernel, dim3(1), dim3(1), 0, st, ab, mask, recs);
 }
 void launch_out_done(ExecRecord* rec, uint64_t seq, cudaStream_t st) {
   out_done_kernel<<<1, 1, 0, st>>>(rec, seq);
@@ -266,25 +308,26 @@ void launch_clock_pub(volatile uint64_t* slot, uint64_t max_ns, cudaStream_t st)
 void launch_stem_im2col(const ActionBlock* ab, void* a, int batch, int H, int W, int OH, int OW,
                         int kpad, cudaStream_t st) {
   long long total = (long long)batch * OH * OW * (kpad / 8);
-  stem_im2col_kernel<<<grid_for(total, 256), 256, 0, st>>>(
-      ab, reinterpret_cast<__nv_bfloat16*>(a), batch, H, W, OH, OW, kpad);
+  launch_pdl(stem_im2col_kernel, dim3(grid_for(total, 256)), dim3(256), 0, st, ab,
+             reinterpret_cast<__nv_bfloat16*>(a), batch, H, W, OH, OW, kpad);
 }
 void launch_maxpool(const ActionBlock* ab, const void* in, void* out, int batch, int H, int W,
                     int C, int OH, int OW, cudaStream_t st) {
   long long total = (long long)batch * OH * OW * (C / 8);
-  maxpool3x3s2_kernel<<<grid_for(total, 256), 256, 0, st>>>(
-      ab, reinterpret_cast<const __nv_bfloat16*>(in), reinterpret_cast<__nv_bfloat16*>(out), batch,
-      H, W, C, OH, OW);
+  launch_pdl(maxpool3x3s2_kernel, dim3(grid_for(total, 256)), dim3(256), 0, st, ab,
+             reinterpret_cast<const __nv_bfloat16*>(in), reinterpret_cast<__nv_bfloat16*>(out),
+             batch, H, W, C, OH, OW);
 }
 void launch_avgpool(const ActionBlock* ab, const void* in, float* pooled, int batch, int HW, int C,
                     cudaStream_t st) {
   int total = batch * (C / 8);
-  avgpool_kernel<<<(total + 127) / 128, 128, 0, st>>>(
-      ab, reinterpret_cast<const __nv_bfloat16*>(in), pooled, batch, HW, C);
+  launch_pdl(avgpool_kernel, dim3((total + 127) / 128), dim3(128), 0, st, ab,
+             reinterpret_cast<const __nv_bfloat16*>(in), pooled, batch, HW, C);
 }
 void launch_fc(const ActionBlock* ab, const float* pooled, int layer, int batch, int C, int classes,
                cudaStream_t st) {
-  fc_kernel<<<(classes + 7) / 8, 256, 0, st>>>(ab, pooled, layer, batch, C, classes);
+  launch_pdl(fc_kernel, dim3((classes + 7) / 8), dim3(256), (size_t)batch * C * 4, st, ab, pooled,
+             layer, batch, C, classes);
 }
 
 }  // namespace cw

@@ -124,6 +124,13 @@ class DeviceRuntime:
                     "profile_ops")
         return ms[:got], kinds[:got]
 
+    def plan_ops(self, arch_id: int, batch: int) -> np.ndarray:
+        n = len(self.archs[arch_id].ops)
+        out = np.zeros((n, 8), np.int32)
+        got = check(lib.cw_rt_plan_ops(self.h, arch_id, batch,
+                                       out.ctypes.data_as(C.POINTER(C.c_int32)), n), "plan_ops")
+        return out[:got]
+
     def buffer_io(self, arch_id: int, buf: int, arr: np.ndarray, to_device: bool):
         check(lib.cw_rt_buffer_io(self.h, arch_id, buf, arr.ctypes.data, arr.nbytes,
                                   1 if to_device else 0), "buffer_io")
