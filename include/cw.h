@@ -89,13 +89,14 @@ int cw_rt_infer_sync(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page,
  * %globaltimer) into exec_ns[i]; *wall_ns = CUDA-event time of all n on the Exec stream. */
 int cw_rt_exec_many(cw_runtime* rt, int arch_id, int batch, const int32_t* hdr_pages, int n,
                     int64_t* exec_ns, int64_t* wall_ns);
-/* Eager run of the (arch, batch) op list with CUDA events between launches on the
- * Exec stream (per-op milliseconds, for the roofline); returns the op count. */
-int cw_rt_profile_ops(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page, float* op_ms,
-                      int32_t* op_kinds, int max_ops);
-/* Per-op launch plan: 8 ints per op (kind, conv mode, BN, m_tiles, split-K, stages,
- * k-blocks, fused-avgpool); returns the op count. */
-int cw_rt_plan_ops(cw_runtime* rt, int arch_id, int batch, int32_t* out8, int max_ops);
+/* One INFER with the megakernel's per-layer trace read back: end_ms[i] = time from
+ * Exec start until plan layer i finished on its last SM; kinds[i] = layer kind
+ * (1 conv, 2 input, 3 maxpool, 4 avgpool, 5 fc, 6 split-K reduce). Returns the layer count. */
+int cw_rt_profile_layers(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page, float* end_ms,
+                         int32_t* kinds, int max_layers);
+/* Megakernel plan: 8 ints per layer (kind, conv mode, N tile, tasks, split-K,
+ * k-blocks, arch op index, fused avgpool); returns the layer count. */
+int cw_rt_plan_layers(cw_runtime* rt, int arch_id, int batch, int32_t* out8, int max_layers);
 /* Copy to/from a workspace activation buffer (parity tests of single layers). */
 int cw_rt_buffer_io(cw_runtime* rt, int arch_id, int buf, void* host, int64_t bytes,
                     int to_device);

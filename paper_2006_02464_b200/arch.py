@@ -49,6 +49,7 @@ class Layer:
     stride: int
     pad: int
     kpad: int            # stored K
+    layout: str = "rsc"  # K order: "rsc" = (r, s, c); "stem4" = (r, q, c4), see fold()
 
 
 @dataclass
@@ -97,10 +98,10 @@ def build_arch(name: str) -> ArchSpec:
     spec = ArchSpec(name)
     flops = 0
 
-    def add_layer(lname, bn, cin, cout, k, stride, pad, kpad=None):
+    def add_layer(lname, bn, cin, cout, k, stride, pad, kpad=None, layout="rsc"):
         kp = kpad if kpad is not None else k * k * cin
-        assert kp % 64 == 0, (lname, kp)
-        lay = Layer(len(spec.layers), lname, bn, cin, cout, k, stride, pad, kp)
+        assert kp % 64 == 0 or layout == "stem4", (lname, kp)
+        lay = Layer(len(spec.layers), lname, bn, cin, cout, k, stride, pad, kp, layout)
         spec.layers.append(lay)
         return lay
 
@@ -116,13 +117,16 @@ def build_arch(name: str) -> ArchSpec:
         flops += 2 * oh * ow * cout * k * k * cin
         return oh, ow
 
-    # Stem: input stage writes im2col rows (K = 7*7*3 = 147 -> 192), then a GEMM.
+    # Stem: the input stage converts fp32 NCHW to bf16 NHWC4 rows (channel 3 = 0,
+    # zero pixels either side); the 7x7/s2 conv reads overlapping 8-pixel row
+    # windows of those rows, K = 7 kernel rows x (8 pixels x 4 channels) = 224.
     h = w = 224
     spec.ops.append(_op(OP_STEM, out_buf=BUF_IM2COL, in_h=h, in_w=w, out_h=112, out_w=112,
-                        kpad=192, cin=3))
-    stem = add_layer("conv1", "bn1", 3, 64, 7, 2, 3, kpad=192)
-    spec.ops.append(_op(OP_CONV, layer=stem.index, in_buf=BUF_IM2COL, out_buf=BUF_STEM, cin=192,
-                        cout=64, relu=1, in_h=112, in_w=112, out_h=112, out_w=112, kpad=192))
+                        kpad=224, cin=3))
+    stem = add_layer("conv1", "bn1", 3, 64, 7, 2, 3, kpad=224, layout="stem4")
+    spec.ops.append(_op(OP_CONV, layer=stem.index, in_buf=BUF_IM2COL, out_buf=BUF_STEM, cin=4,
+                        cout=64, kh=7, kw=7, stride=2, pad=3, relu=1, in_h=224, in_w=224,
+                        out_h=112, out_w=112, kpad=224))
     flops += 2 * 112 * 112 * 64 * 147
     spec.ops.append(_op(OP_MAXPOOL, in_buf=BUF_STEM, out_buf=BUF_X0, cin=64, in_h=112, in_w=112,
                         out_h=56, out_w=56))
@@ -203,6 +207,8 @@ def fold(spec: ArchSpec, params: dict[str, np.ndarray]) -> list[tuple[np.ndarray
 
     Returns per layer (W [Cout][K] fp32 in the device K order, bias [Cout] fp32):
     W[co, (r*KW + s)*Cin + c] = w[co, c, r, s] * gamma/sqrt(var+eps), zero-padded to kpad.
+    Stem ("stem4"): W[co, r*32 + (s+1)*4 + c] (window pixel 0 and channel 3 are zero),
+    matching the NHWC4 row windows the stem conv reads.
     """
     out = []
     for lay in spec.layers:
@@ -219,7 +225,11 @@ def fold(spec: ArchSpec, params: dict[str, np.ndarray]) -> list[tuple[np.ndarray
             wk = (w * scale[:, None, None, None]).transpose(0, 2, 3, 1).reshape(lay.cout, -1)
             b = beta - mu * scale
         wpad = np.zeros((lay.cout, lay.kpad), np.float64)
-        wpad[:, :wk.shape[1]] = wk
+        if lay.layout == "stem4":
+            w4 = wpad.reshape(lay.cout, lay.k, 8, 4)
+            w4[:, :, 1:, :lay.cin] = wk.reshape(lay.cout, lay.k, lay.k, lay.cin)
+        else:
+            wpad[:, :wk.shape[1]] = wk
         out.append((wpad.astype(np.float32), b.astype(np.float32)))
     return out
 

@@ -26,7 +26,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall", "-I", CSRC,
           "-I", os.path.join(REPO, "include")]
-SOURCES = ["conv_tc.cu", "simt_kernels.cu", "runtime.cu", "tmap.cpp", "engine.cpp",
+SOURCES = ["mk_infer.cu", "simt_kernels.cu", "runtime.cu", "tmap.cpp", "engine.cpp",
            "capi_rt.cpp", "capi_engine.cpp"]
 
 
@@ -48,13 +48,13 @@ def _compile(src: str, force: bool) -> str:
     if force or _stale(obj, [path] + _headers()):
         lang = [] if src.endswith(".cu") else ["-x", "cu"]
         cmd = [NVCC, *ARCH, *COMMON, *lang, "-c", path, "-o", obj]
-        if src == "conv_tc.cu":
+        if src == "mk_infer.cu":
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
-        if src == "conv_tc.cu":
-            with open(os.path.join(OBJ, "conv_tc.ptxas.txt"), "w") as f:
+        if src == "mk_infer.cu":
+            with open(os.path.join(OBJ, "mk_infer.ptxas.txt"), "w") as f:
                 f.write(r.stderr)
     return obj
 

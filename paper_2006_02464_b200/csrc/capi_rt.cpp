@@ -185,39 +185,37 @@ int cw_rt_exec_window(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page, 
   return 1;
 }
 
-int cw_rt_profile_ops(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page, float* op_ms,
-                      int32_t* op_kinds, int max_ops) {
+int cw_rt_profile_layers(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page, float* end_ms,
+                         int32_t* kinds, int max_layers) {
   std::vector<float> ms;
-  std::vector<int> kinds;
-  std::string err = rt->rt.profile_ops(arch_id, batch, hdr_page, &ms, &kinds);
+  std::vector<int> k;
+  std::string err = rt->rt.profile_layers(arch_id, batch, hdr_page, &ms, &k);
   if (!err.empty()) return cw::fail(err);
   const int n = (int)ms.size();
-  for (int i = 0; i < n && i < max_ops; ++i) {
-    op_ms[i] = ms[i];
-    op_kinds[i] = kinds[i];
+  for (int i = 0; i < n && i < max_layers; ++i) {
+    end_ms[i] = ms[i];
+    kinds[i] = k[i];
   }
   return n;
 }
 
-int cw_rt_plan_ops(cw_runtime* rt, int arch_id, int batch, int32_t* out8, int max_ops) {
-  const cw::Arch* a = rt->rt.arch(arch_id);
-  if (!a) return cw::fail("unknown arch");
-  auto it = a->plans.find(batch);
-  if (it == a->plans.end()) return cw::fail("no plan for batch");
-  const auto& ops = it->second.ops;
-  for (int i = 0; i < (int)ops.size() && i < max_ops; ++i) {
-    const cw::PlanOp& po = ops[i];
+int cw_rt_plan_layers(cw_runtime* rt, int arch_id, int batch, int32_t* out8, int max_layers) {
+  const cw::Plan* p = rt->rt.plan(arch_id, batch);
+  if (!p) return cw::fail("no plan for batch");
+  const int n = (int)p->layers.size();
+  for (int i = 0; i < n && i < max_layers; ++i) {
+    const cw::MkLayer& d = p->layers[i];
     int32_t* o = out8 + 8 * i;
-    o[0] = po.kind;
-    o[1] = po.kind == cw::OP_CONV ? po.args.mode : -1;
-    o[2] = po.bn;
-    o[3] = po.m_tiles;
-    o[4] = po.kind == cw::OP_CONV ? po.args.splits : 0;
-    o[5] = po.kind == cw::OP_CONV ? po.args.stages : 0;
-    o[6] = po.kind == cw::OP_CONV ? po.args.num_kb : 0;
-    o[7] = po.kind == cw::OP_CONV ? (po.args.pool_out != nullptr) : 0;
+    o[0] = d.kind;
+    o[1] = d.kind == cw::MK_CONV ? d.mode : -1;
+    o[2] = d.bn;
+    o[3] = d.tasks;
+    o[4] = d.splits;
+    o[5] = d.num_kb;
+    o[6] = p->layer_op[i];
+    o[7] = d.pool_out != nullptr;
   }
-  return (int)ops.size();
+  return n;
 }
 
 }  // extern "C"

@@ -57,28 +57,4 @@ struct alignas(64) ExecRecord {
   volatile uint64_t t_out;
 };
 
-struct ConvArgs {
-  int mode;         // 0: A is a 2D [M][K] matrix; 1: A is an NHWC tensor (implicit GEMM)
-  int layer;        // index into the model header
-  int n_out;        // Cout
-  int num_kb;       // K / 64
-  int cin_kb;       // Cin / 64 (mode 1)
-  int kw, stride, pad;
-  int nimg, oh, ow; // output geometry (mode 1)
-  int box_w, box_h, box_n;
-  int tiles_w, tiles_h;
-  int m_total;      // mode 0 rows
-  int relu;
-  void* out;              // bf16 NHWC / [M][Cout]
-  const void* residual;   // bf16, same shape as out, or null
-  const ActionBlock* ab;
-  int stages;             // smem pipeline depth
-  int splits;             // split-K factor (grid.z)
-  int kb_per_split;
-  float* partial;         // split-K: [m_tiles*n_tiles][splits][128][BN] fp32
-  int* counters;          // split-K: [m_tiles*n_tiles], zero between launches
-  float* pool_out;        // fused global avgpool: [nimg][n_out] fp32 (tile = whole images)
-  float pool_scale;
-};
-
 }  // namespace cw

@@ -1,0 +1,73 @@
+// The INFER megakernel's plan format (host planner <-> device kernel).
+//
+// One persistent kernel per INFER runs the whole network: grid = one CTA per
+// SM, each CTA walks the plan's layers in order and executes the tasks of each
+// layer that the static round-robin assigns to it. Layers synchronise through
+// per-layer completion counters in global memory (release/acquire at gpu
+// scope) instead of kernel boundaries, so there is no per-layer launch,
+// prologue, TMEM allocation or tensor-map fetch on the critical path, and the
+// kernel sequence of an (arch, batch) plan is fixed (one
+// precompiled kernel sequence per batch size).
+//
+// Counters never reset: a plan's generation g (bumped by mk_done after every
+// non-skipped INFER) makes layer L complete when counter[L] == (g+1)*tasks[L]
+// (mod 2^32, compared wrap-safely).
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+
+#include "cw_device.h"
+
+namespace cw {
+
+enum MkKind : int32_t {
+  MK_CONV = 1,     // tcgen05 implicit-GEMM conv tile(s)
+  MK_INPUT = 2,    // fp32 NCHW request images -> bf16 NHWC4 (left/right padded rows)
+  MK_MAXPOOL = 3,  // 3x3 / stride 2 / pad 1
+  MK_AVGPOOL = 4,  // global average pool -> fp32 [b][C]
+  MK_FC = 5,       // logits = pooled . W^T + bias -> request output slots
+  MK_REDUCE = 6,   // split-K: sum fp32 partial tiles + bias (+ residual) (+ ReLU) -> bf16
+};
+
+constexpr int kMkMaxDeps = 6;
+constexpr int kMkThreads = 192;            // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue / SIMT
+constexpr uint32_t kMkATile = 128 * 128;   // A tile: 128 rows x 128 B
+constexpr int kMkPadW = 4;                 // MK_INPUT: zero pixels left of every row
+constexpr uint32_t kMkTmemCols = 512;      // two accumulators of up to 256 columns
+constexpr int kMkMaxSlots = 16;            // smem ring slots (per-layer slot size)
+constexpr uint32_t kMkBarBytes = 512;      // full/empty[16], tfull/tempty[2], tmem + gen slots
+
+struct MkLayer {
+  int32_t kind, tasks, rot, ndeps;
+  int32_t deps[kMkMaxDeps];
+  // ---- MK_CONV / MK_REDUCE geometry
+  int32_t mode;  // 0: A = [M][K] matrix; 1: A = NHWC tensor (tap-shifted boxes); 2: stem windows
+  int32_t bn, m_tiles, n_tiles, splits, kb_per_split, num_kb, cin_kb, kw, stride, pad;
+  int32_t box_w, box_h, box_n, tiles_w, tiles_h, m_total, nimg, oh, ow;
+  int32_t relu, wlayer, n_out, tmap, red_rows, kblk;  // kblk: K elements per k-block (64 or 32)
+  int32_t slots, slot_bytes, b_off;  // smem ring geometry of this layer (B tile at b_off in a slot)
+  int32_t pad0_, pad1_;
+  float pool_scale;
+  // ---- SIMT layers
+  int32_t H, W, C, OH, OW, classes, batch, red_parts;
+  void* out;              // bf16 NHWC output (conv / reduce / pools), NHWC4 (input)
+  const void* res;        // bf16 residual, same shape as out, or null
+  float* partial;         // split-K fp32 partials [tile][split][128][bn]
+  float* pool_out;        // fused global average pool [b][n_out] fp32, or null
+  const void* in;         // SIMT input
+};
+
+static_assert(sizeof(MkLayer) % 16 == 0, "MkLayer is copied to smem in 16-byte units");
+
+struct MkArgs {
+  const MkLayer* layers;
+  const CUtensorMap* tmaps;  // A-operand tensor maps (64-byte aligned, device memory)
+  int32_t n_layers;
+  uint32_t ring_bytes;       // smem ring (slots of the per-layer size)
+  const ActionBlock* ab;
+  uint32_t* counters;        // [n_layers]
+  const uint32_t* gen;
+  uint64_t* trace;           // optional [n_layers][gridDim.x] %globaltimer at layer end
+};
+
+}  // namespace cw

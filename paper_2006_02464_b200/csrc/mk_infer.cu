@@ -1,0 +1,763 @@
+// The INFER megakernel: the whole batched CNN forward of one Exec in ONE
+// persistent launch (replaces the emulated Exec wait of the reference worker,
+// pkg/src/sloserve/worker.py:273-277 `dur = exec_duration[b]; call_at(now+dur)`).
+//
+// Grid = one CTA per SM (148 on B200), 192 threads, ~200 KB of shared memory.
+// Every CTA walks the plan (mk.h) layer by layer; the tasks of a layer are
+// dealt round-robin (rotated per layer) over the CTAs. Warp roles:
+//
+//   warp 0     TMA producer. For each of the CTA's conv tasks, per k-block: the
+//              weight tile (B, K-major, from the model's paged weights through
+//              the per-model tensor map in the model header) and the activation
+//              tile (A): mode 0 a [M][K] matrix box, mode 1 a tap-shifted NHWC
+//              box (implicit GEMM; padding = TMA out-of-bounds zero fill,
+//              stride = TMA element stride), mode 2 the stem's overlapping
+//              8-pixel row windows (K = 7 rows x 32). Weight tiles of a layer's
+//              first task are issued BEFORE waiting for the layer's inputs.
+//   warp 1     tcgen05.mma issuer (one thread): M=128, N=bn, K=16 steps, fp32
+//              accumulators in TMEM, two accumulator buffers so the epilogue of
+//              task i overlaps the MMAs of task i+1.
+//   warps 2-5  epilogue: tcgen05.ld 32 lanes x 32 columns, + bias (folded
+//              BatchNorm), + residual, ReLU, bf16 NHWC stores (or fp32 split-K
+//              partials, or the fused global average pool); and the SIMT
+//              layers (input conversion, max pool, avg pool, FC + logits).
+//
+// Layer completion: after a task's stores, one epilogue thread publishes
+// counter[L] += 1 with release semantics; consumers spin with acquire loads
+// (plus an async-proxy fence before TMA reads). Waits time out (trap) rather
+// than hang the GPU if the plan were ever inconsistent.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <cstdio>
+
+#include "cw_device.h"
+#include "mk.h"
+#include "ptx.cuh"
+
+namespace cw {
+
+constexpr uint64_t kMkTimeoutNs = 2000000000ull;  // 2 s: far above any INFER
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __noinline__ void mk_timeout(int where) {
+  printf("cw megakernel: wait timeout (site %d, block %d, thread %d)\n", where, blockIdx.x,
+         threadIdx.x);
+  __trap();
+}
+
+__device__ __forceinline__ void mbar_wait_to(uint32_t bar, uint32_t parity, int site) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  if (ok) return;
+  const uint64_t t0 = globaltimer();
+  uint32_t n = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if ((++n & 1023) == 0 && globaltimer() - t0 > kMkTimeoutNs) mk_timeout(site);
+  }
+}
+
+__device__ __forceinline__ void wait_count(const uint32_t* c, uint32_t target, int site) {
+  if ((int32_t)(ld_acquire_u32(c) - target) >= 0) return;
+  const uint64_t t0 = globaltimer();
+  while ((int32_t)(ld_acquire_u32(c) - target) < 0) {
+    if (globaltimer() - t0 > kMkTimeoutNs) mk_timeout(site);
+  }
+}
+
+// Wait until every dependency layer of `d` has completed in this generation.
+__device__ __forceinline__ void wait_deps(const MkLayer& d, const MkLayer* sl,
+                                          const uint32_t* counters, uint32_t gen1, int site) {
+  for (int i = 0; i < d.ndeps; ++i) {
+    const int p = d.deps[i];
+    wait_count(counters + p, gen1 * (uint32_t)sl[p].tasks, site);
+  }
+}
+
+// UMMA shared-memory descriptor, K-major, 64-byte swizzle (rows of 32 bf16,
+// 8-row atoms 512 B apart).
+__device__ __forceinline__ uint64_t sw64_kmajor_desc(uint32_t smem_addr) {
+  return (uint64_t)((smem_addr & 0x3FFFFu) >> 4) | ((uint64_t)(512 >> 4) << 32) | (1ull << 46) |
+         (4ull << 61);
+}
+
+__device__ __forceinline__ int first_task(const MkLayer& d, int cta, int G) {
+  int t = cta - d.rot % G;
+  return t < 0 ? t + G : t;
+}
+
+// Rows of the A tile (output pixels) for one task.
+__device__ __forceinline__ uint32_t a_rows(const MkLayer& d) {
+  return d.mode == 0 ? 128u : (uint32_t)(d.box_w * d.box_h * d.box_n);
+}
+
+struct TileOrigin {
+  int m0, ow0, oh0, img0, n0;
+};
+
+__device__ __forceinline__ TileOrigin tile_origin(const MkLayer& d, int tile) {
+  TileOrigin o;
+  const int mt = tile / d.n_tiles;
+  o.n0 = (tile - mt * d.n_tiles) * d.bn;
+  o.m0 = 0;
+  o.ow0 = o.oh0 = o.img0 = 0;
+  if (d.mode == 0) {
+    o.m0 = mt * 128;
+  } else {
+    const int tw = mt % d.tiles_w;
+    const int th = (mt / d.tiles_w) % d.tiles_h;
+    const int tn = mt / (d.tiles_w * d.tiles_h);
+    o.ow0 = tw * d.box_w;
+    o.oh0 = th * d.box_h;
+    o.img0 = tn * d.box_n;
+  }
+  return o;
+}
+
+// Output row index (NHWC pixel) of accumulator row `row` in a tile; false if padding.
+__device__ __forceinline__ bool row_pixel(const MkLayer& d, const TileOrigin& o, int row,
+                                          long long* m) {
+  if (d.mode == 0) {
+    *m = (long long)o.m0 + row;
+    return *m < d.m_total;
+  }
+  const int rows = d.box_w * d.box_h * d.box_n;
+  const int wi = row % d.box_w;
+  const int t = row / d.box_w;
+  const int hi = t % d.box_h;
+  const int ni = t / d.box_h;
+  const int ow = o.ow0 + wi, oh = o.oh0 + hi, n = o.img0 + ni;
+  *m = ((long long)n * d.oh + oh) * d.ow + ow;
+  return row < rows && ow < d.ow && oh < d.oh && n < d.nimg;
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 v = __bfloat1622float2(h[i]);
+    f[2 * i] = v.x;
+    f[2 * i + 1] = v.y;
+  }
+}
+
+// ------------------------------------------------------------------ SIMT layers
+// All run on the 128 epilogue threads of every CTA (et = 0..127, G CTAs).
+
+__device__ void simt_input(const MkLayer& d, const ActionBlock* ab, int cta, int G, int et) {
+  // fp32 [C=3][H][W] per request -> bf16 [n][H][W + 2*pad][4] (pixel data at column + pad).
+  const int W4 = d.W / 4;
+  const int items = d.batch * d.H * W4;
+  const int Wp = d.W + 2 * kMkPadW;
+  uint2* out = reinterpret_cast<uint2*>(d.out);
+  const long long plane = (long long)d.H * d.W;
+  for (int it = cta * 128 + et; it < items; it += G * 128) {
+    const int w4 = it % W4;
+    const int t = it / W4;
+    const int h = t % d.H;
+    const int n = t / d.H;
+    const float* img = ab->in[n] + (long long)h * d.W + w4 * 4;
+    const float4 r = __ldcs(reinterpret_cast<const float4*>(img));
+    const float4 g = __ldcs(reinterpret_cast<const float4*>(img + plane));
+    const float4 b = __ldcs(reinterpret_cast<const float4*>(img + 2 * plane));
+    uint2* o = out + ((long long)n * d.H + h) * Wp + kMkPadW + w4 * 4;
+    uint4 p0, p1;
+    p0.x = pack_bf16x2(r.x, g.x);
+    p0.y = pack_bf16x2(b.x, 0.0f);
+    p0.z = pack_bf16x2(r.y, g.y);
+    p0.w = pack_bf16x2(b.y, 0.0f);
+    p1.x = pack_bf16x2(r.z, g.z);
+    p1.y = pack_bf16x2(b.z, 0.0f);
+    p1.z = pack_bf16x2(r.w, g.w);
+    p1.w = pack_bf16x2(b.w, 0.0f);
+    reinterpret_cast<uint4*>(o)[0] = p0;
+    reinterpret_cast<uint4*>(o)[1] = p1;
+  }
+}
+
+__device__ void simt_maxpool(const MkLayer& d, int cta, int G, int et) {
+  const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(d.in);
+  const int chunks = d.C / 8;
+  const int total = d.batch * d.OH * d.OW * chunks;
+  for (int t = cta * 128 + et; t < total; t += G * 128) {
+    const int j = t % chunks;
+    const int p = t / chunks;
+    const int ow = p % d.OW;
+    const int oh = (p / d.OW) % d.OH;
+    const int n = p / (d.OW * d.OH);
+    uint4 v[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+#pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const int ih = oh * 2 - 1 + r, iw = ow * 2 - 1 + s;
+        if (ih >= 0 && ih < d.H && iw >= 0 && iw < d.W)
+          v[r * 3 + s] = __ldcg(reinterpret_cast<const uint4*>(
+              in + (((long long)n * d.H + ih) * d.W + iw) * d.C + j * 8));
+        else
+          v[r * 3 + s] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);  // -inf
+      }
+    }
+    float m[8], f[8];
+    bf16x8_to_f32(v[0], m);
+#pragma unroll
+    for (int i = 1; i < 9; ++i) {
+      bf16x8_to_f32(v[i], f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) m[e] = fmaxf(m[e], f[e]);
+    }
+    uint4 o;
+    o.x = pack_bf16x2(m[0], m[1]);
+    o.y = pack_bf16x2(m[2], m[3]);
+    o.z = pack_bf16x2(m[4], m[5]);
+    o.w = pack_bf16x2(m[6], m[7]);
+    reinterpret_cast<uint4*>(d.out)[t] = o;
+  }
+}
+
+__device__ void simt_avgpool(const MkLayer& d, int cta, int G, int et) {
+  const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(d.in);
+  const int chunks = d.C / 8;
+  const int total = d.batch * chunks;
+  const int HW = d.H * d.W;
+  float* pooled = reinterpret_cast<float*>(d.out);
+  for (int t = cta * 128 + et; t < total; t += G * 128) {
+    const int j = t % chunks;
+    const int n = t / chunks;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, f[8];
+    const __nv_bfloat16* base = in + (long long)n * HW * d.C + j * 8;
+    for (int p = 0; p < HW; ++p) {
+      bf16x8_to_f32(__ldcg(reinterpret_cast<const uint4*>(base + (long long)p * d.C)), f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += f[e];
+    }
+    const float inv = 1.0f / (float)HW;
+    float4* o = reinterpret_cast<float4*>(pooled + (long long)n * d.C + j * 8);
+    o[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+    o[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+  }
+}
+
+// logits[n][j] = pooled[n] . W[j] + bias[j]; pooled staged in (idle) ring smem.
+// One warp per class; C % 256 == 0, C <= 2048.
+__device__ void simt_fc(const MkLayer& d, const ActionBlock* ab, const uint8_t* hdr, float* sp,
+                        int cta, int G, int et) {
+  const float* pooled = reinterpret_cast<const float*>(d.in);
+  const int nb = d.batch, C = d.C;
+  for (int i = et * 4; i < nb * C; i += 128 * 4)
+    *reinterpret_cast<float4*>(sp + i) = __ldcg(reinterpret_cast<const float4*>(pooled + i));
+  named_bar(1, 128);
+  const int warp = et >> 5, lane = et & 31;
+  const __nv_bfloat16* wbase =
+      reinterpret_cast<const __nv_bfloat16* const*>(hdr + kHdrWeightOff)[d.wlayer];
+  const float* bias = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[d.wlayer];
+  const int chunks = C / 256;
+  for (int j = cta * 4 + warp; j < d.classes; j += G * 4) {
+    const __nv_bfloat16* w = wbase + (long long)j * C;
+    float wf[64];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i < chunks) bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(w + (i * 32 + lane) * 8)),
+                                    wf + i * 8);
+    }
+    const float b = __ldg(bias + j);
+    for (int n = 0; n < nb; ++n) {
+      const float* pn = sp + n * C;
+      float acc = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i < chunks) {
+          const float4 p0 = *reinterpret_cast<const float4*>(pn + (i * 32 + lane) * 8);
+          const float4 p1 = *reinterpret_cast<const float4*>(pn + (i * 32 + lane) * 8 + 4);
+          acc += wf[i * 8 + 0] * p0.x + wf[i * 8 + 1] * p0.y + wf[i * 8 + 2] * p0.z +
+                 wf[i * 8 + 3] * p0.w + wf[i * 8 + 4] * p1.x + wf[i * 8 + 5] * p1.y +
+                 wf[i * 8 + 6] * p1.z + wf[i * 8 + 7] * p1.w;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) ab->out[n][j] = acc + b;
+    }
+  }
+}
+
+// Split-K reduction of one task: rows [part*red_rows, +red_rows) of one tile.
+__device__ void simt_reduce(const MkLayer& d, const uint8_t* hdr, int task, int et) {
+  const int R = d.red_parts;
+  const int tile = task / R;
+  const int r0 = (task - tile * R) * d.red_rows;
+  const TileOrigin o = tile_origin(d, tile);
+  const float* bias = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[d.wlayer] + o.n0;
+  const int c4n = d.bn / 4;
+  const int S = d.splits;
+  const float* part = d.partial + (size_t)tile * S * 128 * d.bn;
+  for (int idx = et; idx < d.red_rows * c4n; idx += 128) {
+    const int rr = r0 + idx / c4n;
+    const int c = (idx % c4n) * 4;
+    long long m;
+    if (!row_pixel(d, o, rr, &m)) continue;
+    float4 acc = __ldg(reinterpret_cast<const float4*>(bias + c));
+    const float* src = part + (size_t)rr * d.bn + c;
+    int z = 0;
+    for (; z + 4 <= S; z += 4) {
+      float4 p[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        p[u] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)(z + u) * 128 * d.bn));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc.x += p[u].x;
+        acc.y += p[u].y;
+        acc.z += p[u].z;
+        acc.w += p[u].w;
+      }
+    }
+    for (; z < S; ++z) {
+      const float4 p = __ldcg(reinterpret_cast<const float4*>(src + (size_t)z * 128 * d.bn));
+      acc.x += p.x;
+      acc.y += p.y;
+      acc.z += p.z;
+      acc.w += p.w;
+    }
+    const size_t oidx = (size_t)m * d.n_out + o.n0 + c;
+    if (d.res) {
+      const uint2 r = __ldcg(reinterpret_cast<const uint2*>(
+          reinterpret_cast<const __nv_bfloat16*>(d.res) + oidx));
+      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.x));
+      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&r.y));
+      acc.x += a.x;
+      acc.y += a.y;
+      acc.z += b.x;
+      acc.w += b.y;
+    }
+    if (d.relu) {
+      acc.x = fmaxf(acc.x, 0.0f);
+      acc.y = fmaxf(acc.y, 0.0f);
+      acc.z = fmaxf(acc.z, 0.0f);
+      acc.w = fmaxf(acc.w, 0.0f);
+    }
+    uint2 ov;
+    ov.x = pack_bf16x2(acc.x, acc.y);
+    ov.y = pack_bf16x2(acc.z, acc.w);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(d.out) + oidx) = ov;
+  }
+}
+
+// ------------------------------------------------------------------ the kernel
+
+__global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_constant__ MkArgs args) {
+  const ActionBlock* ab = args.ab;
+  if (ab->skip) return;  // window missed: the gate kernel already recorded the rejection
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t ring_bytes = args.ring_bytes;
+  // Layout after the ring: barriers, tmem/gen slots, bias [2][256] f32, pool scratch
+  // [128][17] f32, then the plan's layer table.
+  const uint32_t bar_full = sbase + ring_bytes;
+  const uint32_t bar_empty = bar_full + 8 * kMkMaxSlots;
+  const uint32_t bar_tfull = bar_empty + 8 * kMkMaxSlots;  // 2 x 8 B
+  const uint32_t bar_tempty = bar_tfull + 2 * 8;          // 2 x 8 B
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + ring_bytes + kMkBarBytes - 32);
+  uint32_t* gen_slot = tmem_slot + 1;
+  float* sbias = reinterpret_cast<float*>(smem + ring_bytes + kMkBarBytes);
+  float* sred = sbias + 2 * 256;
+  MkLayer* sl = reinterpret_cast<MkLayer*>(sred + 128 * 17);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int cta = blockIdx.x;
+  const int G = gridDim.x;
+  const int nl = args.n_layers;
+
+  // ---- prologue: stage the plan in smem, barriers, TMEM
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(args.layers);
+    uint4* dst = reinterpret_cast<uint4*>(sl);
+    const int n16 = nl * (int)sizeof(MkLayer) / 16;
+    for (int i = threadIdx.x; i < n16; i += kMkThreads) dst[i] = __ldg(src + i);
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMkMaxSlots; ++s) {
+      mbar_init(bar_full + 8 * s, 1);
+      mbar_init(bar_empty + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(bar_tfull + 8 * a, 1);
+      mbar_init(bar_tempty + 8 * a, 4);
+    }
+    fence_mbar_init();
+    *gen_slot = *reinterpret_cast<const volatile uint32_t*>(args.gen);
+  }
+  if (warp == 1) tmem_alloc(smem_u32(tmem_slot), kMkTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t gen1 = *gen_slot + 1u;
+  const uint8_t* hdr = ab->hdr;
+  uint32_t* counters = args.counters;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ======================= TMA producer
+      // Slots restart at 0 every layer; bit s of `par` = parity of the fills of
+      // slot s so far (fill n waits for consumption n-1). A layer whose slot
+      // geometry differs from the previous one first drains the ring.
+      uint32_t par = 0;
+      int cur_slots = 0, cur_bytes = 0;
+      for (int L = 0; L < nl; ++L) {
+        const MkLayer& d = sl[L];
+        if (d.kind != MK_CONV) continue;
+        int t = first_task(d, cta, G);
+        if (t >= d.tasks) continue;
+        const CUtensorMap* ta = args.tmaps + d.tmap;
+        const CUtensorMap* tb = reinterpret_cast<const CUtensorMap*>(hdr + d.wlayer * kTmapBytes);
+        tmap_acquire(tb);
+        tmap_prefetch(ta);
+        tmap_prefetch(tb);
+        const int ns = d.slots;
+        const uint32_t sb = (uint32_t)d.slot_bytes;
+        if (ns != cur_slots || d.slot_bytes != cur_bytes) {
+          for (int s = 0; s < cur_slots; ++s) mbar_wait_to(bar_empty + 8 * s, ((par >> s) & 1) ^ 1, 1);
+          cur_slots = ns;
+          cur_bytes = d.slot_bytes;
+        }
+        const uint32_t a_bytes = a_rows(d) * (uint32_t)d.kblk * 2u;
+        const uint32_t tx = a_bytes + (uint32_t)d.bn * (uint32_t)d.kblk * 2u;
+        int slot = 0;
+        bool waited = false;
+        for (; t < d.tasks; t += G) {
+          const int tile = t / d.splits;
+          const int z = t - tile * d.splits;
+          const TileOrigin o = tile_origin(d, tile);
+          const int kb0 = z * d.kb_per_split;
+          const int kb1 = min(d.num_kb, kb0 + d.kb_per_split);
+          const int wb = o.ow0 * d.stride - d.pad;
+          const int hb = o.oh0 * d.stride - d.pad;
+          auto load_a = [&](int kb, int s) {
+            const uint32_t dst = sbase + s * sb;
+            const uint32_t full = bar_full + 8 * s;
+            if (d.mode == 0) {
+              tma_load_2d(dst, ta, full, kb * 64, o.m0);
+            } else if (d.mode == 1) {
+              const int tap = kb / d.cin_kb;
+              const int c0 = (kb - tap * d.cin_kb) * 64;
+              const int r = tap / d.kw;
+              const int q = tap - r * d.kw;
+              tma_load_4d(dst, ta, full, c0, wb + q, hb + r, o.img0);
+            } else {
+              // stem: k-block = kernel row r; window p = ow, input row oh*stride - pad + r
+              tma_load_4d(dst, ta, full, 0, o.ow0, hb + kb, o.img0);
+            }
+          };
+          auto load_b = [&](int kb, int s) {
+            const uint32_t dst = sbase + s * sb + d.b_off;
+            const uint32_t full = bar_full + 8 * s;
+            for (int j = 0; j < d.bn / 64; ++j)
+              tma_load_2d(dst + j * 64 * d.kblk * 2, tb, full, kb * d.kblk, o.n0 + 64 * j);
+          };
+          auto acquire = [&](int s) {
+            mbar_wait_to(bar_empty + 8 * s, ((par >> s) & 1) ^ 1, 3);
+            par ^= 1u << s;
+            mbar_arrive_expect_tx(bar_full + 8 * s, tx);
+          };
+          const int n = kb1 - kb0;
+          int i = 0;
+          if (!waited) {
+            // weights first (independent of the previous layers), then the inputs
+            const int pre = n < ns ? n : ns;
+            int s = slot;
+            for (int k = 0; k < pre; ++k) {
+              acquire(s);
+              load_b(kb0 + k, s);
+              if (++s == ns) s = 0;
+            }
+            wait_deps(d, sl, counters, gen1, 2);
+            fence_proxy_async();
+            waited = true;
+            for (; i < pre; ++i) {
+              load_a(kb0 + i, slot);
+              if (++slot == ns) slot = 0;
+            }
+          }
+          for (; i < n; ++i) {
+            acquire(slot);
+            load_b(kb0 + i, slot);
+            load_a(kb0 + i, slot);
+            if (++slot == ns) slot = 0;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ======================= MMA issuer
+      uint32_t par = 0;  // bit s: parity of the consumptions of slot s so far
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int L = 0; L < nl; ++L) {
+        const MkLayer& d = sl[L];
+        if (d.kind != MK_CONV) continue;
+        const uint32_t idesc = idesc_bf16_f32(128, d.bn);
+        const bool sw64 = d.kblk == 32;
+        const int ksteps = d.kblk / 16;
+        const int ns = d.slots;
+        const uint32_t sb = (uint32_t)d.slot_bytes;
+        int slot = 0;
+        for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
+          const int z = t % d.splits;
+          const int kb0 = z * d.kb_per_split;
+          const int n = min(d.num_kb, kb0 + d.kb_per_split) - kb0;
+          mbar_wait_to(bar_tempty + 8 * acc, acc_phase ^ 1, 4);
+          tc_fence_after();
+          const uint32_t dtm = tmem + acc * 256;
+          for (int i = 0; i < n; ++i) {
+            mbar_wait_to(bar_full + 8 * slot, (par >> slot) & 1, 5);
+            par ^= 1u << slot;
+            tc_fence_after();
+            const uint32_t a_addr = sbase + slot * sb;
+            const uint64_t adesc = sw64 ? sw64_kmajor_desc(a_addr) : sw128_kmajor_desc(a_addr);
+            const uint64_t bdesc = sw64 ? sw64_kmajor_desc(a_addr + d.b_off)
+                                        : sw128_kmajor_desc(a_addr + d.b_off);
+            for (int k = 0; k < ksteps; ++k)
+              mma_bf16(dtm, adesc + 2 * k, bdesc + 2 * k, idesc, (i | k) != 0);
+            mma_commit(bar_empty + 8 * slot);
+            if (++slot == ns) slot = 0;
+          }
+          mma_commit(bar_tfull + 8 * acc);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ======================= epilogue + SIMT layers (warps 2..5)
+    const int q = warp & 3;  // TMEM lane quarter
+    const int row = q * 32 + lane;
+    const int et = threadIdx.x - 64;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int L = 0; L < nl; ++L) {
+      const MkLayer& d = sl[L];
+      if (d.kind == MK_CONV) {
+        int t = first_task(d, cta, G);
+        if (t >= d.tasks) continue;
+        if (et == 0) wait_deps(d, sl, counters, gen1, 6);
+        named_bar(1, 128);
+        const float* bias_all = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[d.wlayer];
+        for (; t < d.tasks; t += G) {
+          const int tile = t / d.splits;
+          const int z = t - tile * d.splits;
+          const TileOrigin o = tile_origin(d, tile);
+          long long m;
+          const bool valid = row_pixel(d, o, row, &m);
+          const uint32_t taddr = tmem + acc * 256 + ((uint32_t)(q * 32) << 16);
+          if (d.splits > 1) {
+            mbar_wait_to(bar_tfull + 8 * acc, acc_phase, 7);
+            tc_fence_after();
+            float* mine = d.partial + ((size_t)tile * d.splits + z) * 128 * d.bn + row * d.bn;
+            for (int c = 0; c < d.bn; c += 32) {
+              uint32_t v[32];
+              tmem_ld16(taddr + c, *reinterpret_cast<uint32_t(*)[16]>(v));
+              tmem_ld16(taddr + c + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+              tmem_ld_wait();
+              float4* dst = reinterpret_cast<float4*>(mine + c);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                __stcg(dst + i, make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                            __uint_as_float(v[4 * i + 2]),
+                                            __uint_as_float(v[4 * i + 3])));
+            }
+          } else {
+            // folded-BN bias of this tile's columns, staged while the MMAs run
+            float* bias = sbias + acc * 256;
+            for (int i = et; i < d.bn; i += 128) bias[i] = __ldg(bias_all + o.n0 + i);
+            const __nv_bfloat16* res_row =
+                (d.res && valid) ? reinterpret_cast<const __nv_bfloat16*>(d.res) + m * d.n_out + o.n0
+                                 : nullptr;
+            uint4 rcur[4];
+            if (res_row) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) rcur[i] = __ldcg(reinterpret_cast<const uint4*>(res_row) + i);
+            }
+            mbar_wait_to(bar_tfull + 8 * acc, acc_phase, 8);
+            tc_fence_after();
+            named_bar(1, 128);  // bias staged
+            __nv_bfloat16* out_row =
+                d.out ? reinterpret_cast<__nv_bfloat16*>(d.out) + m * d.n_out + o.n0 : nullptr;
+            for (int c = 0; c < d.bn; c += 32) {
+              uint4 rnxt[4];
+              if (res_row && c + 32 < d.bn) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                  rnxt[i] = __ldcg(reinterpret_cast<const uint4*>(res_row + c + 32) + i);
+              }
+              uint32_t v[32];
+              tmem_ld16(taddr + c, *reinterpret_cast<uint32_t(*)[16]>(v));
+              tmem_ld16(taddr + c + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+              tmem_ld_wait();
+              float f[32];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float4 bb = reinterpret_cast<const float4*>(bias + c)[i];
+                f[4 * i] = __uint_as_float(v[4 * i]) + bb.x;
+                f[4 * i + 1] = __uint_as_float(v[4 * i + 1]) + bb.y;
+                f[4 * i + 2] = __uint_as_float(v[4 * i + 2]) + bb.z;
+                f[4 * i + 3] = __uint_as_float(v[4 * i + 3]) + bb.w;
+              }
+              if (res_row) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  float rf[8];
+                  bf16x8_to_f32(rcur[i], rf);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) f[8 * i + e] += rf[e];
+                }
+              }
+              if (d.relu) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) f[i] = fmaxf(f[i], 0.0f);
+              }
+              if (d.pool_out) {
+                // Deterministic in-CTA global average pool: the tile holds whole images.
+                for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                  for (int i = 0; i < 16; ++i) sred[row * 17 + i] = valid ? f[16 * h + i] : 0.0f;
+                  named_bar(1, 128);
+                  const int hw = d.oh * d.ow;
+                  if (et < 16 * d.box_n) {
+                    const int img = et >> 4, col = et & 15;
+                    float s = 0.0f;
+                    for (int r = img * hw; r < (img + 1) * hw; ++r) s += sred[r * 17 + col];
+                    if (o.img0 + img < d.nimg)
+                      d.pool_out[(size_t)(o.img0 + img) * d.n_out + o.n0 + c + 16 * h + col] =
+                          s * d.pool_scale;
+                  }
+                  named_bar(1, 128);
+                }
+              } else if (valid && out_row) {
+                uint4* op = reinterpret_cast<uint4*>(out_row + c);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  uint4 w;
+                  w.x = pack_bf16x2(f[8 * i], f[8 * i + 1]);
+                  w.y = pack_bf16x2(f[8 * i + 2], f[8 * i + 3]);
+                  w.z = pack_bf16x2(f[8 * i + 4], f[8 * i + 5]);
+                  w.w = pack_bf16x2(f[8 * i + 6], f[8 * i + 7]);
+                  op[i] = w;
+                }
+              }
+#pragma unroll
+              for (int i = 0; i < 4; ++i) rcur[i] = rnxt[i];
+            }
+          }
+          // accumulator drained: hand it back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          named_bar(1, 128);
+          if (et == 0) red_release_add(counters + L, 1u);  // cumulative over the bar.sync
+        }
+      } else {
+        // SIMT layer (every CTA takes part; MK_REDUCE: its own task list)
+        if (d.kind == MK_REDUCE && first_task(d, cta, G) >= d.tasks) continue;
+        if (et == 0) wait_deps(d, sl, counters, gen1, 9);
+        named_bar(1, 128);
+        int done = 1;
+        switch (d.kind) {
+          case MK_INPUT: simt_input(d, ab, cta, G, et); break;
+          case MK_MAXPOOL: simt_maxpool(d, cta, G, et); break;
+          case MK_AVGPOOL: simt_avgpool(d, cta, G, et); break;
+          case MK_FC: simt_fc(d, ab, hdr, reinterpret_cast<float*>(smem), cta, G, et); break;
+          case MK_REDUCE: {
+            done = 0;
+            for (int t = first_task(d, cta, G); t < d.tasks; t += G, ++done) simt_reduce(d, hdr, t, et);
+            break;
+          }
+          default: break;
+        }
+        named_bar(1, 128);
+        if (et == 0) red_release_add(counters + L, (uint32_t)done);
+      }
+      if (args.trace && et == 0) args.trace[(size_t)L * G + cta] = globaltimer();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem, kMkTmemCols);
+  }
+}
+
+// Bumps the plan generation after a completed (non-skipped) INFER and stamps Exec end.
+__global__ void mk_done_kernel(const ActionBlock* ab, uint32_t ring_mask, ExecRecord* recs,
+                               uint32_t* gen) {
+  const uint64_t i = ab->seq;
+  if (!ab->skip) *gen += 1u;
+  ExecRecord* r = &recs[i & ring_mask];
+  r->t_end = globaltimer();
+  __threadfence_system();
+  r->seq_done = i + 1;
+}
+
+// ------------------------------------------------------------------ host side
+
+cudaError_t configure_mk() {
+  return cudaFuncSetAttribute(mk_infer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              227 * 1024);
+}
+
+uint32_t mk_smem_bytes(uint32_t ring_bytes, int n_layers) {
+  return 1024 + ring_bytes + kMkBarBytes + 2 * 256 * 4 + 128 * 17 * 4 +
+         n_layers * (uint32_t)sizeof(MkLayer);
+}
+
+int mk_blocks_per_sm(uint32_t smem) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mk_infer_kernel, kMkThreads, smem) !=
+      cudaSuccess)
+    return 0;
+  return n;
+}
+
+cudaError_t launch_mk(const MkArgs& a, int grid, uint32_t smem, cudaStream_t st) {
+  mk_infer_kernel<<<grid, kMkThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+void launch_mk_done(const ActionBlock* ab, uint32_t mask, ExecRecord* recs, uint32_t* gen,
+                    cudaStream_t st) {
+  mk_done_kernel<<<1, 1, 0, st>>>(ab, mask, recs, gen);
+}
+
+}  // namespace cw

@@ -34,10 +34,14 @@ Runtime::~Runtime() {
     for (auto& [b, p] : a.plans) {
       if (p.exec) cudaGraphExecDestroy(p.exec);
       if (p.graph) cudaGraphDestroy(p.graph);
+      cudaFree(p.d_layers);
+      cudaFree(p.d_tmaps);
+      cudaFree(p.d_counters);
+      cudaFree(p.d_gen);
+      cudaFree(p.d_trace);
+      cudaFree(p.d_partial);
     }
     for (void* b : a.bufs) cudaFree(b);
-    cudaFree(a.partial);
-    cudaFree(a.counters);
   }
   for (auto& [id, bl] : blobs_) cudaFreeHost(bl.host);
   for (auto e : exec_events_) cudaEventDestroy(e);
@@ -68,9 +72,8 @@ std::string Runtime::open(int device, int64_t pages_total, int64_t page_bytes, i
   CW_TRY(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10) return std::string("sm_100a required, found ") + prop.name;
   if (!tmap_init()) return "cuTensorMapEncodeTiled unavailable";
-  CW_TRY(configure_conv_tc());
-  CW_TRY(configure_simt());
-  pdl_ = getenv("CW_NO_PDL") == nullptr;
+  CW_TRY(configure_mk());
+  num_sms_ = prop.multiProcessorCount;
   pages_total_ = pages_total;
   page_bytes_ = page_bytes;
   CW_TRY(cudaMalloc(&pool_, (size_t)(pages_total * page_bytes)));
@@ -191,7 +194,9 @@ std::string Runtime::register_arch(int id, const CwOp* ops, int n_ops, int n_lay
     if (op.out_buf < 0) continue;
     size_t bytes = 0;
     switch (op.kind) {
-      case OP_STEM: bytes = (size_t)max_b * op.out_h * op.out_w * op.kpad * 2; break;
+      case OP_STEM:  // NHWC4 rows with kMkPadW zero pixels on both sides
+        bytes = (size_t)max_b * op.in_h * (op.in_w + 2 * kMkPadW) * 4 * 2;
+        break;
       case OP_CONV: bytes = (size_t)max_b * op.out_h * op.out_w * op.cout * 2; break;
       case OP_MAXPOOL: bytes = (size_t)max_b * op.out_h * op.out_w * op.cin * 2; break;
       case OP_AVGPOOL: bytes = (size_t)max_b * op.cin * 4; break;
@@ -200,7 +205,8 @@ std::string Runtime::register_arch(int id, const CwOp* ops, int n_ops, int n_lay
     grow(op.out_buf, bytes);
     if (op.kind == OP_CONV)
       a.flops_per_image += 2.0 * op.out_h * op.out_w * op.cout * (double)op.kpad;
-    if (op.kind == OP_CONV && (op.cout % 64 != 0 || op.kpad % 64 != 0)) return "conv shape not 64-aligned";
+    if (op.kind == OP_CONV && (op.cout % 64 != 0 || (op.kpad % 64 != 0 && op.kpad != 224)))
+      return "conv shape not 64-aligned";
   }
   archs_[id] = std::move(a);
   return "";
@@ -240,173 +246,372 @@ static void box_dims(int nimg, int oh, int ow, int* bw, int* bh, int* bn) {
   *bn = n;
 }
 
-// Tile / pipeline / split-K choice for one conv at one batch size. B200: 148 SMs,
-// two 107 KB CTAs per SM when a layer has more than one wave of tiles, else one
-// CTA per SM with a deep (up to 8-stage) pipeline; split K until the grid covers
-// the SMs, keeping >= 4 k-blocks per slice.
-static void plan_conv(ConvArgs& c, int cout, int m_tiles, int* bn_out) {
-  int bn = (cout % 128 == 0) ? 128 : 64;
-  if (bn == 128 && m_tiles * (cout / 128) < 148) bn = 64;
-  const int tiles = m_tiles * (cout / bn);
-  int splits = 1;
-  if (tiles < 148) {
-    splits = std::max(1, std::min(2 * 148 / tiles, c.num_kb / 4));
-    const int per = (c.num_kb + splits - 1) / splits;
-    splits = (c.num_kb + per - 1) / per;
+// Tile width and split-K choice for one conv at one batch size, for G SMs.
+// bn: the widest N tile that still fills the SMs (a 128 x bn tile reads
+// (128 + bn) x 128 B of operands per 64-deep k-block, so wider tiles need less
+// L2 -> SM bandwidth per FLOP); layers with less than half a wave of tiles
+// and a deep K (>= 16 k-blocks: the extra reduce layer costs a few us) split K
+// (>= 4 k-blocks per slice) until the task count reaches ~G.
+static void plan_conv(MkLayer& d, int cout, int G) {
+  static const int kBn[3] = {256, 128, 64};
+  static const double kFeed[3] = {1.0, 0.85, 0.67};
+  double best = -1;
+  int bn = 64;
+  for (int i = 0; i < 3; ++i) {
+    if (cout % kBn[i]) continue;
+    const int tiles = d.m_tiles * (cout / kBn[i]);
+    const int waves = (tiles + G - 1) / G;
+    const double score = (double)tiles / (waves * G) * kFeed[i];
+    if (score > best + 1e-9) {
+      best = score;
+      bn = kBn[i];
+    }
   }
-  c.splits = splits;
-  c.kb_per_split = (c.num_kb + splits - 1) / splits;
-  const int ctas = tiles * splits;
-  const int stage_kb = bn == 64 ? 24 : (bn == 128 ? 32 : 48);
-  int stages = ctas > 148 ? (bn == 64 ? 4 : 3) : 192 / stage_kb;
-  stages = std::max(1, std::min(stages, c.kb_per_split));
-  c.stages = stages;
-  *bn_out = bn;
+  int tiles = d.m_tiles * (cout / bn);
+  int splits = 1;
+  if (2 * tiles < G && d.num_kb >= 16) {
+    bn = 64;
+    tiles = d.m_tiles * (cout / bn);
+    splits = std::max(1, std::min(G / tiles, d.num_kb / 4));
+    const int per = (d.num_kb + splits - 1) / splits;
+    splits = (d.num_kb + per - 1) / per;
+  }
+  d.bn = bn;
+  d.n_tiles = cout / bn;
+  d.splits = splits;
+  d.kb_per_split = (d.num_kb + splits - 1) / splits;
+  d.tasks = tiles * splits;
 }
+
+namespace {
+// Buffer-level hazard tracking -> per-layer dependency lists (RAW, WAR, WAW),
+// transitively reduced.
+struct DepTracker {
+  std::map<int, int> last_writer;
+  std::map<int, std::vector<int>> readers;
+  std::vector<std::vector<char>> reach;  // reach[L][p]: L (transitively) waits for p
+
+  std::string add(MkLayer& d, int L, const std::vector<int>& reads, const std::vector<int>& writes) {
+    std::vector<int> deps;
+    for (int b : reads)
+      if (last_writer.count(b)) deps.push_back(last_writer[b]);
+    for (int b : writes) {
+      if (last_writer.count(b)) deps.push_back(last_writer[b]);
+      for (int r : readers[b]) deps.push_back(r);
+    }
+    std::sort(deps.begin(), deps.end());
+    deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+    deps.erase(std::remove(deps.begin(), deps.end(), L), deps.end());
+    reach.emplace_back(L + 1, 0);
+    std::vector<int> kept;
+    for (int p : deps) {
+      bool implied = false;
+      for (int o : deps)
+        if (o > p && reach[o][p]) implied = true;
+      if (!implied) kept.push_back(p);
+    }
+    for (int p : deps) {
+      reach[L][p] = 1;
+      for (int x = 0; x < p; ++x)
+        if (reach[p][x]) reach[L][x] = 1;
+    }
+    if ((int)kept.size() > kMkMaxDeps) return "too many layer dependencies";
+    d.ndeps = (int)kept.size();
+    for (size_t i = 0; i < kept.size(); ++i) d.deps[i] = kept[i];
+    for (int b : reads) readers[b].push_back(L);
+    for (int b : writes) {
+      last_writer[b] = L;
+      readers[b].clear();
+    }
+    return "";
+  }
+};
+constexpr int kBufPartial = 1000;  // pseudo-buffer: the split-K partial workspace
+}  // namespace
 
 std::string Runtime::build_plan(Arch& a, int batch) {
   Plan& p = a.plans[batch];
   p.batch = batch;
-  p.ops.clear();
+  p.layers.clear();
+  p.layer_op.clear();
+  p.tmaps.clear();
+  const int G = num_sms_;
+  DepTracker deps;
+  size_t partial_need = 0;
+  int rot = 0;
+  std::map<int, int> producer_kind;  // buffer -> op kind that last wrote it
+  bool fc_seen = false;
+  auto push = [&](MkLayer& d, int oi, const std::vector<int>& rd,
+                  const std::vector<int>& wr) -> std::string {
+    const int L = (int)p.layers.size();
+    if (L >= kMaxLayers) return "plan has too many layers";
+    std::string err = deps.add(d, L, rd, wr);
+    if (!err.empty()) return err;
+    d.rot = rot;
+    rot = (rot + d.tasks) % G;
+    p.layers.push_back(d);
+    p.layer_op.push_back(oi);
+    return "";
+  };
   for (size_t oi = 0; oi < a.ops.size(); ++oi) {
     const CwOp& op = a.ops[oi];
-    PlanOp po;
-    po.kind = op.kind;
-    po.batch = batch;
-    po.layer = op.layer;
-    po.in_h = op.in_h;
-    po.in_w = op.in_w;
-    po.out_h = op.out_h;
-    po.out_w = op.out_w;
-    po.kpad = op.kpad;
-    po.c = op.cin;
-    po.classes = op.cout;
-    po.in = op.in_buf >= 0 ? a.bufs[op.in_buf] : nullptr;
-    po.out = op.out_buf >= 0 ? a.bufs[op.out_buf] : nullptr;
-    if (op.kind == OP_AVGPOOL && !p.ops.empty() && p.ops.back().kind == OP_CONV &&
-        p.ops.back().args.pool_out != nullptr) {
-      po.kind = -1;  // fused into the previous conv's epilogue
-    }
-    if (op.kind == OP_CONV) {
-      ConvArgs& c = po.args;
-      c.layer = op.layer;
-      c.n_out = op.cout;
-      c.num_kb = op.kpad / 64;
-      c.relu = op.relu;
-      c.out = po.out;
-      c.residual = op.res_buf >= 0 ? a.bufs[op.res_buf] : nullptr;
-      c.ab = ab_;
-      c.nimg = batch;
-      c.oh = op.out_h;
-      c.ow = op.out_w;
-      c.kw = op.kw;
-      c.stride = op.stride;
-      c.pad = op.pad;
-      // Fuse a following global average pool when one tile can hold whole images.
-      const CwOp* nxt = oi + 1 < a.ops.size() ? &a.ops[oi + 1] : nullptr;
-      const bool fuse_pool = nxt && nxt->kind == OP_AVGPOOL && nxt->in_buf == op.out_buf &&
-                             op.out_h * op.out_w <= 128 && op.cin % 64 == 0;
-      if (!fuse_pool && op.kh == 1 && op.kw == 1 && op.stride == 1 && op.pad == 0) {
-        c.mode = 0;
-        c.m_total = batch * op.out_h * op.out_w;
-        po.m_tiles = (c.m_total + 127) / 128;
-        if (!make_tmap_2d(&po.tmap, po.in, (uint64_t)op.kpad, (uint64_t)c.m_total, 128))
-          return "tensor map (2d) failed";
-      } else {
-        if (op.cin % 64) return "conv Cin must be a multiple of 64";
-        c.mode = 1;
-        c.cin_kb = op.cin / 64;
-        if (fuse_pool) {
-          c.box_w = op.out_w;
-          c.box_h = op.out_h;
-          c.box_n = std::max(1, std::min(batch, 128 / (op.out_w * op.out_h)));
-          c.pool_out = reinterpret_cast<float*>(a.bufs[nxt->out_buf]);
-          c.pool_scale = 1.0f / (float)(op.out_h * op.out_w);
-          c.out = nullptr;
+    if (fc_seen) return "the FC op must be the last op of an arch";
+    MkLayer d;
+    memset(&d, 0, sizeof(d));
+    d.batch = batch;
+    void* in = op.in_buf >= 0 ? a.bufs[op.in_buf] : nullptr;
+    void* out = op.out_buf >= 0 ? a.bufs[op.out_buf] : nullptr;
+    std::string err;
+    switch (op.kind) {
+      case OP_STEM: {
+        d.kind = MK_INPUT;
+        d.tasks = G;
+        d.H = op.in_h;
+        d.W = op.in_w;
+        d.out = out;
+        if (op.in_w % 4) return "input width must be a multiple of 4";
+        err = push(d, (int)oi, {}, {op.out_buf});
+        break;
+      }
+      case OP_CONV: {
+        d.kind = MK_CONV;
+        d.wlayer = op.layer;
+        d.n_out = op.cout;
+        d.relu = op.relu;
+        d.nimg = batch;
+        d.oh = op.out_h;
+        d.ow = op.out_w;
+        d.kw = op.kw;
+        d.stride = op.stride;
+        d.pad = op.pad;
+        d.res = op.res_buf >= 0 ? a.bufs[op.res_buf] : nullptr;
+        d.out = out;
+        const CwOp* nxt = oi + 1 < a.ops.size() ? &a.ops[oi + 1] : nullptr;
+        const bool from_stem = producer_kind.count(op.in_buf) && producer_kind[op.in_buf] == OP_STEM;
+        bool fuse_pool = nxt && nxt->kind == OP_AVGPOOL && nxt->in_buf == op.out_buf &&
+                         op.out_h * op.out_w <= 128 && !from_stem;
+        CUtensorMap tm;
+        if (from_stem) {
+          // 7x7 / stride 2 stem over the NHWC4 rows: k-block = kernel row (32 = 8 px x 4 ch)
+          if (op.kh != 7 || op.kw != 7 || op.stride != 2 || op.pad != 3 || op.kpad != 224)
+            return "unsupported stem geometry";
+          d.mode = 2;
+          d.kblk = 32;
+          d.num_kb = 7;
+          box_dims(batch, op.out_h, op.out_w, &d.box_w, &d.box_h, &d.box_n);
+          d.tiles_w = (op.out_w + d.box_w - 1) / d.box_w;
+          d.tiles_h = (op.out_h + d.box_h - 1) / d.box_h;
+          d.m_tiles = d.tiles_w * d.tiles_h * ((batch + d.box_n - 1) / d.box_n);
+          if (!make_tmap_stem(&tm, in, batch, op.in_h, op.in_w + 2 * kMkPadW, op.out_w, d.box_w,
+                              d.box_h, d.box_n))
+            return "tensor map (stem) failed";
+        } else if (!fuse_pool && op.kh == 1 && op.kw == 1 && op.stride == 1 && op.pad == 0) {
+          d.mode = 0;
+          d.kblk = 64;
+          d.num_kb = op.kpad / 64;
+          d.m_total = batch * op.out_h * op.out_w;
+          d.m_tiles = (d.m_total + 127) / 128;
+          if (!make_tmap_2d(&tm, in, (uint64_t)op.kpad, (uint64_t)d.m_total, 128))
+            return "tensor map (2d) failed";
         } else {
-          box_dims(batch, op.out_h, op.out_w, &c.box_w, &c.box_h, &c.box_n);
+          if (op.cin % 64) return "conv Cin must be a multiple of 64";
+          d.mode = 1;
+          d.kblk = 64;
+          d.num_kb = op.kpad / 64;
+          d.cin_kb = op.cin / 64;
+          if (fuse_pool) {
+            d.box_w = op.out_w;
+            d.box_h = op.out_h;
+            d.box_n = std::max(1, std::min(batch, 128 / (op.out_w * op.out_h)));
+          } else {
+            box_dims(batch, op.out_h, op.out_w, &d.box_w, &d.box_h, &d.box_n);
+          }
+          d.tiles_w = (op.out_w + d.box_w - 1) / d.box_w;
+          d.tiles_h = (op.out_h + d.box_h - 1) / d.box_h;
+          d.m_tiles = d.tiles_w * d.tiles_h * ((batch + d.box_n - 1) / d.box_n);
+          if (!make_tmap_nhwc(&tm, in, batch, op.in_h, op.in_w, op.cin, d.box_w, d.box_h, d.box_n,
+                              op.stride))
+            return "tensor map (nhwc) failed";
         }
-        c.tiles_w = (op.out_w + c.box_w - 1) / c.box_w;
-        c.tiles_h = (op.out_h + c.box_h - 1) / c.box_h;
-        const int tiles_n = (batch + c.box_n - 1) / c.box_n;
-        po.m_tiles = c.tiles_w * c.tiles_h * tiles_n;
-        if (!make_tmap_nhwc(&po.tmap, po.in, batch, op.in_h, op.in_w, op.cin, c.box_w, c.box_h,
-                            c.box_n, op.stride))
-          return "tensor map (nhwc) failed";
+        plan_conv(d, op.cout, G);
+        if (fuse_pool && d.splits > 1) {
+          // the pool runs in the epilogue of whole-image tiles: no split-K there
+          d.splits = 1;
+          d.kb_per_split = d.num_kb;
+          d.tasks = d.m_tiles * d.n_tiles;
+        }
+        if (d.mode == 2 && d.bn > 64) {
+          d.bn = 64;
+          d.n_tiles = op.cout / 64;
+          d.tasks = d.m_tiles * d.n_tiles * d.splits;
+        }
+        d.tmap = (int)p.tmaps.size();
+        p.tmaps.push_back(tm);
+        std::vector<int> rd = {op.in_buf}, wr;
+        if (fuse_pool) {
+          d.pool_out = reinterpret_cast<float*>(a.bufs[nxt->out_buf]);
+          d.pool_scale = 1.0f / (float)(op.out_h * op.out_w);
+          d.out = nullptr;
+          wr.push_back(nxt->out_buf);
+          ++oi;  // the avgpool op is done in this layer's epilogue
+        } else if (d.splits == 1) {
+          wr.push_back(op.out_buf);
+        }
+        if (d.splits > 1) {
+          wr.push_back(kBufPartial);
+          const size_t tiles = (size_t)d.m_tiles * d.n_tiles;
+          partial_need = std::max(partial_need, tiles * d.splits * 128 * d.bn * 4);
+          MkLayer r = d;
+          d.out = nullptr;
+          d.res = nullptr;
+          err = push(d, (int)oi, rd, wr);
+          if (!err.empty()) return err;
+          // the reduce: one task per (tile, row group), ~G tasks in all
+          r.kind = MK_REDUCE;
+          const int rows = d.mode == 0 ? 128 : d.box_w * d.box_h * d.box_n;
+          int parts = 1;
+          while (parts * 2 <= rows && (size_t)tiles * parts * 2 <= (size_t)G) parts *= 2;
+          r.red_rows = (rows + parts - 1) / parts;
+          r.red_parts = (rows + r.red_rows - 1) / r.red_rows;
+          r.tasks = (int)tiles * r.red_parts;
+          std::vector<int> rrd = {kBufPartial};
+          if (op.res_buf >= 0) rrd.push_back(op.res_buf);
+          err = push(r, (int)oi, rrd, {op.out_buf});
+        } else {
+          if (op.res_buf >= 0) rd.push_back(op.res_buf);
+          err = push(d, (int)oi, rd, wr);
+        }
+        break;
       }
-      plan_conv(c, op.cout, po.m_tiles, &po.bn);
-      const int tiles = po.m_tiles * (op.cout / po.bn);
-      if (c.splits > 1) {
-        if (tiles > kCounterStride) return "too many split-K tiles";
-        const size_t need = (size_t)tiles * c.splits * 128 * po.bn * 4;
-        if (need > a.partial_bytes) return "split-K workspace too small";
-        c.partial = a.partial;
-        c.counters = a.counters + oi * kCounterStride;
+      case OP_MAXPOOL: {
+        d.kind = MK_MAXPOOL;
+        d.tasks = G;
+        d.in = in;
+        d.out = out;
+        d.H = op.in_h;
+        d.W = op.in_w;
+        d.C = op.cin;
+        d.OH = op.out_h;
+        d.OW = op.out_w;
+        if (op.cin % 8) return "maxpool C must be a multiple of 8";
+        err = push(d, (int)oi, {op.in_buf}, {op.out_buf});
+        break;
       }
-    }
-    p.ops.push_back(po);
-  }
-  return "";
-}
-
-std::string Runtime::launch_ops(const Plan& p, cudaStream_t st) {
-  for (const PlanOp& po : p.ops) {
-    switch (po.kind) {
-      case OP_STEM:
-        launch_stem_im2col(ab_, po.out, po.batch, po.in_h, po.in_w, po.out_h, po.out_w, po.kpad, st);
+      case OP_AVGPOOL: {
+        d.kind = MK_AVGPOOL;
+        d.tasks = G;
+        d.in = in;
+        d.out = out;
+        d.H = op.in_h;
+        d.W = op.in_w;
+        d.C = op.cin;
+        err = push(d, (int)oi, {op.in_buf}, {op.out_buf});
         break;
-      case OP_CONV:
-        CW_TRY(launch_conv_tc(po.tmap, po.args, po.bn, po.m_tiles, st, pdl_));
+      }
+      case OP_FC: {
+        d.kind = MK_FC;
+        d.tasks = G;
+        d.in = in;
+        d.wlayer = op.layer;
+        d.C = op.cin;
+        d.classes = op.cout;
+        if (op.cin % 256 || op.cin > 2048) return "fc input features must be a multiple of 256, <= 2048";
+        fc_seen = true;
+        err = push(d, (int)oi, {op.in_buf}, {});
         break;
-      case -1:
-        break;
-      case OP_MAXPOOL:
-        launch_maxpool(ab_, po.in, po.out, po.batch, po.in_h, po.in_w, po.c, po.out_h, po.out_w, st);
-        break;
-      case OP_AVGPOOL:
-        launch_avgpool(ab_, po.in, reinterpret_cast<float*>(po.out), po.batch, po.in_h * po.in_w,
-                       po.c, st);
-        break;
-      case OP_FC:
-        launch_fc(ab_, reinterpret_cast<const float*>(po.in), po.layer, po.batch, po.c, po.classes,
-                  st);
-        break;
+      }
       default:
         return "unknown op kind";
     }
-    CW_TRY(cudaGetLastError());
+    if (!err.empty()) return err;
+    if (op.out_buf >= 0) producer_kind[op.out_buf] = op.kind;
   }
+  // ---- shared memory: the ring takes what the plan table and scratch leave; each
+  // conv layer cuts it into as many slots (A tile + B tile, 1 KB aligned) as fit.
+  const int nl = (int)p.layers.size();
+  const uint32_t cap = 227 * 1024;
+  const uint32_t fixed = mk_smem_bytes(0, nl);
+  if (fixed + 64 * 1024 > cap) return "plan too large for shared memory";
+  p.ring_bytes = (cap - fixed) / 1024 * 1024;
+  p.smem = mk_smem_bytes(p.ring_bytes, nl);
+  for (auto& d : p.layers) {
+    if (d.kind != MK_CONV) continue;
+    const uint32_t rows = d.mode == 0 ? 128u : (uint32_t)(d.box_w * d.box_h * d.box_n);
+    const uint32_t a_bytes = rows * d.kblk * 2;
+    d.b_off = (int)((a_bytes + 1023) / 1024 * 1024);
+    d.slot_bytes = (int)((d.b_off + (uint32_t)d.bn * d.kblk * 2 + 1023) / 1024 * 1024);
+    d.slots = std::min<int>(kMkMaxSlots, p.ring_bytes / d.slot_bytes);
+    if (d.slots < 2) return "ring too small for a conv tile";
+  }
+  if (fc_seen) {
+    const MkLayer& f = p.layers.back();
+    if ((size_t)batch * f.C * 4 > p.ring_bytes) return "fc staging exceeds smem";
+  }
+  if (mk_blocks_per_sm(p.smem) < 1) return "megakernel does not fit on an SM";
+  p.grid = G;
+  // ---- device copies
+  if (partial_need) {
+    CW_TRY(cudaMalloc(&p.d_partial, partial_need));
+    for (auto& d : p.layers)
+      if (d.kind == MK_CONV && d.splits > 1) d.partial = p.d_partial;
+      else if (d.kind == MK_REDUCE) d.partial = p.d_partial;
+  }
+  CW_TRY(cudaMalloc(&p.d_layers, sizeof(MkLayer) * nl));
+  CW_TRY(cudaMemcpy(p.d_layers, p.layers.data(), sizeof(MkLayer) * nl, cudaMemcpyHostToDevice));
+  CW_TRY(cudaMalloc(&p.d_tmaps, sizeof(CUtensorMap) * std::max<size_t>(1, p.tmaps.size())));
+  if (!p.tmaps.empty())
+    CW_TRY(cudaMemcpy(p.d_tmaps, p.tmaps.data(), sizeof(CUtensorMap) * p.tmaps.size(),
+                      cudaMemcpyHostToDevice));
+  CW_TRY(cudaMalloc(&p.d_counters, sizeof(uint32_t) * nl));
+  CW_TRY(cudaMemset(p.d_counters, 0, sizeof(uint32_t) * nl));
+  CW_TRY(cudaMalloc(&p.d_gen, sizeof(uint32_t)));
+  CW_TRY(cudaMemset(p.d_gen, 0, sizeof(uint32_t)));
+  CW_TRY(cudaMalloc(&p.d_trace, sizeof(uint64_t) * nl * G));
+  CW_TRY(cudaMemset(p.d_trace, 0, sizeof(uint64_t) * nl * G));
   return "";
 }
 
 std::string Runtime::capture(Arch& a, Plan& p) {
   (void)a;
+  MkArgs args{};
+  args.layers = p.d_layers;
+  args.tmaps = p.d_tmaps;
+  args.n_layers = (int)p.layers.size();
+  args.ring_bytes = p.ring_bytes;
+  args.ab = ab_;
+  args.counters = p.d_counters;
+  args.gen = p.d_gen;
+  args.trace = p.d_trace;
   CW_TRY(cudaStreamBeginCapture(s_cap_, cudaStreamCaptureModeThreadLocal));
   launch_gate(ab_, ring_, kRing - 1, ctr_, exec_recs_, s_cap_);
-  std::string err = launch_ops(p, s_cap_);
-  launch_exec_done(ab_, kRing - 1, exec_recs_, s_cap_);
+  cudaError_t le = launch_mk(args, p.grid, p.smem, s_cap_);
+  launch_mk_done(ab_, kRing - 1, exec_recs_, p.d_gen, s_cap_);
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(s_cap_, &g);
-  if (!err.empty()) return err;
+  CW_TRY(le);
   CW_TRY(e);
   p.graph = g;
   CW_TRY(cudaGraphInstantiate(&p.exec, g, 0));
-  p.launches = 2;
-  for (const PlanOp& po : p.ops) p.launches += po.kind >= 0 ? 1 : 0;
+  p.launches = 3;
   return "";
+}
+
+const Plan* Runtime::plan(int arch, int batch) const {
+  auto it = archs_.find(arch);
+  if (it == archs_.end()) return nullptr;
+  auto pit = it->second.plans.find(batch);
+  return pit == it->second.plans.end() ? nullptr : &pit->second;
 }
 
 std::string Runtime::build_plans() {
   CW_TRY(cudaSetDevice(device_));
   for (auto& [id, a] : archs_) {
     a.bufs.assign(a.buf_bytes.size(), nullptr);
-    for (size_t i = 0; i < a.buf_bytes.size(); ++i)
-      if (a.buf_bytes[i]) CW_TRY(cudaMalloc(&a.bufs[i], a.buf_bytes[i]));
-    // Split-K: at most 2*148 CTAs per split conv, 128 x 128 fp32 partial each.
-    a.partial_bytes = (size_t)2 * 148 * 128 * 128 * 4 * 2;
-    CW_TRY(cudaMalloc(&a.partial, a.partial_bytes));
-    CW_TRY(cudaMalloc(&a.counters, a.ops.size() * kCounterStride * sizeof(int)));
-    CW_TRY(cudaMemset(a.counters, 0, a.ops.size() * kCounterStride * sizeof(int)));
+    for (size_t i = 0; i < a.buf_bytes.size(); ++i) {
+      if (!a.buf_bytes[i]) continue;
+      CW_TRY(cudaMalloc(&a.bufs[i], a.buf_bytes[i]));
+      CW_TRY(cudaMemset(a.bufs[i], 0, a.buf_bytes[i]));  // NHWC4 row padding stays zero
+    }
     for (auto& [b, p] : a.plans) {
       std::string err = build_plan(a, b);
       if (!err.empty()) return err;
@@ -444,9 +649,10 @@ std::string Runtime::load_async(int blob, const int32_t* pages, int npages, int6
     const CwTensorLoc& t = b.locs[l];
     if (t.rows <= 0) continue;
     uint8_t* w = addr(t.w_off);
-    if (t.k % 64 == 0 &&
-        !make_tmap_2d(reinterpret_cast<CUtensorMap*>(hdr + l * kTmapBytes), w, t.k, t.rows, 64))
-      return "weight tensor map failed";
+    CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(hdr + l * kTmapBytes);
+    if (t.k % 64 == 0 && !make_tmap_2d(tm, w, t.k, t.rows, 64)) return "weight tensor map failed";
+    if (t.k % 64 == 32 && !make_tmap_2d_sw64(tm, w, t.k, t.rows, 64))
+      return "weight tensor map (64B swizzle) failed";
     bias_tab[l] = reinterpret_cast<const float*>(addr(t.b_off));
     w_tab[l] = w;
   }
@@ -537,47 +743,31 @@ std::string Runtime::output_async(int arch, uint64_t seq, const int32_t* slots, 
   return "";
 }
 
-std::string Runtime::profile_ops(int arch, int batch, int32_t hdr_page, std::vector<float>* ms,
-                                 std::vector<int>* kinds) {
+std::string Runtime::profile_layers(int arch, int batch, int32_t hdr_page, std::vector<float>* end_ms,
+                                    std::vector<int>* kinds) {
   CW_TRY(cudaSetDevice(device_));
-  auto it = archs_.find(arch);
-  if (it == archs_.end()) return "unknown arch";
-  auto pit = it->second.plans.find(batch);
-  if (pit == it->second.plans.end()) return "no plan for batch size";
-  const Plan& p = pit->second;
-  const uint64_t seq = exec_seq_;
-  ActionDesc& d = ring_[seq & (kRing - 1)];
-  d.seq = seq;
-  d.earliest_gt = 0;
-  d.latest_gt = ~0ull;
-  d.hdr = page_ptr(hdr_page);
-  for (int j = 0; j < kMaxBatch; ++j) {
-    d.in[j] = j < batch ? slot_in(j) : nullptr;
-    d.out[j] = j < batch ? slot_out(j) : nullptr;
-  }
-  d.batch = batch;
-  std::atomic_thread_fence(std::memory_order_seq_cst);
-  std::vector<cudaEvent_t> ev(p.ops.size() + 1);
-  for (auto& e : ev) CW_TRY(cudaEventCreate(&e));
-  launch_gate(ab_, ring_, kRing - 1, ctr_, exec_recs_, s_exec_);
-  CW_TRY(cudaEventRecord(ev[0], s_exec_));
-  for (size_t i = 0; i < p.ops.size(); ++i) {
-    Plan one;
-    one.ops.push_back(p.ops[i]);
-    std::string err = launch_ops(one, s_exec_);
-    if (!err.empty()) return err;
-    CW_TRY(cudaEventRecord(ev[i + 1], s_exec_));
-  }
-  launch_exec_done(ab_, kRing - 1, exec_recs_, s_exec_);
-  exec_seq_ = seq + 1;
+  const Plan* pp = plan(arch, batch);
+  if (!pp || !pp->exec) return "no plan for batch size";
+  const Plan& p = *pp;
+  const int nl = (int)p.layers.size();
+  CW_TRY(cudaMemsetAsync(p.d_trace, 0, sizeof(uint64_t) * nl * p.grid, s_exec_));
+  int32_t slots[kMaxBatch];
+  for (int j = 0; j < kMaxBatch; ++j) slots[j] = j;
+  uint64_t seq = 0;
+  std::string err = exec_async(arch, batch, hdr_page, slots, 0, ~0ull, -1, &seq);
+  if (!err.empty()) return err;
   CW_TRY(cudaStreamSynchronize(s_exec_));
-  ms->resize(p.ops.size());
-  kinds->resize(p.ops.size());
-  for (size_t i = 0; i < p.ops.size(); ++i) {
-    CW_TRY(cudaEventElapsedTime(&(*ms)[i], ev[i], ev[i + 1]));
-    (*kinds)[i] = p.ops[i].kind;
+  std::vector<uint64_t> tr((size_t)nl * p.grid);
+  CW_TRY(cudaMemcpy(tr.data(), p.d_trace, tr.size() * 8, cudaMemcpyDeviceToHost));
+  const uint64_t t0 = exec_record(seq)->t_start;
+  end_ms->assign(nl, 0.0f);
+  kinds->assign(nl, 0);
+  for (int L = 0; L < nl; ++L) {
+    uint64_t mx = 0;
+    for (int c = 0; c < p.grid; ++c) mx = std::max(mx, tr[(size_t)L * p.grid + c]);
+    (*end_ms)[L] = mx > t0 ? (float)((mx - t0) * 1e-6) : 0.0f;
+    (*kinds)[L] = p.layers[L].kind;
   }
-  for (auto& e : ev) cudaEventDestroy(e);
   return "";
 }
 

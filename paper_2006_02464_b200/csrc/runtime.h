@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 #include "cw_device.h"
+#include "mk.h"
 
 namespace cw {
 
@@ -43,23 +44,25 @@ struct CwTensorLoc {
   int32_t k;
 };
 
-struct PlanOp {
-  int kind = 0;  // OpKind, or -1 when fused into the previous op
-  ConvArgs args{};
-  CUtensorMap tmap{};
-  int bn = 0, m_tiles = 0;
-  int batch = 0;
-  const void* in = nullptr;
-  void* out = nullptr;
-  int in_h = 0, in_w = 0, c = 0, out_h = 0, out_w = 0, kpad = 0, layer = 0, classes = 0;
-};
-
+// One (arch, batch) INFER plan: the megakernel's layer table (mk.h) in device
+// memory, its A-operand tensor maps, completion counters and generation, and
+// the captured graph gate -> megakernel -> done.
 struct Plan {
   int batch = 0;
-  std::vector<PlanOp> ops;
+  std::vector<MkLayer> layers;
+  std::vector<int> layer_op;  // arch op index of each layer
+  std::vector<CUtensorMap> tmaps;
+  MkLayer* d_layers = nullptr;
+  CUtensorMap* d_tmaps = nullptr;
+  uint32_t* d_counters = nullptr;
+  uint32_t* d_gen = nullptr;
+  uint64_t* d_trace = nullptr;
+  float* d_partial = nullptr;
+  uint32_t ring_bytes = 0, smem = 0;
+  int grid = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  int launches = 0;  // kernels per INFER (gate + ops + exec_done)
+  int launches = 0;  // kernels per INFER (gate + megakernel + done)
 };
 
 struct Arch {
@@ -71,11 +74,7 @@ struct Arch {
   std::vector<size_t> buf_bytes;
   std::map<int, Plan> plans;
   double flops_per_image = 0;
-  float* partial = nullptr;       // split-K fp32 workspace (shared by all ops: layers run in order)
-  size_t partial_bytes = 0;
-  int* counters = nullptr;        // split-K tile counters, kCounterStride per op
 };
-constexpr int kCounterStride = 4096;
 
 struct Blob {
   int id = -1;
@@ -149,10 +148,12 @@ class Runtime {
     return out_host_ + (seq & (kRing - 1)) * (size_t)kMaxBatch * out_floats_max_;
   }
 
-  // Eager (non-graph) run of the (arch, batch) ops with CUDA events between
-  // launches on the Exec stream; per-op milliseconds (profiling / roofline).
-  std::string profile_ops(int arch, int batch, int32_t hdr_page, std::vector<float>* ms,
-                          std::vector<int>* kinds);
+  // One INFER of the (arch, batch) plan with the megakernel's per-layer trace
+  // read back: for every plan layer, the time (ms) from Exec start until its
+  // last task finished on any SM, and the layer kind (profiling / roofline).
+  std::string profile_layers(int arch, int batch, int32_t hdr_page, std::vector<float>* end_ms,
+                             std::vector<int>* kinds);
+  const Plan* plan(int arch, int batch) const;
 
   // Blocking helpers (tests, bench).
   std::string sync_all();
@@ -172,7 +173,7 @@ class Runtime {
  private:
   std::string build_plan(Arch& a, int batch);
   std::string capture(Arch& a, Plan& p);
-  std::string launch_ops(const Plan& p, cudaStream_t st);
+  int num_sms_ = 148;
 
   int device_ = -1;
   int64_t pages_total_ = 0, page_bytes_ = 0;
@@ -203,7 +204,6 @@ class Runtime {
   std::map<int, Blob> blobs_;
   int64_t gt_offset_ = 0;
   bool plans_built_ = false;
-  bool pdl_ = true;  // programmatic dependent launch between graph nodes
 };
 
 }  // namespace cw

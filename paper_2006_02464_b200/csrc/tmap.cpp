@@ -50,4 +50,34 @@ bool make_tmap_nhwc(CUtensorMap* out, const void* base, uint64_t n, uint64_t h, 
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool make_tmap_2d_sw64(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows,
+                       uint32_t box_rows) {
+  if (!tmap_init()) return false;
+  cuuint64_t dims[2] = {k, rows};
+  cuuint64_t strides[1] = {k * 2};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return g_encode(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Stem windows over NHWC4 rows (bf16 [n][h][wp][4]): element (e, p, h, n) is
+// channel e % 4 of padded pixel 2p + e / 4 of row h, i.e. window p is the 64
+// contiguous bytes starting at padded column 2p; consecutive windows overlap
+// (16-byte stride). Rows are traversed with element stride 2 (the conv stride).
+bool make_tmap_stem(CUtensorMap* out, const void* base, uint64_t n, uint64_t h, uint64_t wp,
+                    uint64_t windows, uint32_t box_w, uint32_t box_h, uint32_t box_n) {
+  if (!tmap_init()) return false;
+  cuuint64_t dims[4] = {32, windows, h, n};
+  cuuint64_t strides[3] = {16, wp * 8, h * wp * 8};
+  cuuint32_t box[4] = {32, box_w, box_h * 2, box_n};
+  cuuint32_t estr[4] = {1, 1, 2, 1};
+  return g_encode(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace cw

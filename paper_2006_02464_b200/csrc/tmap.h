@@ -18,4 +18,12 @@ bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows,
 bool make_tmap_nhwc(CUtensorMap* out, const void* base, uint64_t n, uint64_t h, uint64_t w,
                     uint64_t c, uint32_t box_w, uint32_t box_h, uint32_t box_n, uint32_t stride);
 
+// [rows][k] bf16 row-major matrix, box = 32 (k) x box_rows, 64B swizzle (stem weights).
+bool make_tmap_2d_sw64(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows,
+                       uint32_t box_rows);
+
+// Overlapping 8-pixel windows over NHWC4 rows for the 7x7/s2 stem (see tmap.cpp).
+bool make_tmap_stem(CUtensorMap* out, const void* base, uint64_t n, uint64_t h, uint64_t wp,
+                    uint64_t windows, uint32_t box_w, uint32_t box_h, uint32_t box_n);
+
 }  // namespace cw

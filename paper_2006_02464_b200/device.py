@@ -115,20 +115,25 @@ class DeviceRuntime:
               "exec_many")
         return ex, wall.value
 
-    def profile_ops(self, arch_id: int, batch: int, hdr_page: int) -> tuple[np.ndarray, np.ndarray]:
-        n = len(self.archs[arch_id].ops)
+    def profile_layers(self, arch_id: int, batch: int, hdr_page: int
+                       ) -> tuple[np.ndarray, np.ndarray]:
+        """One INFER with the megakernel trace: per plan layer, ms from Exec start
+        until the layer's last task finished, and the layer kind (MK_*)."""
+        n = 1024
         ms = np.zeros(n, np.float32)
         kinds = np.zeros(n, np.int32)
-        got = check(lib.cw_rt_profile_ops(self.h, arch_id, batch, hdr_page, ms.ctypes.data,
-                                          kinds.ctypes.data_as(C.POINTER(C.c_int32)), n),
-                    "profile_ops")
+        got = check(lib.cw_rt_profile_layers(self.h, arch_id, batch, hdr_page, ms.ctypes.data,
+                                             kinds.ctypes.data_as(C.POINTER(C.c_int32)), n),
+                    "profile_layers")
         return ms[:got], kinds[:got]
 
-    def plan_ops(self, arch_id: int, batch: int) -> np.ndarray:
-        n = len(self.archs[arch_id].ops)
+    def plan_layers(self, arch_id: int, batch: int) -> np.ndarray:
+        """[layers][8]: kind, conv mode, N tile, tasks, split-K, k-blocks, arch op, fused pool."""
+        n = 1024
         out = np.zeros((n, 8), np.int32)
-        got = check(lib.cw_rt_plan_ops(self.h, arch_id, batch,
-                                       out.ctypes.data_as(C.POINTER(C.c_int32)), n), "plan_ops")
+        got = check(lib.cw_rt_plan_layers(self.h, arch_id, batch,
+                                          out.ctypes.data_as(C.POINTER(C.c_int32)), n),
+                    "plan_layers")
         return out[:got]
 
     def buffer_io(self, arch_id: int, buf: int, arr: np.ndarray, to_device: bool):
