@@ -94,6 +94,12 @@ int cw_rt_exec_many(cw_runtime* rt, int arch_id, int batch, const int32_t* hdr_p
  * (1 conv, 2 input, 3 maxpool, 4 avgpool, 5 fc, 6 split-K reduce). Returns the layer count. */
 int cw_rt_profile_layers(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page, float* end_ms,
                          int32_t* kinds, int max_layers);
+/* Raw trace of the last cw_rt_profile_layers run: [layers + 1][SMs][4] %globaltimer
+ * values (0 = not reached): layer done, inputs ready (TMA producer), first accumulator
+ * ready (epilogue), first tile landed (MMA); the extra last row holds per SM
+ * (globaltimer, clock64) at kernel start and (globaltimer, clock64) at kernel end.
+ * Returns the word count. */
+int64_t cw_rt_last_trace(cw_runtime* rt, uint64_t* out, int64_t max_words);
 /* Megakernel plan: 8 ints per layer (kind, conv mode, N tile, tasks, split-K,
  * k-blocks, arch op index, fused avgpool); returns the layer count. */
 int cw_rt_plan_layers(cw_runtime* rt, int arch_id, int batch, int32_t* out8, int max_layers);

@@ -13,7 +13,7 @@ state_dict so the CPU oracle can load them into torchvision's own modules.
 
 Blob layout (all offsets are blob byte offsets; blob offset o lives in blob
 page o // page_bytes at in-page offset o % page_bytes):
-    [0, 32 KiB)   header, filled at LOAD with the page-resolved tensor maps
+    [0, 64 KiB)   header, filled at LOAD with the page-resolved tensor maps
     tensors       per layer: folded weights bf16 [Cout][K] (K = KH*KW*Cin,
                   tap-major / channel-minor, zero-padded to a multiple of 64),
                   folded bias fp32 [Cout]; 256-byte aligned, never straddling a page.
@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _lib
 
-HEADER_BYTES = 32768
+HEADER_BYTES = 65536
 BN_EPS = 1e-5
 
 OP_STEM, OP_CONV, OP_MAXPOOL, OP_AVGPOOL, OP_FC = 0, 1, 2, 3, 4

@@ -199,6 +199,13 @@ int cw_rt_profile_layers(cw_runtime* rt, int arch_id, int batch, int32_t hdr_pag
   return n;
 }
 
+int64_t cw_rt_last_trace(cw_runtime* rt, uint64_t* out, int64_t max_words) {
+  const auto& tr = rt->rt.last_trace();
+  const int64_t n = (int64_t)tr.size();
+  for (int64_t i = 0; i < n && i < max_words; ++i) out[i] = tr[i];
+  return n;
+}
+
 int cw_rt_plan_layers(cw_runtime* rt, int arch_id, int batch, int32_t* out8, int max_layers) {
   const cw::Plan* p = rt->rt.plan(arch_id, batch);
   if (!p) return cw::fail("no plan for batch");

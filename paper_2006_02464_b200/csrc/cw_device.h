@@ -3,10 +3,10 @@
 // Layout in HBM:
 //   * Model header: the first kHeaderBytes of a resident model's page 0. It is
 //     written by the LOAD copy (built on the host at LOAD time because it holds
-//     absolute addresses of the model's pages): one CUtensorMap per layer for
-//     the weight matrix ([Cout][KH*KW*Cin] bf16, K-major), then a table of
-//     per-layer bias pointers (fp32, folded BatchNorm shift) and raw weight
-//     pointers.
+//     absolute addresses of the model's pages): two CUtensorMaps per layer for
+//     the weight matrix ([Cout][KH*KW*Cin] bf16, K-major; 64-row boxes and
+//     min(256, Cout)-row boxes), then a table of per-layer bias pointers (fp32,
+//     folded BatchNorm shift) and raw weight pointers.
 //   * ActionBlock: one per engine in device memory, rewritten by the gate
 //     kernel at the start of every INFER from the host descriptor ring. Every
 //     kernel of the per-(arch, batch) CUDA graph reads its dynamic inputs
@@ -20,9 +20,12 @@ namespace cw {
 constexpr int kMaxLayers = 192;        // ResNet-152 has 156 (155 convs + fc)
 constexpr int kMaxBatch = 16;
 constexpr uint32_t kTmapBytes = 128;
-constexpr uint32_t kHdrBiasOff = kMaxLayers * kTmapBytes;           // const float* [kMaxLayers]
+// weight tensor maps: box 64 rows x 64 K at [0, ...), box min(256, Cout) rows at kHdrWideOff
+constexpr uint32_t kHdrWideOff = kMaxLayers * kTmapBytes;
+constexpr uint32_t kHdrBiasOff = 2 * kMaxLayers * kTmapBytes;       // const float* [kMaxLayers]
 constexpr uint32_t kHdrWeightOff = kHdrBiasOff + kMaxLayers * 8;   // const void*  [kMaxLayers]
-constexpr uint32_t kHeaderBytes = 32768;                             // reserved at blob start
+constexpr uint32_t kHeaderBytes = 65536;                             // reserved at blob start
+static_assert(kHdrWeightOff + kMaxLayers * 8 <= kHeaderBytes, "model header overflow");
 
 struct ActionBlock {
   const uint8_t* hdr;          // model header (page 0 of the model)

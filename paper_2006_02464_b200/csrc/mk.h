@@ -67,7 +67,9 @@ struct MkArgs {
   const ActionBlock* ab;
   uint32_t* counters;        // [n_layers]
   const uint32_t* gen;
-  uint64_t* trace;           // optional [n_layers][gridDim.x] %globaltimer at layer end
+  // optional [n_layers][gridDim.x][4] %globaltimer: 0 layer done (epilogue), 1 inputs
+  // ready (producer), 2 first accumulator ready (epilogue), 3 first tile landed (MMA)
+  uint64_t* trace;
 };
 
 }  // namespace cw

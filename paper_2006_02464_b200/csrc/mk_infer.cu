@@ -58,44 +58,58 @@ __device__ __noinline__ void mk_timeout(int where) {
   __trap();
 }
 
-__device__ __forceinline__ void mbar_wait_to(uint32_t bar, uint32_t parity, int site) {
+// Phase wait with a suspend-time hint: a waiting thread sleeps in hardware
+// until the phase completes (or the hint expires) instead of spinning, so the
+// four epilogue warps waiting on an accumulator do not steal issue slots from
+// the producer / MMA threads that share their SM sub-partitions.
+template <uint32_t kHintNs>
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(bar), "r"(parity)
+      : "r"(bar), "r"(parity), "n"(kHintNs)
       : "memory");
-  if (ok) return;
-  const uint64_t t0 = globaltimer();
-  uint32_t n = 0;
-  while (true) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    if (ok) return;
-    if ((++n & 1023) == 0 && globaltimer() - t0 > kMkTimeoutNs) mk_timeout(site);
-  }
+  return ok != 0;
 }
 
-__device__ __forceinline__ void wait_count(const uint32_t* c, uint32_t target, int site) {
-  if ((int32_t)(ld_acquire_u32(c) - target) >= 0) return;
+template <uint32_t kHintNs = 200>
+__device__ __forceinline__ void mbar_wait_to(uint32_t bar, uint32_t parity, int site) {
+  if (mbar_try_wait_hint<kHintNs>(bar, parity)) return;
   const uint64_t t0 = globaltimer();
-  while ((int32_t)(ld_acquire_u32(c) - target) < 0) {
+  while (!mbar_try_wait_hint<kHintNs>(bar, parity)) {
     if (globaltimer() - t0 > kMkTimeoutNs) mk_timeout(site);
   }
 }
 
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Spin with relaxed loads (an acquire load invalidates the SM's L1 every time:
+// CCTL.IVALL), then one acquire fence once the count is reached.
+__device__ __forceinline__ void wait_count(const uint32_t* c, uint32_t target, int site) {
+  if ((int32_t)(ld_relaxed_u32(c) - target) < 0) {
+    const uint64_t t0 = globaltimer();
+    while ((int32_t)(ld_relaxed_u32(c) - target) < 0) {
+      if (globaltimer() - t0 > kMkTimeoutNs) mk_timeout(site);
+    }
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
 // Wait until every dependency layer of `d` has completed in this generation.
-__device__ __forceinline__ void wait_deps(const MkLayer& d, const MkLayer* sl,
-                                          const uint32_t* counters, uint32_t gen1, int site) {
-  for (int i = 0; i < d.ndeps; ++i) {
-    const int p = d.deps[i];
+// (reads the dependency list from the smem plan: a register copy of the layer
+// indexed dynamically would be demoted to local memory)
+__device__ __forceinline__ void wait_deps(const MkLayer* sl, int L, const uint32_t* counters,
+                                          uint32_t gen1, int site) {
+  const int nd = sl[L].ndeps;
+  for (int i = 0; i < nd; ++i) {
+    const int p = sl[L].deps[i];
     wait_count(counters + p, gen1 * (uint32_t)sl[p].tasks, site);
   }
 }
@@ -177,6 +191,7 @@ __device__ void simt_input(const MkLayer& d, const ActionBlock* ab, int cta, int
   const int Wp = d.W + 2 * kMkPadW;
   uint2* out = reinterpret_cast<uint2*>(d.out);
   const long long plane = (long long)d.H * d.W;
+#pragma unroll 4
   for (int it = cta * 128 + et; it < items; it += G * 128) {
     const int w4 = it % W4;
     const int t = it / W4;
@@ -267,12 +282,20 @@ __device__ void simt_avgpool(const MkLayer& d, int cta, int G, int et) {
 // logits[n][j] = pooled[n] . W[j] + bias[j]; pooled staged in (idle) ring smem.
 // One warp per class; C % 256 == 0, C <= 2048.
 __device__ void simt_fc(const MkLayer& d, const ActionBlock* ab, const uint8_t* hdr, float* sp,
-                        int cta, int G, int et) {
+                        uint32_t bar, int cta, int G, int et) {
   const float* pooled = reinterpret_cast<const float*>(d.in);
   const int nb = d.batch, C = d.C;
-  for (int i = et * 4; i < nb * C; i += 128 * 4)
-    *reinterpret_cast<float4*>(sp + i) = __ldcg(reinterpret_cast<const float4*>(pooled + i));
-  named_bar(1, 128);
+  // one bulk async copy of the pooled features [nb][C] into shared memory
+  if (et == 0) {
+    fence_proxy_async();
+    const uint32_t bytes = (uint32_t)(nb * C * 4);
+    mbar_arrive_expect_tx(bar, bytes);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(sp)), "l"(pooled), "r"(bytes), "r"(bar)
+        : "memory");
+  }
+  mbar_wait_to<2000>(bar, 0, 10);
   const int warp = et >> 5, lane = et & 31;
   const __nv_bfloat16* wbase =
       reinterpret_cast<const __nv_bfloat16* const*>(hdr + kHdrWeightOff)[d.wlayer];
@@ -374,6 +397,12 @@ __device__ void simt_reduce(const MkLayer& d, const uint8_t* hdr, int task, int 
 __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_constant__ MkArgs args) {
   const ActionBlock* ab = args.ab;
   if (ab->skip) return;  // window missed: the gate kernel already recorded the rejection
+  uint64_t* clk_trace =
+      args.trace ? args.trace + ((size_t)args.n_layers * gridDim.x + blockIdx.x) * 4 : nullptr;
+  if (clk_trace && threadIdx.x == 0) {
+    clk_trace[0] = globaltimer();
+    clk_trace[1] = clock64();
+  }
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
@@ -385,11 +414,13 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   const uint32_t bar_empty = bar_full + 8 * kMkMaxSlots;
   const uint32_t bar_tfull = bar_empty + 8 * kMkMaxSlots;  // 2 x 8 B
   const uint32_t bar_tempty = bar_tfull + 2 * 8;          // 2 x 8 B
+  const uint32_t bar_simt = bar_tempty + 2 * 8;           // SIMT-layer bulk copies
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + ring_bytes + kMkBarBytes - 32);
   uint32_t* gen_slot = tmem_slot + 1;
   float* sbias = reinterpret_cast<float*>(smem + ring_bytes + kMkBarBytes);
   float* sred = sbias + 2 * 256;
-  MkLayer* sl = reinterpret_cast<MkLayer*>(sred + 128 * 17);
+  uint4* sstage = reinterpret_cast<uint4*>(sred + 128 * 17);  // 4 warps x 4 KB
+  MkLayer* sl = reinterpret_cast<MkLayer*>(sstage + 4 * 4096 / 16);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -413,6 +444,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
       mbar_init(bar_tfull + 8 * a, 1);
       mbar_init(bar_tempty + 8 * a, 4);
     }
+    mbar_init(bar_simt, 1);
     fence_mbar_init();
     *gen_slot = *reinterpret_cast<const volatile uint32_t*>(args.gen);
   }
@@ -434,12 +466,15 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
       uint32_t par = 0;
       int cur_slots = 0, cur_bytes = 0;
       for (int L = 0; L < nl; ++L) {
-        const MkLayer& d = sl[L];
-        if (d.kind != MK_CONV) continue;
+        if (sl[L].kind != MK_CONV) continue;
+        const MkLayer d = sl[L];  // registers: the asm memory clobbers would force re-loads
         int t = first_task(d, cta, G);
         if (t >= d.tasks) continue;
         const CUtensorMap* ta = args.tmaps + d.tmap;
-        const CUtensorMap* tb = reinterpret_cast<const CUtensorMap*>(hdr + d.wlayer * kTmapBytes);
+        // B: one TMA per k-block when the N tile spans the wide map's box (min(256, Cout) rows)
+        const bool wide = d.kblk == 64 && d.bn == min(256, d.n_out);
+        const CUtensorMap* tb = reinterpret_cast<const CUtensorMap*>(
+            hdr + (wide ? kHdrWideOff : 0) + d.wlayer * kTmapBytes);
         tmap_acquire(tb);
         tmap_prefetch(ta);
         tmap_prefetch(tb);
@@ -452,6 +487,11 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         }
         const uint32_t a_bytes = a_rows(d) * (uint32_t)d.kblk * 2u;
         const uint32_t tx = a_bytes + (uint32_t)d.bn * (uint32_t)d.kblk * 2u;
+        const uint32_t b_box = 64u * (uint32_t)d.kblk * 2u;
+        const int nbox = wide ? 1 : d.bn / 64;
+        const int cin = d.cin_kb * 64;
+        const int mode = d.mode, kw = d.kw, kblk = d.kblk;
+        const uint32_t b_off = (uint32_t)d.b_off;
         int slot = 0;
         bool waited = false;
         for (; t < d.tasks; t += G) {
@@ -462,58 +502,75 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           const int kb1 = min(d.num_kb, kb0 + d.kb_per_split);
           const int wb = o.ow0 * d.stride - d.pad;
           const int hb = o.oh0 * d.stride - d.pad;
-          auto load_a = [&](int kb, int s) {
-            const uint32_t dst = sbase + s * sb;
-            const uint32_t full = bar_full + 8 * s;
-            if (d.mode == 0) {
-              tma_load_2d(dst, ta, full, kb * 64, o.m0);
-            } else if (d.mode == 1) {
-              const int tap = kb / d.cin_kb;
-              const int c0 = (kb - tap * d.cin_kb) * 64;
-              const int r = tap / d.kw;
-              const int q = tap - r * d.kw;
-              tma_load_4d(dst, ta, full, c0, wb + q, hb + r, o.img0);
-            } else {
-              // stem: k-block = kernel row r; window p = ow, input row oh*stride - pad + r
-              tma_load_4d(dst, ta, full, 0, o.ow0, hb + kb, o.img0);
-            }
-          };
-          auto load_b = [&](int kb, int s) {
-            const uint32_t dst = sbase + s * sb + d.b_off;
-            const uint32_t full = bar_full + 8 * s;
-            for (int j = 0; j < d.bn / 64; ++j)
-              tma_load_2d(dst + j * 64 * d.kblk * 2, tb, full, kb * d.kblk, o.n0 + 64 * j);
-          };
-          auto acquire = [&](int s) {
-            mbar_wait_to(bar_empty + 8 * s, ((par >> s) & 1) ^ 1, 3);
-            par ^= 1u << s;
-            mbar_arrive_expect_tx(bar_full + 8 * s, tx);
-          };
+          // A coordinates walk k-blocks in order: (channel block, tap column q, tap row r)
+          int a_kb = kb0, a_c0 = 0, a_q = 0, a_r = 0;
+          if (d.mode == 1) {
+            const int tap = kb0 / d.cin_kb;
+            a_c0 = (kb0 - tap * d.cin_kb) * 64;
+            a_r = tap / d.kw;
+            a_q = tap - a_r * d.kw;
+          }
           const int n = kb1 - kb0;
+#define CW_ACQUIRE(s_)                                                    \
+  do {                                                                    \
+    mbar_wait_to(bar_empty + 8 * (s_), ((par >> (s_)) & 1) ^ 1, 3);      \
+    par ^= 1u << (s_);                                                    \
+    mbar_arrive_expect_tx(bar_full + 8 * (s_), tx);                       \
+  } while (0)
+#define CW_LOAD_B(kb_, s_)                                                          \
+  do {                                                                              \
+    const uint32_t dst_ = sbase + (s_) * sb + b_off;                                \
+    for (int j = 0; j < nbox; ++j)                                                  \
+      tma_load_2d(dst_ + j * b_box, tb, bar_full + 8 * (s_), (kb_) * kblk, o.n0 + 64 * j); \
+  } while (0)
+#define CW_LOAD_A(s_)                                                                  \
+  do {                                                                                 \
+    const uint32_t dst_ = sbase + (s_) * sb;                                           \
+    if (mode == 0) {                                                                   \
+      tma_load_2d(dst_, ta, bar_full + 8 * (s_), a_kb * 64, o.m0);                     \
+    } else if (mode == 1) {                                                            \
+      tma_load_4d(dst_, ta, bar_full + 8 * (s_), a_c0, wb + a_q, hb + a_r, o.img0);    \
+      a_c0 += 64;                                                                      \
+      if (a_c0 == cin) {                                                               \
+        a_c0 = 0;                                                                      \
+        if (++a_q == kw) {                                                             \
+          a_q = 0;                                                                     \
+          ++a_r;                                                                       \
+        }                                                                              \
+      }                                                                                \
+    } else {                                                                           \
+      tma_load_4d(dst_, ta, bar_full + 8 * (s_), 0, o.ow0, hb + a_kb, o.img0);         \
+    }                                                                                  \
+    ++a_kb;                                                                            \
+  } while (0)
           int i = 0;
           if (!waited) {
             // weights first (independent of the previous layers), then the inputs
             const int pre = n < ns ? n : ns;
             int s = slot;
             for (int k = 0; k < pre; ++k) {
-              acquire(s);
-              load_b(kb0 + k, s);
+              CW_ACQUIRE(s);
+              CW_LOAD_B(kb0 + k, s);
               if (++s == ns) s = 0;
             }
-            wait_deps(d, sl, counters, gen1, 2);
+            wait_deps(sl, L, counters, gen1, 2);
             fence_proxy_async();
             waited = true;
+            if (args.trace) args.trace[((size_t)L * G + cta) * 4 + 1] = globaltimer();
             for (; i < pre; ++i) {
-              load_a(kb0 + i, slot);
+              CW_LOAD_A(slot);
               if (++slot == ns) slot = 0;
             }
           }
           for (; i < n; ++i) {
-            acquire(slot);
-            load_b(kb0 + i, slot);
-            load_a(kb0 + i, slot);
+            CW_ACQUIRE(slot);
+            CW_LOAD_B(kb0 + i, slot);
+            CW_LOAD_A(slot);
             if (++slot == ns) slot = 0;
           }
+#undef CW_ACQUIRE
+#undef CW_LOAD_B
+#undef CW_LOAD_A
         }
       }
     }
@@ -524,14 +581,15 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int L = 0; L < nl; ++L) {
-        const MkLayer& d = sl[L];
-        if (d.kind != MK_CONV) continue;
+        if (sl[L].kind != MK_CONV) continue;
+        const MkLayer d = sl[L];
         const uint32_t idesc = idesc_bf16_f32(128, d.bn);
         const bool sw64 = d.kblk == 32;
         const int ksteps = d.kblk / 16;
         const int ns = d.slots;
         const uint32_t sb = (uint32_t)d.slot_bytes;
         int slot = 0;
+        bool first = true;
         for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
           const int z = t % d.splits;
           const int kb0 = z * d.kb_per_split;
@@ -542,6 +600,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           for (int i = 0; i < n; ++i) {
             mbar_wait_to(bar_full + 8 * slot, (par >> slot) & 1, 5);
             par ^= 1u << slot;
+            if (first && args.trace) args.trace[((size_t)L * G + cta) * 4 + 3] = globaltimer();
+            first = false;
             tc_fence_after();
             const uint32_t a_addr = sbase + slot * sb;
             const uint64_t adesc = sw64 ? sw64_kmajor_desc(a_addr) : sw128_kmajor_desc(a_addr);
@@ -562,17 +622,29 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     const int q = warp & 3;  // TMEM lane quarter
     const int row = q * 32 + lane;
     const int et = threadIdx.x - 64;
+    // per-warp staging: 32 rows x 128 B, 16-byte chunks XOR-swizzled by row
+    uint8_t* stg = reinterpret_cast<uint8_t*>(sstage) + (warp - 2) * 4096;
+    auto stg_chunk = [stg](int r, int c) {
+      return reinterpret_cast<uint4*>(stg + r * 128 + ((c ^ (r & 7)) << 4));
+    };
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int L = 0; L < nl; ++L) {
-      const MkLayer& d = sl[L];
-      if (d.kind == MK_CONV) {
+      if (sl[L].kind == MK_CONV) {
+        const MkLayer d = sl[L];
         int t = first_task(d, cta, G);
         if (t >= d.tasks) continue;
-        if (et == 0) wait_deps(d, sl, counters, gen1, 6);
-        named_bar(1, 128);
         const float* bias_all = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[d.wlayer];
-        for (; t < d.tasks; t += G) {
+        if (d.splits == 1) {
+          // folded-BN bias of the first task's columns (weights: no dependency)
+          const int n0 = (t / d.splits % d.n_tiles) * d.bn;
+          for (int i = et; i < d.bn; i += 128) sbias[acc * 256 + i] = __ldg(bias_all + n0 + i);
+        }
+        if (et == 0) wait_deps(sl, L, counters, gen1, 6);
+        named_bar(1, 128);
+        bool first = true;
+        int done = 0;
+        for (; t < d.tasks; t += G, ++done) {
           const int tile = t / d.splits;
           const int z = t - tile * d.splits;
           const TileOrigin o = tile_origin(d, tile);
@@ -580,102 +652,150 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           const bool valid = row_pixel(d, o, row, &m);
           const uint32_t taddr = tmem + acc * 256 + ((uint32_t)(q * 32) << 16);
           if (d.splits > 1) {
-            mbar_wait_to(bar_tfull + 8 * acc, acc_phase, 7);
+            // fp32 partial tile: 32-column chunks through the warp's staging buffer,
+            // stored row-contiguous (8 lanes x 16 B = one 128-byte line per row).
+            mbar_wait_to<2000>(bar_tfull + 8 * acc, acc_phase, 7);
             tc_fence_after();
-            float* mine = d.partial + ((size_t)tile * d.splits + z) * 128 * d.bn + row * d.bn;
+            float* part = d.partial + ((size_t)tile * d.splits + z) * 128 * d.bn;
             for (int c = 0; c < d.bn; c += 32) {
               uint32_t v[32];
               tmem_ld16(taddr + c, *reinterpret_cast<uint32_t(*)[16]>(v));
               tmem_ld16(taddr + c + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
               tmem_ld_wait();
-              float4* dst = reinterpret_cast<float4*>(mine + c);
 #pragma unroll
-              for (int i = 0; i < 8; ++i)
-                __stcg(dst + i, make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                            __uint_as_float(v[4 * i + 2]),
-                                            __uint_as_float(v[4 * i + 3])));
+              for (int k = 0; k < 8; ++k)
+                *stg_chunk(lane, k) = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+              __syncwarp();
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int r = i * 4 + (lane >> 3);
+                __stcg(reinterpret_cast<uint4*>(part + (size_t)(q * 32 + r) * d.bn + c) + (lane & 7),
+                       *stg_chunk(r, lane & 7));
+              }
+              __syncwarp();
             }
           } else {
             // folded-BN bias of this tile's columns, staged while the MMAs run
             float* bias = sbias + acc * 256;
-            for (int i = et; i < d.bn; i += 128) bias[i] = __ldg(bias_all + o.n0 + i);
-            const __nv_bfloat16* res_row =
-                (d.res && valid) ? reinterpret_cast<const __nv_bfloat16*>(d.res) + m * d.n_out + o.n0
-                                 : nullptr;
-            uint4 rcur[4];
-            if (res_row) {
+            if (done > 0)
+              for (int i = et; i < d.bn; i += 128) bias[i] = __ldg(bias_all + o.n0 + i);
+            if (d.pool_out) {
+              // Last conv: + bias (+ residual), ReLU, then a deterministic in-CTA
+              // global average pool (the tile holds whole images).
+              const __nv_bfloat16* res_row =
+                  (d.res && valid) ? reinterpret_cast<const __nv_bfloat16*>(d.res) + m * d.n_out + o.n0
+                                   : nullptr;
+              mbar_wait_to<2000>(bar_tfull + 8 * acc, acc_phase, 8);
+              tc_fence_after();
+              named_bar(1, 128);  // bias staged
+              for (int c = 0; c < d.bn; c += 16) {
+                uint32_t v[16];
+                tmem_ld16(taddr + c, v);
+                tmem_ld_wait();
+                float f[16];
 #pragma unroll
-              for (int i = 0; i < 4; ++i) rcur[i] = __ldcg(reinterpret_cast<const uint4*>(res_row) + i);
-            }
-            mbar_wait_to(bar_tfull + 8 * acc, acc_phase, 8);
-            tc_fence_after();
-            named_bar(1, 128);  // bias staged
-            __nv_bfloat16* out_row =
-                d.out ? reinterpret_cast<__nv_bfloat16*>(d.out) + m * d.n_out + o.n0 : nullptr;
-            for (int c = 0; c < d.bn; c += 32) {
-              uint4 rnxt[4];
-              if (res_row && c + 32 < d.bn) {
+                for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(v[i]) + bias[c + i];
+                if (res_row) {
+                  float rf[8];
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                  rnxt[i] = __ldcg(reinterpret_cast<const uint4*>(res_row + c + 32) + i);
+                  for (int h = 0; h < 2; ++h) {
+                    bf16x8_to_f32(__ldcg(reinterpret_cast<const uint4*>(res_row + c) + h), rf);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) f[8 * h + e] += rf[e];
+                  }
+                }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                  if (d.relu) f[i] = fmaxf(f[i], 0.0f);
+                  sred[row * 17 + i] = valid ? f[i] : 0.0f;
+                }
+                named_bar(1, 128);
+                const int hw = d.oh * d.ow;
+                if (et < 16 * d.box_n) {
+                  const int img = et >> 4, col = et & 15;
+                  float s = 0.0f;
+                  for (int r = img * hw; r < (img + 1) * hw; ++r) s += sred[r * 17 + col];
+                  if (o.img0 + img < d.nimg)
+                    d.pool_out[(size_t)(o.img0 + img) * d.n_out + o.n0 + c + col] = s * d.pool_scale;
+                }
+                named_bar(1, 128);
               }
-              uint32_t v[32];
-              tmem_ld16(taddr + c, *reinterpret_cast<uint32_t(*)[16]>(v));
-              tmem_ld16(taddr + c + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
-              tmem_ld_wait();
-              float f[32];
+            } else {
+              // 64-column chunks: accumulators (+ bias, + residual, ReLU) -> bf16 rows in the
+              // warp's staging buffer -> coalesced row stores (8 lanes x 16 B per 128-byte
+              // row segment). The residual chunk comes in the same coalesced way.
+              long long mr[8];
+              uint32_t vmask = 0;
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                const float4 bb = reinterpret_cast<const float4*>(bias + c)[i];
-                f[4 * i] = __uint_as_float(v[4 * i]) + bb.x;
-                f[4 * i + 1] = __uint_as_float(v[4 * i + 1]) + bb.y;
-                f[4 * i + 2] = __uint_as_float(v[4 * i + 2]) + bb.z;
-                f[4 * i + 3] = __uint_as_float(v[4 * i + 3]) + bb.w;
+                long long mm;
+                if (row_pixel(d, o, q * 32 + i * 4 + (lane >> 3), &mm)) vmask |= 1u << i;
+                mr[i] = mm;
               }
-              if (res_row) {
+              const int ch = lane & 7;
+              const __nv_bfloat16* res = reinterpret_cast<const __nv_bfloat16*>(d.res);
+              __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(d.out);
+              uint4 rr[8];
+              if (res) {
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  float rf[8];
-                  bf16x8_to_f32(rcur[i], rf);
-#pragma unroll
-                  for (int e = 0; e < 8; ++e) f[8 * i + e] += rf[e];
-                }
+                for (int i = 0; i < 8; ++i)
+                  if (vmask >> i & 1)
+                    rr[i] = __ldcg(reinterpret_cast<const uint4*>(res + mr[i] * d.n_out + o.n0) + ch);
               }
-              if (d.relu) {
+              mbar_wait_to<2000>(bar_tfull + 8 * acc, acc_phase, 8);
+              tc_fence_after();
+              if (first && et == 0 && args.trace)
+                args.trace[((size_t)L * G + cta) * 4 + 2] = globaltimer();
+              first = false;
+              named_bar(1, 128);  // bias staged
+              for (int c = 0; c < d.bn; c += 64) {
+                uint32_t v[64];
+                tmem_ld16(taddr + c, *reinterpret_cast<uint32_t(*)[16]>(v));
+                tmem_ld16(taddr + c + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+                tmem_ld16(taddr + c + 32, *reinterpret_cast<uint32_t(*)[16]>(v + 32));
+                tmem_ld16(taddr + c + 48, *reinterpret_cast<uint32_t(*)[16]>(v + 48));
+                if (res) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) f[i] = fmaxf(f[i], 0.0f);
-              }
-              if (d.pool_out) {
-                // Deterministic in-CTA global average pool: the tile holds whole images.
-                for (int h = 0; h < 2; ++h) {
+                  for (int i = 0; i < 8; ++i) *stg_chunk(i * 4 + (lane >> 3), ch) = rr[i];
+                  if (c + 64 < d.bn) {
 #pragma unroll
-                  for (int i = 0; i < 16; ++i) sred[row * 17 + i] = valid ? f[16 * h + i] : 0.0f;
-                  named_bar(1, 128);
-                  const int hw = d.oh * d.ow;
-                  if (et < 16 * d.box_n) {
-                    const int img = et >> 4, col = et & 15;
-                    float s = 0.0f;
-                    for (int r = img * hw; r < (img + 1) * hw; ++r) s += sred[r * 17 + col];
-                    if (o.img0 + img < d.nimg)
-                      d.pool_out[(size_t)(o.img0 + img) * d.n_out + o.n0 + c + 16 * h + col] =
-                          s * d.pool_scale;
+                    for (int i = 0; i < 8; ++i)
+                      if (vmask >> i & 1)
+                        rr[i] = __ldcg(reinterpret_cast<const uint4*>(res + mr[i] * d.n_out + o.n0 + c + 64) + ch);
                   }
-                  named_bar(1, 128);
                 }
-              } else if (valid && out_row) {
-                uint4* op = reinterpret_cast<uint4*>(out_row + c);
+                tmem_ld_wait();
+                __syncwarp();
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
+                for (int k = 0; k < 8; ++k) {
+                  float f[8];
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[8 * k + e]) + bias[c + 8 * k + e];
+                  if (res) {
+                    float rf[8];
+                    bf16x8_to_f32(*stg_chunk(lane, k), rf);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) f[e] += rf[e];
+                  }
+                  if (d.relu) {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) f[e] = fmaxf(f[e], 0.0f);
+                  }
                   uint4 w;
-                  w.x = pack_bf16x2(f[8 * i], f[8 * i + 1]);
-                  w.y = pack_bf16x2(f[8 * i + 2], f[8 * i + 3]);
-                  w.z = pack_bf16x2(f[8 * i + 4], f[8 * i + 5]);
-                  w.w = pack_bf16x2(f[8 * i + 6], f[8 * i + 7]);
-                  op[i] = w;
+                  w.x = pack_bf16x2(f[0], f[1]);
+                  w.y = pack_bf16x2(f[2], f[3]);
+                  w.z = pack_bf16x2(f[4], f[5]);
+                  w.w = pack_bf16x2(f[6], f[7]);
+                  *stg_chunk(lane, k) = w;
                 }
-              }
+                __syncwarp();
 #pragma unroll
-              for (int i = 0; i < 4; ++i) rcur[i] = rnxt[i];
+                for (int i = 0; i < 8; ++i)
+                  if (vmask >> i & 1)
+                    reinterpret_cast<uint4*>(out + mr[i] * d.n_out + o.n0 + c)[ch] =
+                        *stg_chunk(i * 4 + (lane >> 3), ch);
+                __syncwarp();
+              }
             }
           }
           // accumulator drained: hand it back to the MMA warp
@@ -683,20 +803,24 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-          named_bar(1, 128);
-          if (et == 0) red_release_add(counters + L, 1u);  // cumulative over the bar.sync
         }
+        // one release per layer and CTA: all of its tasks' stores (cumulative over the bar.sync)
+        named_bar(1, 128);
+        if (et == 0) red_release_add(counters + L, (uint32_t)done);
       } else {
         // SIMT layer (every CTA takes part; MK_REDUCE: its own task list)
+        const MkLayer& d = sl[L];
         if (d.kind == MK_REDUCE && first_task(d, cta, G) >= d.tasks) continue;
-        if (et == 0) wait_deps(d, sl, counters, gen1, 9);
+        if (et == 0) wait_deps(sl, L, counters, gen1, 9);
         named_bar(1, 128);
         int done = 1;
         switch (d.kind) {
           case MK_INPUT: simt_input(d, ab, cta, G, et); break;
           case MK_MAXPOOL: simt_maxpool(d, cta, G, et); break;
           case MK_AVGPOOL: simt_avgpool(d, cta, G, et); break;
-          case MK_FC: simt_fc(d, ab, hdr, reinterpret_cast<float*>(smem), cta, G, et); break;
+          case MK_FC:
+            simt_fc(d, ab, hdr, reinterpret_cast<float*>(smem), bar_simt, cta, G, et);
+            break;
           case MK_REDUCE: {
             done = 0;
             for (int t = first_task(d, cta, G); t < d.tasks; t += G, ++done) simt_reduce(d, hdr, t, et);
@@ -707,7 +831,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         named_bar(1, 128);
         if (et == 0) red_release_add(counters + L, (uint32_t)done);
       }
-      if (args.trace && et == 0) args.trace[(size_t)L * G + cta] = globaltimer();
+      if (args.trace && et == 0) args.trace[((size_t)L * G + cta) * 4] = globaltimer();
     }
   }
   tc_fence_before();
@@ -716,6 +840,10 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     __syncwarp();
     tc_fence_after();
     tmem_dealloc(tmem, kMkTmemCols);
+  }
+  if (clk_trace && threadIdx.x == 0) {
+    clk_trace[3] = clock64();
+    clk_trace[2] = globaltimer();
   }
 }
 
@@ -738,7 +866,7 @@ cudaError_t configure_mk() {
 }
 
 uint32_t mk_smem_bytes(uint32_t ring_bytes, int n_layers) {
-  return 1024 + ring_bytes + kMkBarBytes + 2 * 256 * 4 + 128 * 17 * 4 +
+  return 1024 + ring_bytes + kMkBarBytes + 2 * 256 * 4 + 128 * 17 * 4 + 4 * 4096 +
          n_layers * (uint32_t)sizeof(MkLayer);
 }
 

@@ -246,41 +246,61 @@ static void box_dims(int nimg, int oh, int ow, int* bw, int* bh, int* bn) {
   *bn = n;
 }
 
-// Tile width and split-K choice for one conv at one batch size, for G SMs.
-// bn: the widest N tile that still fills the SMs (a 128 x bn tile reads
-// (128 + bn) x 128 B of operands per 64-deep k-block, so wider tiles need less
-// L2 -> SM bandwidth per FLOP); layers with less than half a wave of tiles
-// and a deep K (>= 16 k-blocks: the extra reduce layer costs a few us) split K
-// (>= 4 k-blocks per slice) until the task count reaches ~G.
-static void plan_conv(MkLayer& d, int cout, int G) {
+// Tile width and split-K choice for one conv at one batch size, for G SMs, from
+// a cost model with constants measured on B200 (tools/mma_probe.cu,
+// tools/tma_probe.cu, tools/epi_probe.cu):
+//   * a 64-deep k-block of tcgen05.mma (4 x K=16) costs ~0.27 us at ANY N <= 256
+//     (per-instruction cost), so FLOP efficiency grows with the N tile;
+//   * the single producer thread spends ~0.08 us per TMA it issues;
+//   * TMA feeds one SM at ~140 GB/s;
+//   * the 4-warp epilogue drains ~20 GB/s per SM (bf16 tile rows, ~3 TB/s chip);
+//   * a split-K reduce layer costs ~3 us plus its partial-tile traffic.
+// Epilogue of task i overlaps the MMAs of task i+1 (two TMEM accumulators).
+static void plan_conv(MkLayer& d, int cout, int G, bool allow_split) {
   static const int kBn[3] = {256, 128, 64};
-  static const double kFeed[3] = {1.0, 0.85, 0.67};
-  double best = -1;
-  int bn = 64;
+  const double rows = d.mode == 0 ? 128.0 : (double)(d.box_w * d.box_h * d.box_n);
+  const double a_bytes = rows * d.kblk * 2;
+  double best = 1e30;
+  int best_bn = 64, best_s = 1;
   for (int i = 0; i < 3; ++i) {
-    if (cout % kBn[i]) continue;
-    const int tiles = d.m_tiles * (cout / kBn[i]);
-    const int waves = (tiles + G - 1) / G;
-    const double score = (double)tiles / (waves * G) * kFeed[i];
-    if (score > best + 1e-9) {
-      best = score;
-      bn = kBn[i];
+    const int bn = kBn[i];
+    if (cout % bn) continue;
+    if (d.mode == 2 && bn != 64) continue;
+    const int tiles = d.m_tiles * (cout / bn);
+    const int n_tma = 1 + ((bn == std::min(256, cout) && d.kblk == 64) ? 1 : bn / 64);
+    const double t_kb = std::max({0.30, 0.08 * n_tma + 0.1, (a_bytes + bn * d.kblk * 2.0) / 140e3});
+    for (int s = 1; s <= 32; ++s) {
+      if (s > 1 && (!allow_split || d.num_kb / s < 2)) break;
+      const int per = (d.num_kb + s - 1) / s;
+      const int splits = (d.num_kb + per - 1) / per;
+      if (splits != s) continue;
+      const int tasks = tiles * s;
+      const int waves = (tasks + G - 1) / G;
+      const double t_main = per * t_kb;
+      const double t_epi = rows * bn * (s > 1 ? 4.0 : 2.0) / 20e3;
+      double t = waves * std::max(t_main, t_epi) + std::min(t_main, t_epi) + 1.5;
+      if (s > 1) t += 3.0 + (double)tiles * 128 * bn * (4.0 * s + 2.0) / (G * 40e3);
+      if (t < best - 1e-9) {
+        best = t;
+        best_bn = bn;
+        best_s = s;
+      }
     }
   }
-  int tiles = d.m_tiles * (cout / bn);
-  int splits = 1;
-  if (2 * tiles < G && d.num_kb >= 16) {
-    bn = 64;
-    tiles = d.m_tiles * (cout / bn);
-    splits = std::max(1, std::min(G / tiles, d.num_kb / 4));
-    const int per = (d.num_kb + splits - 1) / splits;
-    splits = (d.num_kb + per - 1) / per;
+  // experiment overrides (profiling only): CW_FORCE_BN, CW_FORCE_SPLIT
+  if (const char* e = getenv("CW_FORCE_BN")) {
+    const int bn = atoi(e);
+    if (bn > 0 && cout % bn == 0 && (d.mode != 2 || bn == 64)) best_bn = bn;
   }
-  d.bn = bn;
-  d.n_tiles = cout / bn;
-  d.splits = splits;
-  d.kb_per_split = (d.num_kb + splits - 1) / splits;
-  d.tasks = tiles * splits;
+  if (const char* e = getenv("CW_FORCE_SPLIT")) {
+    const int sp = atoi(e);
+    if (sp > 0 && allow_split && d.num_kb / sp >= 1) best_s = sp;
+  }
+  d.bn = best_bn;
+  d.n_tiles = cout / best_bn;
+  d.splits = best_s;
+  d.kb_per_split = (d.num_kb + best_s - 1) / best_s;
+  d.tasks = d.m_tiles * d.n_tiles * best_s;
 }
 
 namespace {
@@ -433,18 +453,8 @@ std::string Runtime::build_plan(Arch& a, int batch) {
                               op.stride))
             return "tensor map (nhwc) failed";
         }
-        plan_conv(d, op.cout, G);
-        if (fuse_pool && d.splits > 1) {
-          // the pool runs in the epilogue of whole-image tiles: no split-K there
-          d.splits = 1;
-          d.kb_per_split = d.num_kb;
-          d.tasks = d.m_tiles * d.n_tiles;
-        }
-        if (d.mode == 2 && d.bn > 64) {
-          d.bn = 64;
-          d.n_tiles = op.cout / 64;
-          d.tasks = d.m_tiles * d.n_tiles * d.splits;
-        }
+        // (the fused pool runs in the epilogue of whole-image tiles: no split-K there)
+        plan_conv(d, op.cout, G, !fuse_pool);
         d.tmap = (int)p.tmaps.size();
         p.tmaps.push_back(tm);
         std::vector<int> rd = {op.in_buf}, wr;
@@ -566,8 +576,8 @@ std::string Runtime::build_plan(Arch& a, int batch) {
   CW_TRY(cudaMemset(p.d_counters, 0, sizeof(uint32_t) * nl));
   CW_TRY(cudaMalloc(&p.d_gen, sizeof(uint32_t)));
   CW_TRY(cudaMemset(p.d_gen, 0, sizeof(uint32_t)));
-  CW_TRY(cudaMalloc(&p.d_trace, sizeof(uint64_t) * nl * G));
-  CW_TRY(cudaMemset(p.d_trace, 0, sizeof(uint64_t) * nl * G));
+  CW_TRY(cudaMalloc(&p.d_trace, sizeof(uint64_t) * (nl + 1) * G * 4));
+  CW_TRY(cudaMemset(p.d_trace, 0, sizeof(uint64_t) * (nl + 1) * G * 4));
   return "";
 }
 
@@ -650,7 +660,10 @@ std::string Runtime::load_async(int blob, const int32_t* pages, int npages, int6
     if (t.rows <= 0) continue;
     uint8_t* w = addr(t.w_off);
     CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(hdr + l * kTmapBytes);
+    CUtensorMap* tw = reinterpret_cast<CUtensorMap*>(hdr + kHdrWideOff + l * kTmapBytes);
     if (t.k % 64 == 0 && !make_tmap_2d(tm, w, t.k, t.rows, 64)) return "weight tensor map failed";
+    if (t.k % 64 == 0 && !make_tmap_2d(tw, w, t.k, t.rows, std::min(256, t.rows)))
+      return "weight tensor map (wide) failed";
     if (t.k % 64 == 32 && !make_tmap_2d_sw64(tm, w, t.k, t.rows, 64))
       return "weight tensor map (64B swizzle) failed";
     bias_tab[l] = reinterpret_cast<const float*>(addr(t.b_off));
@@ -750,21 +763,23 @@ std::string Runtime::profile_layers(int arch, int batch, int32_t hdr_page, std::
   if (!pp || !pp->exec) return "no plan for batch size";
   const Plan& p = *pp;
   const int nl = (int)p.layers.size();
-  CW_TRY(cudaMemsetAsync(p.d_trace, 0, sizeof(uint64_t) * nl * p.grid, s_exec_));
+  CW_TRY(cudaMemsetAsync(p.d_trace, 0, sizeof(uint64_t) * (nl + 1) * p.grid * 4, s_exec_));
   int32_t slots[kMaxBatch];
   for (int j = 0; j < kMaxBatch; ++j) slots[j] = j;
   uint64_t seq = 0;
   std::string err = exec_async(arch, batch, hdr_page, slots, 0, ~0ull, -1, &seq);
   if (!err.empty()) return err;
   CW_TRY(cudaStreamSynchronize(s_exec_));
-  std::vector<uint64_t> tr((size_t)nl * p.grid);
+  std::vector<uint64_t>& tr = last_trace_;
+  tr.assign((size_t)(nl + 1) * p.grid * 4, 0);
   CW_TRY(cudaMemcpy(tr.data(), p.d_trace, tr.size() * 8, cudaMemcpyDeviceToHost));
   const uint64_t t0 = exec_record(seq)->t_start;
+  last_trace_t0_ = t0;
   end_ms->assign(nl, 0.0f);
   kinds->assign(nl, 0);
   for (int L = 0; L < nl; ++L) {
     uint64_t mx = 0;
-    for (int c = 0; c < p.grid; ++c) mx = std::max(mx, tr[(size_t)L * p.grid + c]);
+    for (int c = 0; c < p.grid; ++c) mx = std::max(mx, tr[((size_t)L * p.grid + c) * 4]);
     (*end_ms)[L] = mx > t0 ? (float)((mx - t0) * 1e-6) : 0.0f;
     (*kinds)[L] = p.layers[L].kind;
   }

@@ -154,6 +154,9 @@ class Runtime {
   std::string profile_layers(int arch, int batch, int32_t hdr_page, std::vector<float>* end_ms,
                              std::vector<int>* kinds);
   const Plan* plan(int arch, int batch) const;
+  // Raw trace of the last profile_layers run ([layers][grid][4], see MkArgs::trace).
+  const std::vector<uint64_t>& last_trace() const { return last_trace_; }
+  uint64_t last_trace_t0() const { return last_trace_t0_; }
 
   // Blocking helpers (tests, bench).
   std::string sync_all();
@@ -174,6 +177,8 @@ class Runtime {
   std::string build_plan(Arch& a, int batch);
   std::string capture(Arch& a, Plan& p);
   int num_sms_ = 148;
+  std::vector<uint64_t> last_trace_;
+  uint64_t last_trace_t0_ = 0;
 
   int device_ = -1;
   int64_t pages_total_ = 0, page_bytes_ = 0;

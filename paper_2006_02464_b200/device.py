@@ -127,6 +127,20 @@ class DeviceRuntime:
                     "profile_layers")
         return ms[:got], kinds[:got]
 
+    def last_trace(self, n_layers: int) -> np.ndarray:
+        """(trace, t0, clk): trace [layers][SMs][4] ns since Exec start of the last
+        profile_layers run (-1 = not reached): layer done, inputs ready, first
+        accumulator ready, first tile landed; clk [SMs][4] = raw (globaltimer,
+        clock64) at megakernel start and (globaltimer, clock64) at its end."""
+        n = lib.cw_rt_last_trace(self.h, None, 0)
+        out = np.zeros(n, np.uint64)
+        lib.cw_rt_last_trace(self.h, out.ctypes.data, n)
+        raw = out.reshape(n_layers + 1, -1, 4).astype(np.int64)
+        clk = raw[n_layers]
+        t0 = int(clk[clk[:, 0] > 0, 0].min()) if (clk[:, 0] > 0).any() else 0
+        tr = np.where(raw[:n_layers] > 0, raw[:n_layers] - t0, -1)
+        return tr, t0, clk
+
     def plan_layers(self, arch_id: int, batch: int) -> np.ndarray:
         """[layers][8]: kind, conv mode, N tile, tasks, split-K, k-blocks, arch op, fused pool."""
         n = 1024

@@ -44,3 +44,35 @@ with DeviceRuntime(pages_total=8 * blob.pages, io_slots=16) as rt:
                   f"sp{sp:3d} kb{kb:3d} pool{pool} end {t * 1e3:8.1f} us  +{dt:6.1f} us "
                   f"{tf:7.1f} TF/s")
             prev = max(prev, t)
+
+    # Fine-grained view of the last profiled INFER: per layer, over the SMs with
+    # work, the median time of inputs-ready (producer), first-tile-landed (MMA),
+    # first-accumulator-ready (epilogue) and done, relative to the layer's start
+    # (the previous layer's end).
+    if "--detail" in sys.argv:
+        for b in batches:
+            rt.profile_layers(0, b, 0)
+            plan = rt.plan_layers(0, b)
+            tr, _, clk = rt.last_trace(len(plan))
+            ok = clk[:, 2] > clk[:, 0]
+            mhz = (clk[ok, 3] - clk[ok, 1]) / ((clk[ok, 2] - clk[ok, 0]) / 1e3)
+            print(f"SM clock during the megakernel: median {np.median(mhz):.0f} MHz "
+                  f"(min {mhz.min():.0f}, max {mhz.max():.0f}); kernel span "
+                  f"{(clk[ok, 2].max() - clk[ok, 0].min()) / 1e3:.1f} us")
+            print(f"== detail b={b}: us since previous layer end (median over SMs with work / max)")
+            prev = 0
+            for i, pl in enumerate(plan):
+                row = tr[i]
+                done = row[:, 0]
+                act = done >= 0
+                if not act.any():
+                    continue
+                def med(k):
+                    v = row[act, k]
+                    v = v[v >= 0]
+                    return (np.median(v) - prev) / 1e3 if len(v) else float("nan")
+                end = done[act].max()
+                print(f"{i:3d} {names.get(int(pl[0]), '?'):7s} tasks{int(pl[3]):5d} sms{int(act.sum()):4d} "
+                      f"in {med(1):7.1f} land {med(3):7.1f} acc {med(2):7.1f} "
+                      f"done {(np.median(done[act]) - prev) / 1e3:7.1f} / {(end - prev) / 1e3:7.1f}")
+                prev = max(prev, end)
