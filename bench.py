@@ -270,6 +270,7 @@ def run_ours(args, d: Dist) -> dict | None:
         conv_t = 0.0
         prev = 0.0
         for k, t in zip(kinds, ends):
+            t = float(t)
             if k == 1:
                 conv_t += max(0.0, t - prev)
             prev = max(prev, t)
