@@ -46,7 +46,9 @@ struct MkLayer {
   int32_t box_w, box_h, box_n, tiles_w, tiles_h, m_total, nimg, oh, ow;
   int32_t relu, wlayer, n_out, tmap, red_rows, kblk;  // kblk: K elements per k-block (64 or 32)
   int32_t slots, slot_bytes, b_off;  // smem ring geometry of this layer (B tile at b_off in a slot)
-  int32_t pad0_, pad1_;
+  // stem with fused 3x3/s2/p1 max pool: pooled columns per tile (0 = no fusion);
+  // a tile covers conv rows 2ph-1..2ph+1 and conv columns 2pw0-1..2pw0+2*pool_pw-1
+  int32_t pool_pw, pool_oh;
   float pool_scale;
   // ---- SIMT layers
   int32_t H, W, C, OH, OW, classes, batch, red_parts;
@@ -70,6 +72,7 @@ struct MkArgs {
   // optional [n_layers][gridDim.x][4] %globaltimer: 0 layer done (epilogue), 1 inputs
   // ready (producer), 2 first accumulator ready (epilogue), 3 first tile landed (MMA)
   uint64_t* trace;
+  uint32_t flags;            // experiments only (CW_MK_FLAGS): 1 no MMA, 2 no A loads, 4 no B loads
 };
 
 }  // namespace cw

@@ -75,7 +75,11 @@ __device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar, uint32_t parity
   return ok != 0;
 }
 
-template <uint32_t kHintNs = 200>
+// ptxas turns the hint into a NANOSLEEP between checks, i.e. the wake-up
+// granularity of a waiting warp.
+constexpr uint32_t kEpiWaitNs = 512;
+
+template <uint32_t kHintNs = 64>
 __device__ __forceinline__ void mbar_wait_to(uint32_t bar, uint32_t parity, int site) {
   if (mbar_try_wait_hint<kHintNs>(bar, parity)) return;
   const uint64_t t0 = globaltimer();
@@ -147,8 +151,13 @@ __device__ __forceinline__ TileOrigin tile_origin(const MkLayer& d, int tile) {
     const int tw = mt % d.tiles_w;
     const int th = (mt / d.tiles_w) % d.tiles_h;
     const int tn = mt / (d.tiles_w * d.tiles_h);
-    o.ow0 = tw * d.box_w;
-    o.oh0 = th * d.box_h;
+    if (d.pool_pw) {  // fused stem max pool: tile = pooled row th, pooled columns from tw*pool_pw
+      o.ow0 = 2 * tw * d.pool_pw - 1;
+      o.oh0 = 2 * th - 1;
+    } else {
+      o.ow0 = tw * d.box_w;
+      o.oh0 = th * d.box_h;
+    }
     o.img0 = tn * d.box_n;
   }
   return o;
@@ -168,7 +177,7 @@ __device__ __forceinline__ bool row_pixel(const MkLayer& d, const TileOrigin& o,
   const int ni = t / d.box_h;
   const int ow = o.ow0 + wi, oh = o.oh0 + hi, n = o.img0 + ni;
   *m = ((long long)n * d.oh + oh) * d.ow + ow;
-  return row < rows && ow < d.ow && oh < d.oh && n < d.nimg;
+  return row < rows && ow >= 0 && oh >= 0 && ow < d.ow && oh < d.oh && n < d.nimg;
 }
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
@@ -184,7 +193,7 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
 // ------------------------------------------------------------------ SIMT layers
 // All run on the 128 epilogue threads of every CTA (et = 0..127, G CTAs).
 
-__device__ void simt_input(const MkLayer& d, const ActionBlock* ab, int cta, int G, int et) {
+__device__ __noinline__ void simt_input(const MkLayer& d, const ActionBlock* ab, int cta, int G, int et) {
   // fp32 [C=3][H][W] per request -> bf16 [n][H][W + 2*pad][4] (pixel data at column + pad).
   const int W4 = d.W / 4;
   const int items = d.batch * d.H * W4;
@@ -216,7 +225,7 @@ __device__ void simt_input(const MkLayer& d, const ActionBlock* ab, int cta, int
   }
 }
 
-__device__ void simt_maxpool(const MkLayer& d, int cta, int G, int et) {
+__device__ __noinline__ void simt_maxpool(const MkLayer& d, int cta, int G, int et) {
   const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(d.in);
   const int chunks = d.C / 8;
   const int total = d.batch * d.OH * d.OW * chunks;
@@ -256,7 +265,7 @@ __device__ void simt_maxpool(const MkLayer& d, int cta, int G, int et) {
   }
 }
 
-__device__ void simt_avgpool(const MkLayer& d, int cta, int G, int et) {
+__device__ __noinline__ void simt_avgpool(const MkLayer& d, int cta, int G, int et) {
   const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(d.in);
   const int chunks = d.C / 8;
   const int total = d.batch * chunks;
@@ -295,7 +304,7 @@ __device__ void simt_fc(const MkLayer& d, const ActionBlock* ab, const uint8_t* 
             "r"(smem_u32(sp)), "l"(pooled), "r"(bytes), "r"(bar)
         : "memory");
   }
-  mbar_wait_to<2000>(bar, 0, 10);
+  mbar_wait_to<kEpiWaitNs>(bar, 0, 10);
   const int warp = et >> 5, lane = et & 31;
   const __nv_bfloat16* wbase =
       reinterpret_cast<const __nv_bfloat16* const*>(hdr + kHdrWeightOff)[d.wlayer];
@@ -331,7 +340,7 @@ __device__ void simt_fc(const MkLayer& d, const ActionBlock* ab, const uint8_t* 
 }
 
 // Split-K reduction of one task: rows [part*red_rows, +red_rows) of one tile.
-__device__ void simt_reduce(const MkLayer& d, const uint8_t* hdr, int task, int et) {
+__device__ __noinline__ void simt_reduce(const MkLayer& d, const uint8_t* hdr, int task, int et) {
   const int R = d.red_parts;
   const int tile = task / R;
   const int r0 = (task - tile * R) * d.red_rows;
@@ -347,26 +356,34 @@ __device__ void simt_reduce(const MkLayer& d, const uint8_t* hdr, int task, int 
     if (!row_pixel(d, o, rr, &m)) continue;
     float4 acc = __ldg(reinterpret_cast<const float4*>(bias + c));
     const float* src = part + (size_t)rr * d.bn + c;
+    const size_t zs = (size_t)128 * d.bn;
     int z = 0;
-    for (; z + 4 <= S; z += 4) {
-      float4 p[4];
+    for (; z + 8 <= S; z += 8) {  // 8 independent L2 loads in flight
+      float4 p[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        p[u] = __ldcg(reinterpret_cast<const float4*>(src + (size_t)(z + u) * 128 * d.bn));
+      for (int u = 0; u < 8; ++u) p[u] = __ldcg(reinterpret_cast<const float4*>(src + (z + u) * zs));
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         acc.x += p[u].x;
         acc.y += p[u].y;
         acc.z += p[u].z;
         acc.w += p[u].w;
       }
     }
-    for (; z < S; ++z) {
-      const float4 p = __ldcg(reinterpret_cast<const float4*>(src + (size_t)z * 128 * d.bn));
-      acc.x += p.x;
-      acc.y += p.y;
-      acc.z += p.z;
-      acc.w += p.w;
+    if (z < S) {
+      float4 p[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (z + u < S) p[u] = __ldcg(reinterpret_cast<const float4*>(src + (z + u) * zs));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (z + u < S) {
+          acc.x += p[u].x;
+          acc.y += p[u].y;
+          acc.z += p[u].z;
+          acc.w += p[u].w;
+        }
+      }
     }
     const size_t oidx = (size_t)m * d.n_out + o.n0 + c;
     if (d.res) {
@@ -389,6 +406,69 @@ __device__ void simt_reduce(const MkLayer& d, const uint8_t* hdr, int task, int 
     ov.x = pack_bf16x2(acc.x, acc.y);
     ov.y = pack_bf16x2(acc.z, acc.w);
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(d.out) + oidx) = ov;
+  }
+}
+
+// Stem conv with the 3x3/s2/p1 max pool fused: the tile's conv pixels
+// (3 conv rows x 2*pool_pw+1 columns) -> bias, ReLU, bf16 into the CTA staging
+// buffer, then each pooled pixel = max over its valid 3x3 window (identical to
+// pooling the bf16 conv output; padding = -inf = skipped).
+__device__ __noinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigin o, uint32_t taddr,
+                                           const float* bias, uint8_t* pb, int row, int et) {
+  const MkLayer& d = *dp;
+              {
+    uint32_t v[64];
+    tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(v));
+    tmem_ld16(taddr + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+    tmem_ld16(taddr + 32, *reinterpret_cast<uint32_t(*)[16]>(v + 32));
+    tmem_ld16(taddr + 48, *reinterpret_cast<uint32_t(*)[16]>(v + 48));
+    tmem_ld_wait();
+    if (row < d.box_w * d.box_h) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          f[e] = fmaxf(__uint_as_float(v[8 * k + e]) + bias[8 * k + e], 0.0f);
+        uint4 w;
+        w.x = pack_bf16x2(f[0], f[1]);
+        w.y = pack_bf16x2(f[2], f[3]);
+        w.z = pack_bf16x2(f[4], f[5]);
+        w.w = pack_bf16x2(f[6], f[7]);
+        *reinterpret_cast<uint4*>(pb + row * 128 + ((k ^ (row & 7)) << 4)) = w;
+      }
+    }
+  }
+  named_bar(1, 128);
+  const int pw0 = (o.ow0 + 1) / 2, ph = (o.oh0 + 1) / 2;
+  __nv_bfloat16* pout = reinterpret_cast<__nv_bfloat16*>(d.out);
+  for (int it = et; it < d.pool_pw * 8; it += 128) {
+    const int j = it >> 3, k = it & 7;
+    if (pw0 + j >= d.OW) continue;
+    float mx[8], f[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int cr = o.oh0 + r;
+      if (cr < 0 || cr >= d.oh) continue;
+#pragma unroll
+      for (int cq = 0; cq < 3; ++cq) {
+        const int c = 2 * j + cq, cc = o.ow0 + c;
+        if (cc < 0 || cc >= d.ow) continue;
+        const int prow = r * d.box_w + c;
+        bf16x8_to_f32(*reinterpret_cast<const uint4*>(pb + prow * 128 + ((k ^ (prow & 7)) << 4)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx[e] = fmaxf(mx[e], f[e]);
+      }
+    }
+    uint4 w;
+    w.x = pack_bf16x2(mx[0], mx[1]);
+    w.y = pack_bf16x2(mx[2], mx[3]);
+    w.z = pack_bf16x2(mx[4], mx[5]);
+    w.w = pack_bf16x2(mx[6], mx[7]);
+    *reinterpret_cast<uint4*>(
+        pout + (((size_t)o.img0 * d.OH + ph) * d.OW + pw0 + j) * d.n_out + k * 8) = w;
   }
 }
 
@@ -458,8 +538,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   uint32_t* counters = args.counters;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ======================= TMA producer
+    {
+      // ======================= TMA producer (whole warp converged; one elected lane issues)
       // Slots restart at 0 every layer; bit s of `par` = parity of the fills of
       // slot s so far (fill n waits for consumption n-1). A layer whose slot
       // geometry differs from the previous one first drains the ring.
@@ -475,9 +555,12 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         const bool wide = d.kblk == 64 && d.bn == min(256, d.n_out);
         const CUtensorMap* tb = reinterpret_cast<const CUtensorMap*>(
             hdr + (wide ? kHdrWideOff : 0) + d.wlayer * kTmapBytes);
-        tmap_acquire(tb);
-        tmap_prefetch(ta);
-        tmap_prefetch(tb);
+        if (elect_one()) {
+          tmap_acquire(tb);
+          tmap_prefetch(ta);
+          tmap_prefetch(tb);
+        }
+        __syncwarp();
         const int ns = d.slots;
         const uint32_t sb = (uint32_t)d.slot_bytes;
         if (ns != cur_slots || d.slot_bytes != cur_bytes) {
@@ -486,7 +569,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           cur_bytes = d.slot_bytes;
         }
         const uint32_t a_bytes = a_rows(d) * (uint32_t)d.kblk * 2u;
-        const uint32_t tx = a_bytes + (uint32_t)d.bn * (uint32_t)d.kblk * 2u;
+        const bool no_a = args.flags & 2, no_b = args.flags & 4;
+        const uint32_t tx = (no_a ? 0u : a_bytes) + (no_b ? 0u : (uint32_t)d.bn * (uint32_t)d.kblk * 2u);
         const uint32_t b_box = 64u * (uint32_t)d.kblk * 2u;
         const int nbox = wide ? 1 : d.bn / 64;
         const int cin = d.cin_kb * 64;
@@ -513,23 +597,36 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           const int n = kb1 - kb0;
 #define CW_ACQUIRE(s_)                                                    \
   do {                                                                    \
-    mbar_wait_to(bar_empty + 8 * (s_), ((par >> (s_)) & 1) ^ 1, 3);      \
+    mbar_wait_to<256>(bar_empty + 8 * (s_), ((par >> (s_)) & 1) ^ 1, 3); \
     par ^= 1u << (s_);                                                    \
-    mbar_arrive_expect_tx(bar_full + 8 * (s_), tx);                       \
+    if (elect_one()) mbar_arrive_expect_tx(bar_full + 8 * (s_), tx);      \
+    __syncwarp();                                                         \
   } while (0)
 #define CW_LOAD_B(kb_, s_)                                                          \
   do {                                                                              \
     const uint32_t dst_ = sbase + (s_) * sb + b_off;                                \
-    for (int j = 0; j < nbox; ++j)                                                  \
-      tma_load_2d(dst_ + j * b_box, tb, bar_full + 8 * (s_), (kb_) * kblk, o.n0 + 64 * j); \
+    const int kx_ = (kb_) * kblk;                                                   \
+    if (elect_one())                                                                \
+      for (int j = 0; j < (no_b ? 0 : nbox); ++j)                                   \
+        tma_load_2d(dst_ + j * b_box, tb, bar_full + 8 * (s_), kx_, o.n0 + 64 * j);  \
+    __syncwarp();                                                                   \
   } while (0)
 #define CW_LOAD_A(s_)                                                                  \
   do {                                                                                 \
     const uint32_t dst_ = sbase + (s_) * sb;                                           \
-    if (mode == 0) {                                                                   \
-      tma_load_2d(dst_, ta, bar_full + 8 * (s_), a_kb * 64, o.m0);                     \
-    } else if (mode == 1) {                                                            \
-      tma_load_4d(dst_, ta, bar_full + 8 * (s_), a_c0, wb + a_q, hb + a_r, o.img0);    \
+    const uint32_t fb_ = bar_full + 8 * (s_);                                          \
+    if (elect_one()) {                                                                 \
+      if (no_a) {                                                                      \
+      } else if (mode == 0) {                                                          \
+        tma_load_2d(dst_, ta, fb_, a_kb * 64, o.m0);                                   \
+      } else if (mode == 1) {                                                          \
+        tma_load_4d(dst_, ta, fb_, a_c0, wb + a_q, hb + a_r, o.img0);                  \
+      } else {                                                                         \
+        tma_load_4d(dst_, ta, fb_, 0, o.ow0, hb + a_kb, o.img0);                       \
+      }                                                                                \
+    }                                                                                  \
+    __syncwarp();                                                                      \
+    if (mode == 1) {                                                                   \
       a_c0 += 64;                                                                      \
       if (a_c0 == cin) {                                                               \
         a_c0 = 0;                                                                      \
@@ -538,8 +635,6 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           ++a_r;                                                                       \
         }                                                                              \
       }                                                                                \
-    } else {                                                                           \
-      tma_load_4d(dst_, ta, bar_full + 8 * (s_), 0, o.ow0, hb + a_kb, o.img0);         \
     }                                                                                  \
     ++a_kb;                                                                            \
   } while (0)
@@ -556,7 +651,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
             wait_deps(sl, L, counters, gen1, 2);
             fence_proxy_async();
             waited = true;
-            if (args.trace) args.trace[((size_t)L * G + cta) * 4 + 1] = globaltimer();
+            if (args.trace && lane == 0) args.trace[((size_t)L * G + cta) * 4 + 1] = globaltimer();
             for (; i < pre; ++i) {
               CW_LOAD_A(slot);
               if (++slot == ns) slot = 0;
@@ -575,8 +670,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ======================= MMA issuer
+    {
+      // ======================= MMA issuer (whole warp converged; one elected lane issues)
       uint32_t par = 0;  // bit s: parity of the consumptions of slot s so far
       int acc = 0;
       uint32_t acc_phase = 0;
@@ -594,25 +689,38 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           const int z = t % d.splits;
           const int kb0 = z * d.kb_per_split;
           const int n = min(d.num_kb, kb0 + d.kb_per_split) - kb0;
-          mbar_wait_to(bar_tempty + 8 * acc, acc_phase ^ 1, 4);
+          mbar_wait_to<512>(bar_tempty + 8 * acc, acc_phase ^ 1, 4);
           tc_fence_after();
           const uint32_t dtm = tmem + acc * 256;
           for (int i = 0; i < n; ++i) {
-            mbar_wait_to(bar_full + 8 * slot, (par >> slot) & 1, 5);
+            mbar_wait_to<32>(bar_full + 8 * slot, (par >> slot) & 1, 5);
             par ^= 1u << slot;
-            if (first && args.trace) args.trace[((size_t)L * G + cta) * 4 + 3] = globaltimer();
+            if (first && lane == 0 && args.trace)
+              args.trace[((size_t)L * G + cta) * 4 + 3] = globaltimer();
             first = false;
             tc_fence_after();
             const uint32_t a_addr = sbase + slot * sb;
             const uint64_t adesc = sw64 ? sw64_kmajor_desc(a_addr) : sw128_kmajor_desc(a_addr);
             const uint64_t bdesc = sw64 ? sw64_kmajor_desc(a_addr + d.b_off)
                                         : sw128_kmajor_desc(a_addr + d.b_off);
-            for (int k = 0; k < ksteps; ++k)
-              mma_bf16(dtm, adesc + 2 * k, bdesc + 2 * k, idesc, (i | k) != 0);
-            mma_commit(bar_empty + 8 * slot);
+            if (elect_one()) {
+              if (!(args.flags & 1)) {
+                if (ksteps == 4) {
+                  mma_bf16(dtm, adesc, bdesc, idesc, i != 0);
+#pragma unroll
+                  for (int k = 1; k < 4; ++k) mma_bf16(dtm, adesc + 2 * k, bdesc + 2 * k, idesc, 1);
+                } else {
+                  mma_bf16(dtm, adesc, bdesc, idesc, i != 0);
+                  mma_bf16(dtm, adesc + 2, bdesc + 2, idesc, 1);
+                }
+              }
+              mma_commit(bar_empty + 8 * slot);
+            }
+            __syncwarp();
             if (++slot == ns) slot = 0;
           }
-          mma_commit(bar_tfull + 8 * acc);
+          if (elect_one()) mma_commit(bar_tfull + 8 * acc);
+          __syncwarp();
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
       }
@@ -654,7 +762,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           if (d.splits > 1) {
             // fp32 partial tile: 32-column chunks through the warp's staging buffer,
             // stored row-contiguous (8 lanes x 16 B = one 128-byte line per row).
-            mbar_wait_to<2000>(bar_tfull + 8 * acc, acc_phase, 7);
+            mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 7);
             tc_fence_after();
             float* part = d.partial + ((size_t)tile * d.splits + z) * 128 * d.bn;
             for (int c = 0; c < d.bn; c += 32) {
@@ -679,13 +787,18 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
             float* bias = sbias + acc * 256;
             if (done > 0)
               for (int i = et; i < d.bn; i += 128) bias[i] = __ldg(bias_all + o.n0 + i);
-            if (d.pool_out) {
+            if (d.pool_pw) {
+              mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 8);
+              tc_fence_after();
+              named_bar(1, 128);  // bias staged; the previous tile's pooling reads are done
+              epi_stem_pool(sl + L, o, taddr, bias, reinterpret_cast<uint8_t*>(sstage), row, et);
+            } else if (d.pool_out) {
               // Last conv: + bias (+ residual), ReLU, then a deterministic in-CTA
               // global average pool (the tile holds whole images).
               const __nv_bfloat16* res_row =
                   (d.res && valid) ? reinterpret_cast<const __nv_bfloat16*>(d.res) + m * d.n_out + o.n0
                                    : nullptr;
-              mbar_wait_to<2000>(bar_tfull + 8 * acc, acc_phase, 8);
+              mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 8);
               tc_fence_after();
               named_bar(1, 128);  // bias staged
               for (int c = 0; c < d.bn; c += 16) {
@@ -724,13 +837,13 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
               // 64-column chunks: accumulators (+ bias, + residual, ReLU) -> bf16 rows in the
               // warp's staging buffer -> coalesced row stores (8 lanes x 16 B per 128-byte
               // row segment). The residual chunk comes in the same coalesced way.
-              long long mr[8];
+              uint32_t mr[8];  // element offset of the row's first column in this tile (< 2^32)
               uint32_t vmask = 0;
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 long long mm;
                 if (row_pixel(d, o, q * 32 + i * 4 + (lane >> 3), &mm)) vmask |= 1u << i;
-                mr[i] = mm;
+                mr[i] = (uint32_t)(mm * d.n_out + o.n0);
               }
               const int ch = lane & 7;
               const __nv_bfloat16* res = reinterpret_cast<const __nv_bfloat16*>(d.res);
@@ -740,20 +853,15 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
                   if (vmask >> i & 1)
-                    rr[i] = __ldcg(reinterpret_cast<const uint4*>(res + mr[i] * d.n_out + o.n0) + ch);
+                    rr[i] = __ldcg(reinterpret_cast<const uint4*>(res + mr[i]) + ch);
               }
-              mbar_wait_to<2000>(bar_tfull + 8 * acc, acc_phase, 8);
+              mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 8);
               tc_fence_after();
               if (first && et == 0 && args.trace)
                 args.trace[((size_t)L * G + cta) * 4 + 2] = globaltimer();
               first = false;
               named_bar(1, 128);  // bias staged
               for (int c = 0; c < d.bn; c += 64) {
-                uint32_t v[64];
-                tmem_ld16(taddr + c, *reinterpret_cast<uint32_t(*)[16]>(v));
-                tmem_ld16(taddr + c + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
-                tmem_ld16(taddr + c + 32, *reinterpret_cast<uint32_t(*)[16]>(v + 32));
-                tmem_ld16(taddr + c + 48, *reinterpret_cast<uint32_t(*)[16]>(v + 48));
                 if (res) {
 #pragma unroll
                   for (int i = 0; i < 8; ++i) *stg_chunk(i * 4 + (lane >> 3), ch) = rr[i];
@@ -761,38 +869,47 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
 #pragma unroll
                     for (int i = 0; i < 8; ++i)
                       if (vmask >> i & 1)
-                        rr[i] = __ldcg(reinterpret_cast<const uint4*>(res + mr[i] * d.n_out + o.n0 + c + 64) + ch);
+                        rr[i] = __ldcg(reinterpret_cast<const uint4*>(res + mr[i] + c + 64) + ch);
                   }
                 }
-                tmem_ld_wait();
                 __syncwarp();
+                // two 32-column halves keep the accumulator registers at 32
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                  float f[8];
+                for (int h = 0; h < 2; ++h) {
+                  uint32_t v[32];
+                  tmem_ld16(taddr + c + 32 * h, *reinterpret_cast<uint32_t(*)[16]>(v));
+                  tmem_ld16(taddr + c + 32 * h + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+                  tmem_ld_wait();
 #pragma unroll
-                  for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[8 * k + e]) + bias[c + 8 * k + e];
-                  if (res) {
-                    float rf[8];
-                    bf16x8_to_f32(*stg_chunk(lane, k), rf);
+                  for (int kk = 0; kk < 4; ++kk) {
+                    const int k = 4 * h + kk;
+                    float f[8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) f[e] += rf[e];
+                    for (int e = 0; e < 8; ++e)
+                      f[e] = __uint_as_float(v[8 * kk + e]) + bias[c + 8 * k + e];
+                    if (res) {
+                      float rf[8];
+                      bf16x8_to_f32(*stg_chunk(lane, k), rf);
+#pragma unroll
+                      for (int e = 0; e < 8; ++e) f[e] += rf[e];
+                    }
+                    if (d.relu) {
+#pragma unroll
+                      for (int e = 0; e < 8; ++e) f[e] = fmaxf(f[e], 0.0f);
+                    }
+                    uint4 w;
+                    w.x = pack_bf16x2(f[0], f[1]);
+                    w.y = pack_bf16x2(f[2], f[3]);
+                    w.z = pack_bf16x2(f[4], f[5]);
+                    w.w = pack_bf16x2(f[6], f[7]);
+                    *stg_chunk(lane, k) = w;
                   }
-                  if (d.relu) {
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) f[e] = fmaxf(f[e], 0.0f);
-                  }
-                  uint4 w;
-                  w.x = pack_bf16x2(f[0], f[1]);
-                  w.y = pack_bf16x2(f[2], f[3]);
-                  w.z = pack_bf16x2(f[4], f[5]);
-                  w.w = pack_bf16x2(f[6], f[7]);
-                  *stg_chunk(lane, k) = w;
                 }
                 __syncwarp();
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
                   if (vmask >> i & 1)
-                    reinterpret_cast<uint4*>(out + mr[i] * d.n_out + o.n0 + c)[ch] =
+                    reinterpret_cast<uint4*>(out + mr[i] + c)[ch] =
                         *stg_chunk(i * 4 + (lane >> 3), ch);
                 __syncwarp();
               }
@@ -813,6 +930,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         if (d.kind == MK_REDUCE && first_task(d, cta, G) >= d.tasks) continue;
         if (et == 0) wait_deps(sl, L, counters, gen1, 9);
         named_bar(1, 128);
+        if (args.trace && et == 0) args.trace[((size_t)L * G + cta) * 4 + 1] = globaltimer();
         int done = 1;
         switch (d.kind) {
           case MK_INPUT: simt_input(d, ab, cta, G, et); break;
@@ -828,6 +946,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           }
           default: break;
         }
+        if (args.trace && et == 0) args.trace[((size_t)L * G + cta) * 4 + 2] = globaltimer();
         named_bar(1, 128);
         if (et == 0) red_release_add(counters + L, (uint32_t)done);
       }

@@ -418,10 +418,26 @@ std::string Runtime::build_plan(Arch& a, int batch) {
           d.mode = 2;
           d.kblk = 32;
           d.num_kb = 7;
-          box_dims(batch, op.out_h, op.out_w, &d.box_w, &d.box_h, &d.box_n);
-          d.tiles_w = (op.out_w + d.box_w - 1) / d.box_w;
-          d.tiles_h = (op.out_h + d.box_h - 1) / d.box_h;
-          d.m_tiles = d.tiles_w * d.tiles_h * ((batch + d.box_n - 1) / d.box_n);
+          const bool fuse_max = nxt && nxt->kind == OP_MAXPOOL && nxt->in_buf == op.out_buf &&
+                                getenv("CW_NO_STEM_POOL") == nullptr;
+          if (fuse_max) {
+            // tiles of 20 pooled columns of one pooled row: 3 x 41 conv pixels (123 <= 128 rows)
+            d.pool_pw = 20;
+            d.OH = nxt->out_h;
+            d.OW = nxt->out_w;
+            d.box_w = 2 * d.pool_pw + 1;
+            d.box_h = 3;
+            d.box_n = 1;
+            d.tiles_w = (d.OW + d.pool_pw - 1) / d.pool_pw;
+            d.tiles_h = d.OH;
+            d.m_tiles = d.tiles_w * d.tiles_h * batch;
+            d.out = a.bufs[nxt->out_buf];
+          } else {
+            box_dims(batch, op.out_h, op.out_w, &d.box_w, &d.box_h, &d.box_n);
+            d.tiles_w = (op.out_w + d.box_w - 1) / d.box_w;
+            d.tiles_h = (op.out_h + d.box_h - 1) / d.box_h;
+            d.m_tiles = d.tiles_w * d.tiles_h * ((batch + d.box_n - 1) / d.box_n);
+          }
           if (!make_tmap_stem(&tm, in, batch, op.in_h, op.in_w + 2 * kMkPadW, op.out_w, d.box_w,
                               d.box_h, d.box_n))
             return "tensor map (stem) failed";
@@ -454,11 +470,14 @@ std::string Runtime::build_plan(Arch& a, int batch) {
             return "tensor map (nhwc) failed";
         }
         // (the fused pool runs in the epilogue of whole-image tiles: no split-K there)
-        plan_conv(d, op.cout, G, !fuse_pool);
+        plan_conv(d, op.cout, G, !fuse_pool && !d.pool_pw);
         d.tmap = (int)p.tmaps.size();
         p.tmaps.push_back(tm);
         std::vector<int> rd = {op.in_buf}, wr;
-        if (fuse_pool) {
+        if (d.pool_pw) {
+          wr.push_back(nxt->out_buf);
+          ++oi;  // the max pool op is done in this layer's epilogue
+        } else if (fuse_pool) {
           d.pool_out = reinterpret_cast<float*>(a.bufs[nxt->out_buf]);
           d.pool_scale = 1.0f / (float)(op.out_h * op.out_w);
           d.out = nullptr;
@@ -592,6 +611,7 @@ std::string Runtime::capture(Arch& a, Plan& p) {
   args.counters = p.d_counters;
   args.gen = p.d_gen;
   args.trace = p.d_trace;
+  if (const char* e = getenv("CW_MK_FLAGS")) args.flags = (uint32_t)atoi(e);  // experiments only
   CW_TRY(cudaStreamBeginCapture(s_cap_, cudaStreamCaptureModeThreadLocal));
   launch_gate(ab_, ring_, kRing - 1, ctr_, exec_recs_, s_cap_);
   cudaError_t le = launch_mk(args, p.grid, p.smem, s_cap_);

@@ -34,19 +34,27 @@ def run(b, h, cin, cout, k, stride):
         for _ in range(5):
             ends, _ = rt.profile_layers(0, b, 0)
             plan = rt.plan_layers(0, b)
-            tr, _, _ = rt.last_trace(len(plan))
+            tr, _, clk = rt.last_trace(len(plan))
+            ok = clk[:, 2] > clk[:, 0]
+            mhz = float(np.median((clk[ok, 3] - clk[ok, 1]) / ((clk[ok, 2] - clk[ok, 0]) / 1e3)))
             row = tr[0]
             act = row[:, 0] >= 0
             land = np.median(row[act, 3])
             acc = np.median(row[act, 2][row[act, 2] >= 0]) if (row[act, 2] >= 0).any() else np.nan
-            res.append((ends[-1] * 1e3, (acc - land) / 1e3))
+            inp = np.median(row[act, 1])
+            done = np.median(row[act, 0])
+            res.append((ends[-1] * 1e3, (acc - land) / 1e3, mhz, inp / 1e3, land / 1e3, acc / 1e3,
+                        done / 1e3, row[act, 0].max() / 1e3))
         kind, mode, bn, tasks, sp, kb, _, _ = (int(x) for x in plan[0])
-        t, span = np.median(np.array(res), axis=0)
+        t, span, mhz, inp, land, acc, done, dmax = np.median(np.array(res), axis=0)
         kb_task = -(-kb // sp)
         flops = 2.0 * b * oh * oh * cout * k * k * cin
         print(f"b{b} {h}x{h} {cin}->{cout} k{k}s{stride}: bn {bn} split {sp} tasks {tasks} "
               f"kb/task {kb_task}: layer {t:6.1f} us ({flops / t / 1e6:6.1f} TF/s), "
-              f"first task MMA pipe {span:5.2f} us = {span / kb_task:5.3f} us/kb", flush=True)
+              f"first task MMA pipe {span:5.2f} us = {span / kb_task:5.3f} us/kb "
+              f"= {span / kb_task * mhz:5.0f} cycles/kb at {mhz:.0f} MHz\n"
+              f"    since kernel start: inputs ready {inp:.1f}, first tile {land:.1f}, first acc "
+              f"{acc:.1f}, done median {done:.1f} / max {dmax:.1f} us", flush=True)
 
 
 for case in sys.argv[1:]:
