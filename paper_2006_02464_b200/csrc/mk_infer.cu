@@ -744,9 +744,14 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         if (t >= d.tasks) continue;
         const float* bias_all = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[d.wlayer];
         if (d.splits == 1) {
-          // folded-BN bias of the first task's columns (weights: no dependency)
+          // folded-BN bias of the first task's columns (weights: no dependency); a
+          // layer with one N tile uses the same columns for every task: both buffers
           const int n0 = (t / d.splits % d.n_tiles) * d.bn;
-          for (int i = et; i < d.bn; i += 128) sbias[acc * 256 + i] = __ldg(bias_all + n0 + i);
+          for (int i = et; i < d.bn; i += 128) {
+            const float bv = __ldg(bias_all + n0 + i);
+            sbias[acc * 256 + i] = bv;
+            if (d.n_tiles == 1) sbias[(acc ^ 1) * 256 + i] = bv;
+          }
         }
         if (et == 0) wait_deps(sl, L, counters, gen1, 6);
         named_bar(1, 128);
@@ -785,7 +790,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           } else {
             // folded-BN bias of this tile's columns, staged while the MMAs run
             float* bias = sbias + acc * 256;
-            if (done > 0)
+            const bool bias_fixed = d.n_tiles == 1;  // staged once for the layer
+            if (done > 0 && !bias_fixed)
               for (int i = et; i < d.bn; i += 128) bias[i] = __ldg(bias_all + o.n0 + i);
             if (d.pool_pw) {
               mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 8);
@@ -800,7 +806,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                                    : nullptr;
               mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 8);
               tc_fence_after();
-              named_bar(1, 128);  // bias staged
+              if (!bias_fixed) named_bar(1, 128);  // bias staged
               for (int c = 0; c < d.bn; c += 16) {
                 uint32_t v[16];
                 tmem_ld16(taddr + c, v);
@@ -860,7 +866,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
               if (first && et == 0 && args.trace)
                 args.trace[((size_t)L * G + cta) * 4 + 2] = globaltimer();
               first = false;
-              named_bar(1, 128);  // bias staged
+              if (!bias_fixed) named_bar(1, 128);  // bias staged
               for (int c = 0; c < d.bn; c += 64) {
                 if (res) {
 #pragma unroll

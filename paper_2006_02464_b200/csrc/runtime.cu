@@ -253,7 +253,8 @@ static void box_dims(int nimg, int oh, int ow, int* bw, int* bh, int* bn) {
 //     (per-instruction cost), so FLOP efficiency grows with the N tile;
 //   * the single producer thread spends ~0.08 us per TMA it issues;
 //   * TMA feeds one SM at ~140 GB/s;
-//   * the 4-warp epilogue drains ~20 GB/s per SM (bf16 tile rows, ~3 TB/s chip);
+//   * the 4-warp epilogue drains ~20 GB/s per SM (bf16 tile rows, ~3 TB/s chip)
+//     plus ~0.8 us of fixed latency per tile (bias / residual loads, barriers);
 //   * a split-K reduce layer costs ~3 us plus its partial-tile traffic.
 // Epilogue of task i overlaps the MMAs of task i+1 (two TMEM accumulators).
 static void plan_conv(MkLayer& d, int cout, int G, bool allow_split) {
@@ -277,7 +278,7 @@ static void plan_conv(MkLayer& d, int cout, int G, bool allow_split) {
       const int tasks = tiles * s;
       const int waves = (tasks + G - 1) / G;
       const double t_main = per * t_kb;
-      const double t_epi = rows * bn * (s > 1 ? 4.0 : 2.0) / 20e3;
+      const double t_epi = rows * bn * (s > 1 ? 4.0 : 2.0) / 20e3 + 0.8;  // + per-task fixed cost
       double t = waves * std::max(t_main, t_epi) + std::min(t_main, t_epi) + 1.5;
       if (s > 1) t += 3.0 + (double)tiles * 128 * bn * (4.0 * s + 2.0) / (G * 40e3);
       if (t < best - 1e-9) {
