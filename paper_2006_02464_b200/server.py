@@ -83,7 +83,7 @@ def serve(listen: str, catalog, gpu_count: int = 1, pages_per_gpu: int = 500, ji
         while True:
             try:
                 msg = wire.recv(conn)
-            except OSError:
+            except (OSError, wire.WireError):
                 break
             if msg is None:
                 break
@@ -104,11 +104,17 @@ def serve(listen: str, catalog, gpu_count: int = 1, pages_per_gpu: int = 500, ji
         lsock.close()
         if mode != "cuda":
             loop.stop(join=False)
-        worker.close()
-    if telemetry_path:
-        with open(telemetry_path, "w", newline="") as f:
-            w = csv.writer(f)
-            w.writerow(TELEMETRY_HEADER)
-            for r in worker.records:
-                w.writerow([r.action_id, r.kind, r.model_id, r.gpu_index, r.batch_size, r.status,
-                            r.start, r.end, r.device_duration])
+        try:
+            worker.close()
+        finally:
+            if telemetry_path:
+                _write_telemetry(telemetry_path, worker.records)
+
+
+def _write_telemetry(path: str, records) -> None:
+    with open(path, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(TELEMETRY_HEADER)
+        for r in list(records):
+            w.writerow([r.action_id, r.kind, r.model_id, r.gpu_index, r.batch_size, r.status,
+                        r.start, r.end, r.device_duration])
