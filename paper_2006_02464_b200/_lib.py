@@ -12,6 +12,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcw.so")
+if os.environ.get("CW_LIB"):  # experiments only: a variant built with CW_BUILD_TAG
+    LIB_PATH = os.path.join(_HERE, os.environ["CW_LIB"])
 
 MAX_BATCH = 16
 

@@ -19,8 +19,11 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 REPO = os.path.dirname(PKG)
-LIB = os.path.join(PKG, "libcw.so")
-OBJ = os.path.join(REPO, "build", "obj")
+# experiments only: CW_BUILD_TAG=x CW_NVCC_DEFS="-DFOO=1" builds libcw_x.so from build/obj_x
+_TAG = os.environ.get("CW_BUILD_TAG", "")
+LIB = os.path.join(PKG, f"libcw_{_TAG}.so" if _TAG else "libcw.so")
+OBJ = os.path.join(REPO, "build", f"obj_{_TAG}" if _TAG else "obj")
+DEFS = os.environ.get("CW_NVCC_DEFS", "").split() if _TAG else []
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -47,7 +50,7 @@ def _compile(src: str, force: bool) -> str:
     obj = os.path.join(OBJ, src + ".o")
     if force or _stale(obj, [path] + _headers()):
         lang = [] if src.endswith(".cu") else ["-x", "cu"]
-        cmd = [NVCC, *ARCH, *COMMON, *lang, "-c", path, "-o", obj]
+        cmd = [NVCC, *ARCH, *COMMON, *DEFS, *lang, "-c", path, "-o", obj]
         if src == "mk_infer.cu":
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -30,12 +30,24 @@ enum MkKind : int32_t {
 };
 
 constexpr int kMkMaxDeps = 6;
-constexpr int kMkThreads = 192;            // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue / SIMT
+#ifndef CW_PRODUCERS
+#define CW_PRODUCERS 1
+#endif
+// TMA producer warps: warp 0 (and warp 6): producer p fills the ring slots s with s % P == p, so
+// the issue path of P k-blocks runs in parallel (one warp's path is ~570 cycles per k-block).
+constexpr int kMkProducers = CW_PRODUCERS;
+// warp 0 (+6) TMA, warp 1 MMA, warps 2-5 epilogue / SIMT
+constexpr int kMkThreads = 192 + 32 * (kMkProducers - 1);
 constexpr uint32_t kMkATile = 128 * 128;   // A tile: 128 rows x 128 B
 constexpr int kMkPadW = 4;                 // MK_INPUT: zero pixels left of every row
 constexpr uint32_t kMkTmemCols = 512;      // two accumulators of up to 256 columns
 constexpr int kMkMaxSlots = 16;            // smem ring slots (per-layer slot size)
-constexpr uint32_t kMkBarBytes = 512;      // full/empty[16], tfull/tempty[2], tmem + gen slots
+constexpr uint32_t kMkBarBytes = 512;
+#ifdef CW_KB_TRACE
+constexpr uint32_t kMkSmemCap = 224 * 1024;  // debug builds keep a static trace array
+#else
+constexpr uint32_t kMkSmemCap = 227 * 1024;  // dynamic shared memory per CTA
+#endif      // full/empty[16], tfull/tempty[2], tmem + gen slots
 
 struct MkLayer {
   int32_t kind, tasks, rot, ndeps;
@@ -45,7 +57,9 @@ struct MkLayer {
   int32_t bn, m_tiles, n_tiles, splits, kb_per_split, num_kb, cin_kb, kw, stride, pad;
   int32_t box_w, box_h, box_n, tiles_w, tiles_h, m_total, nimg, oh, ow;
   int32_t relu, wlayer, n_out, tmap, red_rows, kblk;  // kblk: K elements per k-block (64 or 32)
-  int32_t slots, slot_bytes, b_off;  // smem ring geometry of this layer (B tile at b_off in a slot)
+  int32_t slots, slot_bytes, b_off;  // smem ring geometry of this layer (B tile at b_off in a sub-slot)
+  int32_t kpack, sub_bytes;  // k-blocks per ring slot (sub-slots of sub_bytes) behind one barrier
+  int32_t pad_[2];
   // stem with fused 3x3/s2/p1 max pool: pooled columns per tile (0 = no fusion);
   // a tile covers conv rows 2ph-1..2ph+1 and conv columns 2pw0-1..2pw0+2*pool_pw-1
   int32_t pool_pw, pool_oh;

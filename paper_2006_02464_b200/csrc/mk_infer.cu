@@ -77,13 +77,44 @@ __device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar, uint32_t parity
 
 // ptxas turns the hint into a NANOSLEEP between checks, i.e. the wake-up
 // granularity of a waiting warp.
-constexpr uint32_t kEpiWaitNs = 512;
+#ifndef CW_HINT_EPI
+#define CW_HINT_EPI 512
+#endif
+constexpr uint32_t kEpiWaitNs = CW_HINT_EPI;
+
+__device__ __forceinline__ bool mbar_try_wait_nohint(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+template <uint32_t kHintNs>
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  if constexpr (kHintNs == 0) return mbar_try_wait_nohint(bar, parity);
+  else return mbar_try_wait_hint<kHintNs>(bar, parity);
+}
+
+#ifndef CW_HINT_EMPTY
+#define CW_HINT_EMPTY 256
+#endif
+#ifndef CW_HINT_FULL
+#define CW_HINT_FULL 32
+#endif
+#ifndef CW_HINT_TEMPTY
+#define CW_HINT_TEMPTY 512
+#endif
 
 template <uint32_t kHintNs = 64>
 __device__ __forceinline__ void mbar_wait_to(uint32_t bar, uint32_t parity, int site) {
-  if (mbar_try_wait_hint<kHintNs>(bar, parity)) return;
+  if (mbar_try<kHintNs>(bar, parity)) return;
   const uint64_t t0 = globaltimer();
-  while (!mbar_try_wait_hint<kHintNs>(bar, parity)) {
+  while (!mbar_try<kHintNs>(bar, parity)) {
     if (globaltimer() - t0 > kMkTimeoutNs) mk_timeout(site);
   }
 }
@@ -505,6 +536,10 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int cta = blockIdx.x;
+#ifdef CW_KB_TRACE
+  __shared__ uint64_t kbt[4][64];  // debug: producer acquire / A issued, MMA full / committed
+  int kbp = 0, kbm = 0;
+#endif
   const int G = gridDim.x;
   const int nl = args.n_layers;
 
@@ -537,12 +572,14 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   const uint8_t* hdr = ab->hdr;
   uint32_t* counters = args.counters;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 6) {
+    const int pw = warp == 0 ? 0 : 1;  // producer index
     {
       // ======================= TMA producer (whole warp converged; one elected lane issues)
-      // Slots restart at 0 every layer; bit s of `par` = parity of the fills of
-      // slot s so far (fill n waits for consumption n-1). A layer whose slot
-      // geometry differs from the previous one first drains the ring.
+      // A ring slot holds `kpack` consecutive k-blocks (sub-slots of sub_bytes: A tile, then
+      // B tile at b_off) behind one full/empty barrier pair. Slots restart at 0 every layer;
+      // bit s of `par` = parity of the fills of slot s so far (fill n waits for consumption
+      // n-1). A layer whose slot geometry differs from the previous one first drains the ring.
       uint32_t par = 0;
       int cur_slots = 0, cur_bytes = 0;
       for (int L = 0; L < nl; ++L) {
@@ -564,18 +601,25 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         const int ns = d.slots;
         const uint32_t sb = (uint32_t)d.slot_bytes;
         if (ns != cur_slots || d.slot_bytes != cur_bytes) {
-          for (int s = 0; s < cur_slots; ++s) mbar_wait_to(bar_empty + 8 * s, ((par >> s) & 1) ^ 1, 1);
+          for (int s = 0; s < cur_slots; ++s)
+            if (s % kMkProducers == pw) mbar_wait_to(bar_empty + 8 * s, ((par >> s) & 1) ^ 1, 1);
+          // a new slot may overlap an old slot of the other producer: both drain first
+          if (kMkProducers > 1) named_bar(2, 32 * kMkProducers);
           cur_slots = ns;
           cur_bytes = d.slot_bytes;
         }
         const uint32_t a_bytes = a_rows(d) * (uint32_t)d.kblk * 2u;
+#ifdef CW_MK_EXPERIMENTS
         const bool no_a = args.flags & 2, no_b = args.flags & 4;
-        const uint32_t tx = (no_a ? 0u : a_bytes) + (no_b ? 0u : (uint32_t)d.bn * (uint32_t)d.kblk * 2u);
+#else
+        constexpr bool no_a = false, no_b = false;
+#endif
+        const uint32_t tx1 = (no_a ? 0u : a_bytes) + (no_b ? 0u : (uint32_t)d.bn * (uint32_t)d.kblk * 2u);
         const uint32_t b_box = 64u * (uint32_t)d.kblk * 2u;
         const int nbox = wide ? 1 : d.bn / 64;
         const int cin = d.cin_kb * 64;
-        const int mode = d.mode, kw = d.kw, kblk = d.kblk;
-        const uint32_t b_off = (uint32_t)d.b_off;
+        const int mode = d.mode, kw = d.kw, kblk = d.kblk, kpack = d.kpack;
+        const uint32_t b_off = (uint32_t)d.b_off, sub = (uint32_t)d.sub_bytes;
         int slot = 0;
         bool waited = false;
         for (; t < d.tasks; t += G) {
@@ -595,37 +639,25 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
             a_q = tap - a_r * d.kw;
           }
           const int n = kb1 - kb0;
-#define CW_ACQUIRE(s_)                                                    \
-  do {                                                                    \
-    mbar_wait_to<256>(bar_empty + 8 * (s_), ((par >> (s_)) & 1) ^ 1, 3); \
-    par ^= 1u << (s_);                                                    \
-    if (elect_one()) mbar_arrive_expect_tx(bar_full + 8 * (s_), tx);      \
-    __syncwarp();                                                         \
-  } while (0)
-#define CW_LOAD_B(kb_, s_)                                                          \
+          const int nslots = (n + kpack - 1) / kpack;
+#define CW_ACQUIRE(s_, m_)                                                          \
   do {                                                                              \
-    const uint32_t dst_ = sbase + (s_) * sb + b_off;                                \
+    mbar_wait_to<CW_HINT_EMPTY>(bar_empty + 8 * (s_), ((par >> (s_)) & 1) ^ 1, 3);  \
+    par ^= 1u << (s_);                                                              \
+    if (elect_one()) mbar_arrive_expect_tx(bar_full + 8 * (s_), tx1 * (uint32_t)(m_)); \
+    __syncwarp();                                                                   \
+  } while (0)
+#define CW_LOAD_B(kb_, dst0_, s_)                                                   \
+  do {                                                                              \
+    const uint32_t dst_ = (dst0_) + b_off;                                          \
     const int kx_ = (kb_) * kblk;                                                   \
     if (elect_one())                                                                \
       for (int j = 0; j < (no_b ? 0 : nbox); ++j)                                   \
         tma_load_2d(dst_ + j * b_box, tb, bar_full + 8 * (s_), kx_, o.n0 + 64 * j);  \
     __syncwarp();                                                                   \
   } while (0)
-#define CW_LOAD_A(s_)                                                                  \
+#define CW_ADV_A()                                                                      \
   do {                                                                                 \
-    const uint32_t dst_ = sbase + (s_) * sb;                                           \
-    const uint32_t fb_ = bar_full + 8 * (s_);                                          \
-    if (elect_one()) {                                                                 \
-      if (no_a) {                                                                      \
-      } else if (mode == 0) {                                                          \
-        tma_load_2d(dst_, ta, fb_, a_kb * 64, o.m0);                                   \
-      } else if (mode == 1) {                                                          \
-        tma_load_4d(dst_, ta, fb_, a_c0, wb + a_q, hb + a_r, o.img0);                  \
-      } else {                                                                         \
-        tma_load_4d(dst_, ta, fb_, 0, o.ow0, hb + a_kb, o.img0);                       \
-      }                                                                                \
-    }                                                                                  \
-    __syncwarp();                                                                      \
     if (mode == 1) {                                                                   \
       a_c0 += 64;                                                                      \
       if (a_c0 == cin) {                                                               \
@@ -638,34 +670,77 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     }                                                                                  \
     ++a_kb;                                                                            \
   } while (0)
-          int i = 0;
+#define CW_LOAD_A(dst_, s_)                                                            \
+  do {                                                                                 \
+    const uint32_t fb_ = bar_full + 8 * (s_);                                          \
+    if (elect_one()) {                                                                 \
+      if (no_a) {                                                                      \
+      } else if (mode == 0) {                                                          \
+        tma_load_2d(dst_, ta, fb_, a_kb * 64, o.m0);                                   \
+      } else if (mode == 1) {                                                          \
+        tma_load_4d(dst_, ta, fb_, a_c0, wb + a_q, hb + a_r, o.img0);                  \
+      } else {                                                                         \
+        tma_load_4d(dst_, ta, fb_, 0, o.ow0, hb + a_kb, o.img0);                       \
+      }                                                                                \
+    }                                                                                  \
+    __syncwarp();                                                                      \
+    CW_ADV_A();                                                                        \
+  } while (0)
+#define CW_MINE(s_) ((s_) % kMkProducers == pw)
+          int c = 0;  // slots of this task done
           if (!waited) {
             // weights first (independent of the previous layers), then the inputs
-            const int pre = n < ns ? n : ns;
+            const int pre = nslots < ns ? nslots : ns;
             int s = slot;
             for (int k = 0; k < pre; ++k) {
-              CW_ACQUIRE(s);
-              CW_LOAD_B(kb0 + k, s);
+              if (CW_MINE(s)) {
+                const int m = min(kpack, n - k * kpack);
+                CW_ACQUIRE(s, m);
+                for (int j = 0; j < m; ++j) CW_LOAD_B(kb0 + k * kpack + j, sbase + s * sb + j * sub, s);
+              }
               if (++s == ns) s = 0;
             }
             wait_deps(sl, L, counters, gen1, 2);
             fence_proxy_async();
             waited = true;
-            if (args.trace && lane == 0) args.trace[((size_t)L * G + cta) * 4 + 1] = globaltimer();
-            for (; i < pre; ++i) {
-              CW_LOAD_A(slot);
+            if (args.trace && lane == 0 && pw == 0)
+              args.trace[((size_t)L * G + cta) * 4 + 1] = globaltimer();
+            for (; c < pre; ++c) {
+              const int m = min(kpack, n - c * kpack);
+              if (CW_MINE(slot)) {
+                for (int j = 0; j < m; ++j) CW_LOAD_A(sbase + slot * sb + j * sub, slot);
+              } else {
+                for (int j = 0; j < m; ++j) CW_ADV_A();
+              }
               if (++slot == ns) slot = 0;
             }
           }
-          for (; i < n; ++i) {
-            CW_ACQUIRE(slot);
-            CW_LOAD_B(kb0 + i, slot);
-            CW_LOAD_A(slot);
+          for (; c < nslots; ++c) {
+            const int m = min(kpack, n - c * kpack);
+            if (CW_MINE(slot)) {
+              CW_ACQUIRE(slot, m);
+#ifdef CW_KB_TRACE
+              if (cta == 0 && kbp < 64 && lane == 0 && pw == 0) kbt[0][kbp] = clock64();
+#endif
+              for (int j = 0; j < m; ++j) {
+                const uint32_t dst = sbase + slot * sb + j * sub;
+                CW_LOAD_B(kb0 + c * kpack + j, dst, slot);
+                CW_LOAD_A(dst, slot);
+              }
+#ifdef CW_KB_TRACE
+              if (cta == 0 && kbp < 64 && lane == 0 && pw == 0) kbt[1][kbp] = clock64();
+              if (pw == 0) ++kbp;
+#endif
+            } else {
+              for (int j = 0; j < m; ++j) CW_ADV_A();
+            }
             if (++slot == ns) slot = 0;
           }
 #undef CW_ACQUIRE
 #undef CW_LOAD_B
 #undef CW_LOAD_A
+#undef CW_ADV_A
+#undef CW_MINE
         }
       }
     }
@@ -680,43 +755,64 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         const MkLayer d = sl[L];
         const uint32_t idesc = idesc_bf16_f32(128, d.bn);
         const bool sw64 = d.kblk == 32;
-        const int ksteps = d.kblk / 16;
-        const int ns = d.slots;
+        const int ns = d.slots, kpack = d.kpack;
         const uint32_t sb = (uint32_t)d.slot_bytes;
+        // descriptor of slot 0 / sub-slot 0, and the 16-byte-unit strides of slots / sub-slots
+        const uint64_t adesc0 = sw64 ? sw64_kmajor_desc(sbase) : sw128_kmajor_desc(sbase);
+        const uint64_t bdesc0 = adesc0 + ((uint32_t)d.b_off >> 4);
+        const uint32_t sdesc = sb >> 4, subdesc = (uint32_t)d.sub_bytes >> 4;
         int slot = 0;
         bool first = true;
         for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
           const int z = t % d.splits;
           const int kb0 = z * d.kb_per_split;
           const int n = min(d.num_kb, kb0 + d.kb_per_split) - kb0;
-          mbar_wait_to<512>(bar_tempty + 8 * acc, acc_phase ^ 1, 4);
+          mbar_wait_to<CW_HINT_TEMPTY>(bar_tempty + 8 * acc, acc_phase ^ 1, 4);
           tc_fence_after();
           const uint32_t dtm = tmem + acc * 256;
-          for (int i = 0; i < n; ++i) {
-            mbar_wait_to<32>(bar_full + 8 * slot, (par >> slot) & 1, 5);
+          for (int i = 0; i < n; i += kpack) {
+            mbar_wait_to<CW_HINT_FULL>(bar_full + 8 * slot, (par >> slot) & 1, 5);
+#ifdef CW_KB_TRACE
+            if (cta == 0 && kbm < 64 && lane == 0) kbt[2][kbm] = clock64();
+#endif
             par ^= 1u << slot;
-            if (first && lane == 0 && args.trace)
-              args.trace[((size_t)L * G + cta) * 4 + 3] = globaltimer();
-            first = false;
+            if (first) {
+              if (lane == 0 && args.trace) args.trace[((size_t)L * G + cta) * 4 + 3] = globaltimer();
+              first = false;
+            }
             tc_fence_after();
-            const uint32_t a_addr = sbase + slot * sb;
-            const uint64_t adesc = sw64 ? sw64_kmajor_desc(a_addr) : sw128_kmajor_desc(a_addr);
-            const uint64_t bdesc = sw64 ? sw64_kmajor_desc(a_addr + d.b_off)
-                                        : sw128_kmajor_desc(a_addr + d.b_off);
+            const uint64_t ad = adesc0 + slot * sdesc, bd = bdesc0 + slot * sdesc;
+            const int m = min(kpack, n - i);
             if (elect_one()) {
-              if (!(args.flags & 1)) {
-                if (ksteps == 4) {
-                  mma_bf16(dtm, adesc, bdesc, idesc, i != 0);
+#ifdef CW_MK_EXPERIMENTS
+              if (!(args.flags & 1))
+#endif
+              {
+                if (!sw64) {
+                  mma_bf16(dtm, ad, bd, idesc, i != 0);
 #pragma unroll
-                  for (int k = 1; k < 4; ++k) mma_bf16(dtm, adesc + 2 * k, bdesc + 2 * k, idesc, 1);
+                  for (int k = 1; k < 4; ++k) mma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, 1);
+                  if (m > 1) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                      mma_bf16(dtm, ad + subdesc + 2 * k, bd + subdesc + 2 * k, idesc, 1);
+                  }
                 } else {
-                  mma_bf16(dtm, adesc, bdesc, idesc, i != 0);
-                  mma_bf16(dtm, adesc + 2, bdesc + 2, idesc, 1);
+                  mma_bf16(dtm, ad, bd, idesc, i != 0);
+                  mma_bf16(dtm, ad + 2, bd + 2, idesc, 1);
+                  if (m > 1) {
+                    mma_bf16(dtm, ad + subdesc, bd + subdesc, idesc, 1);
+                    mma_bf16(dtm, ad + subdesc + 2, bd + subdesc + 2, idesc, 1);
+                  }
                 }
               }
               mma_commit(bar_empty + 8 * slot);
             }
             __syncwarp();
+#ifdef CW_KB_TRACE
+            if (cta == 0 && kbm < 64 && lane == 0) kbt[3][kbm] = clock64();
+            ++kbm;
+#endif
             if (++slot == ns) slot = 0;
           }
           if (elect_one()) mma_commit(bar_tfull + 8 * acc);
@@ -725,7 +821,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         }
       }
     }
-  } else {
+  } else if (warp >= 2 && warp <= 5) {
     // ======================= epilogue + SIMT layers (warps 2..5)
     const int q = warp & 3;  // TMEM lane quarter
     const int row = q * 32 + lane;
@@ -961,6 +1057,14 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   }
   tc_fence_before();
   __syncthreads();
+#ifdef CW_KB_TRACE
+  if (cta == 0 && threadIdx.x == 0) {
+    for (int i = 0; i < 40; ++i)
+      printf("kb %2d acq %6lld issued %6lld full %6lld committed %6lld\n", i,
+             (long long)(kbt[0][i] - kbt[0][0]), (long long)(kbt[1][i] - kbt[0][0]),
+             (long long)(kbt[2][i] - kbt[0][0]), (long long)(kbt[3][i] - kbt[0][0]));
+  }
+#endif
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
@@ -987,7 +1091,7 @@ __global__ void mk_done_kernel(const ActionBlock* ab, uint32_t ring_mask, ExecRe
 
 cudaError_t configure_mk() {
   return cudaFuncSetAttribute(mk_infer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              227 * 1024);
+                              kMkSmemCap);
 }
 
 uint32_t mk_smem_bytes(uint32_t ring_bytes, int n_layers) {

@@ -559,18 +559,29 @@ std::string Runtime::build_plan(Arch& a, int batch) {
   // ---- shared memory: the ring takes what the plan table and scratch leave; each
   // conv layer cuts it into as many slots (A tile + B tile, 1 KB aligned) as fit.
   const int nl = (int)p.layers.size();
-  const uint32_t cap = 227 * 1024;
+  const uint32_t cap = kMkSmemCap;
   const uint32_t fixed = mk_smem_bytes(0, nl);
   if (fixed + 64 * 1024 > cap) return "plan too large for shared memory";
   p.ring_bytes = (cap - fixed) / 1024 * 1024;
   p.smem = mk_smem_bytes(p.ring_bytes, nl);
+  int kpack_env = 0, min_slots = 2 * kMkProducers;  // experiment overrides (profiling only)
+  if (const char* e = getenv("CW_KPACK")) kpack_env = atoi(e);
+  if (const char* e = getenv("CW_KPACK_MINSLOTS")) min_slots = atoi(e);
   for (auto& d : p.layers) {
     if (d.kind != MK_CONV) continue;
     const uint32_t rows = d.mode == 0 ? 128u : (uint32_t)(d.box_w * d.box_h * d.box_n);
     const uint32_t a_bytes = rows * d.kblk * 2;
     d.b_off = (int)((a_bytes + 1023) / 1024 * 1024);
-    d.slot_bytes = (int)((d.b_off + (uint32_t)d.bn * d.kblk * 2 + 1023) / 1024 * 1024);
+    d.sub_bytes = (int)((d.b_off + (uint32_t)d.bn * d.kblk * 2 + 1023) / 1024 * 1024);
+    // k-blocks per slot: 2 halves the per-k-block barrier / issue work of the producer and
+    // MMA warps when the ring still holds >= 2 slots per producer
+    int kpack = 2;
+    if (kpack_env > 0) kpack = kpack_env;
+    if ((int)(p.ring_bytes / (kpack * d.sub_bytes)) < min_slots) kpack = 1;
+    d.kpack = kpack;
+    d.slot_bytes = kpack * d.sub_bytes;
     d.slots = std::min<int>(kMkMaxSlots, p.ring_bytes / d.slot_bytes);
+    d.slots -= d.slots % kMkProducers;  // producer p owns the slots s % P == p
     if (d.slots < 2) return "ring too small for a conv tile";
   }
   if (fc_seen) {
