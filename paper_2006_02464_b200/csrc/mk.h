@@ -43,6 +43,14 @@ constexpr int kMkPadW = 4;                 // MK_INPUT: zero pixels left of ever
 constexpr uint32_t kMkTmemCols = 512;      // two accumulators of up to 256 columns
 constexpr int kMkMaxSlots = 16;            // smem ring slots (per-layer slot size)
 constexpr uint32_t kMkBarBytes = 512;
+// Epilogue staging: kMkOutBufs buffers of one 128-row x 64-column bf16 chunk (16 KB, 128-byte
+// swizzle): a chunk's residual lands there by TMA, the epilogue rewrites it in place with the
+// output, and a TMA store drains it. Also the stem-pool / split-K / avg-pool scratch.
+#ifndef CW_OUT_BUFS
+#define CW_OUT_BUFS 4
+#endif
+constexpr int kMkOutBufs = CW_OUT_BUFS;
+constexpr uint32_t kMkOutBufBytes = 16384;
 #ifdef CW_KB_TRACE
 constexpr uint32_t kMkSmemCap = 224 * 1024;  // debug builds keep a static trace array
 #else
@@ -59,7 +67,7 @@ struct MkLayer {
   int32_t relu, wlayer, n_out, tmap, red_rows, kblk;  // kblk: K elements per k-block (64 or 32)
   int32_t slots, slot_bytes, b_off;  // smem ring geometry of this layer (B tile at b_off in a sub-slot)
   int32_t kpack, sub_bytes;  // k-blocks per ring slot (sub-slots of sub_bytes) behind one barrier
-  int32_t pad_[2];
+  int32_t tmap_out, tmap_res;  // TMA store / residual-load maps (64-column boxes), -1 if unused
   // stem with fused 3x3/s2/p1 max pool: pooled columns per tile (0 = no fusion);
   // a tile covers conv rows 2ph-1..2ph+1 and conv columns 2pw0-1..2pw0+2*pool_pw-1
   int32_t pool_pw, pool_oh;

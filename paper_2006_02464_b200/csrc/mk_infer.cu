@@ -519,19 +519,23 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   const uint32_t ring_bytes = args.ring_bytes;
-  // Layout after the ring: barriers, tmem/gen slots, bias [2][256] f32, pool scratch
-  // [128][17] f32, then the plan's layer table.
-  const uint32_t bar_full = sbase + ring_bytes;
+  // Layout after the ring: epilogue staging buffers (1024-aligned), barriers, tmem/gen slots,
+  // bias [2][256] f32, then the plan's layer table.
+  uint8_t* obufs = smem + ring_bytes;
+  const uint32_t obase = sbase + ring_bytes;
+  const uint32_t bar_full = obase + kMkOutBufs * kMkOutBufBytes;
   const uint32_t bar_empty = bar_full + 8 * kMkMaxSlots;
   const uint32_t bar_tfull = bar_empty + 8 * kMkMaxSlots;  // 2 x 8 B
   const uint32_t bar_tempty = bar_tfull + 2 * 8;          // 2 x 8 B
   const uint32_t bar_simt = bar_tempty + 2 * 8;           // SIMT-layer bulk copies
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + ring_bytes + kMkBarBytes - 32);
+  const uint32_t bar_res = bar_simt + 8;                  // kMkOutBufs x 8 B: residual chunks
+  uint8_t* bar_area = obufs + kMkOutBufs * kMkOutBufBytes;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_area + kMkBarBytes - 32);
   uint32_t* gen_slot = tmem_slot + 1;
-  float* sbias = reinterpret_cast<float*>(smem + ring_bytes + kMkBarBytes);
-  float* sred = sbias + 2 * 256;
-  uint4* sstage = reinterpret_cast<uint4*>(sred + 128 * 17);  // 4 warps x 4 KB
-  MkLayer* sl = reinterpret_cast<MkLayer*>(sstage + 4 * 4096 / 16);
+  float* sbias = reinterpret_cast<float*>(bar_area + kMkBarBytes);
+  float* sred = reinterpret_cast<float*>(obufs + kMkOutBufBytes);  // [128][17] f32 (avg pool)
+  uint4* sstage = reinterpret_cast<uint4*>(obufs);                 // stem pool / split-K staging
+  MkLayer* sl = reinterpret_cast<MkLayer*>(sbias + 2 * 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -560,6 +564,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
       mbar_init(bar_tempty + 8 * a, 4);
     }
     mbar_init(bar_simt, 1);
+    for (int b = 0; b < kMkOutBufs; ++b) mbar_init(bar_res + 8 * b, 1);
     fence_mbar_init();
     *gen_slot = *reinterpret_cast<const volatile uint32_t*>(args.gen);
   }
@@ -826,6 +831,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     const int q = warp & 3;  // TMEM lane quarter
     const int row = q * 32 + lane;
     const int et = threadIdx.x - 64;
+    uint32_t ocnt = 0;  // TMA-epilogue chunks staged so far (buffer ocnt % kMkOutBufs)
+    uint32_t rpar = 0;  // bit b: phase parity of the next residual landing in buffer b
     // per-warp staging: 32 rows x 128 B, 16-byte chunks XOR-swizzled by row
     uint8_t* stg = reinterpret_cast<uint8_t*>(sstage) + (warp - 2) * 4096;
     auto stg_chunk = [stg](int r, int c) {
@@ -936,26 +943,27 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                 named_bar(1, 128);
               }
             } else {
-              // 64-column chunks: accumulators (+ bias, + residual, ReLU) -> bf16 rows in the
-              // warp's staging buffer -> coalesced row stores (8 lanes x 16 B per 128-byte
-              // row segment). The residual chunk comes in the same coalesced way.
-              uint32_t mr[8];  // element offset of the row's first column in this tile (< 2^32)
-              uint32_t vmask = 0;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                long long mm;
-                if (row_pixel(d, o, q * 32 + i * 4 + (lane >> 3), &mm)) vmask |= 1u << i;
-                mr[i] = (uint32_t)(mm * d.n_out + o.n0);
-              }
-              const int ch = lane & 7;
-              const __nv_bfloat16* res = reinterpret_cast<const __nv_bfloat16*>(d.res);
-              __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(d.out);
-              uint4 rr[8];
-              if (res) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                  if (vmask >> i & 1)
-                    rr[i] = __ldcg(reinterpret_cast<const uint4*>(res + mr[i]) + ch);
+              // TMA epilogue, 64-column chunks through the staging buffers (running chunk
+              // counter ocnt, buffer ocnt % kMkOutBufs): the residual chunk lands by TMA
+              // (issued kMkOutBufs-1 chunks ahead, the first ones before the accumulator
+              // wait), each thread rewrites its row in place with bias + residual (+ ReLU) in
+              // bf16, and one thread drains the chunk with a TMA store (partial tiles are
+              // clipped by the tensor map bounds).
+              const CUtensorMap* tmo = args.tmaps + d.tmap_out;
+              const CUtensorMap* tmr = d.res ? args.tmaps + d.tmap_res : nullptr;
+              const int nch = d.bn >> 6;
+              const bool m2d = d.mode == 0;
+              auto issue_res = [&](uint32_t b, int c) {
+                const uint32_t dst = obase + b * kMkOutBufBytes, bar = bar_res + 8 * b;
+                mbar_arrive_expect_tx(bar, a_rows(d) * 128u);  // the box: tile rows x 64 cols
+                if (m2d) tma_load_2d(dst, tmr, bar, o.n0 + 64 * c, o.m0);
+                else tma_load_4d(dst, tmr, bar, o.n0 + 64 * c, o.ow0, o.oh0, o.img0);
+              };
+              if (tmr && et == 0) {
+                for (int j = 0; j < nch && j < kMkOutBufs - 1; ++j) {
+                  bulk_wait_read_n(kMkOutBufs - 1 - j);  // the buffer's previous store has read it
+                  issue_res((ocnt + j) % kMkOutBufs, j);
+                }
               }
               mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 8);
               tc_fence_after();
@@ -963,24 +971,22 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                 args.trace[((size_t)L * G + cta) * 4 + 2] = globaltimer();
               first = false;
               if (!bias_fixed) named_bar(1, 128);  // bias staged
-              for (int c = 0; c < d.bn; c += 64) {
-                if (res) {
-#pragma unroll
-                  for (int i = 0; i < 8; ++i) *stg_chunk(i * 4 + (lane >> 3), ch) = rr[i];
-                  if (c + 64 < d.bn) {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                      if (vmask >> i & 1)
-                        rr[i] = __ldcg(reinterpret_cast<const uint4*>(res + mr[i] + c + 64) + ch);
-                  }
+              for (int c = 0; c < nch; ++c, ++ocnt) {
+                const uint32_t b = ocnt % kMkOutBufs;
+                uint8_t* buf = obufs + b * kMkOutBufBytes;
+                auto chunk = [buf, row](int k) {
+                  return reinterpret_cast<uint4*>(buf + row * 128 + ((k ^ (row & 7)) << 4));
+                };
+                if (tmr) {
+                  mbar_wait_to<64>(bar_res + 8 * b, (rpar >> b) & 1, 11);
+                  rpar ^= 1u << b;
                 }
-                __syncwarp();
                 // two 32-column halves keep the accumulator registers at 32
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                   uint32_t v[32];
-                  tmem_ld16(taddr + c + 32 * h, *reinterpret_cast<uint32_t(*)[16]>(v));
-                  tmem_ld16(taddr + c + 32 * h + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+                  tmem_ld16(taddr + 64 * c + 32 * h, *reinterpret_cast<uint32_t(*)[16]>(v));
+                  tmem_ld16(taddr + 64 * c + 32 * h + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
                   tmem_ld_wait();
 #pragma unroll
                   for (int kk = 0; kk < 4; ++kk) {
@@ -988,10 +994,10 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                     float f[8];
 #pragma unroll
                     for (int e = 0; e < 8; ++e)
-                      f[e] = __uint_as_float(v[8 * kk + e]) + bias[c + 8 * k + e];
-                    if (res) {
+                      f[e] = __uint_as_float(v[8 * kk + e]) + bias[64 * c + 8 * k + e];
+                    if (tmr) {
                       float rf[8];
-                      bf16x8_to_f32(*stg_chunk(lane, k), rf);
+                      bf16x8_to_f32(*chunk(k), rf);
 #pragma unroll
                       for (int e = 0; e < 8; ++e) f[e] += rf[e];
                     }
@@ -1004,16 +1010,23 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                     w.y = pack_bf16x2(f[2], f[3]);
                     w.z = pack_bf16x2(f[4], f[5]);
                     w.w = pack_bf16x2(f[6], f[7]);
-                    *stg_chunk(lane, k) = w;
+                    *chunk(k) = w;
                   }
                 }
-                __syncwarp();
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                  if (vmask >> i & 1)
-                    reinterpret_cast<uint4*>(out + mr[i] + c)[ch] =
-                        *stg_chunk(i * 4 + (lane >> 3), ch);
-                __syncwarp();
+                fence_proxy_async_smem();
+                // before the barrier: the store that last used the NEXT chunk's buffer has read it
+                if (et == 0) bulk_wait_read<kMkOutBufs - 2>();
+                named_bar(1, 128);
+                if (et == 0) {
+                  const uint32_t src = obase + b * kMkOutBufBytes;
+                  if (m2d) tma_store_2d(tmo, src, o.n0 + 64 * c, o.m0);
+                  else tma_store_4d(tmo, src, o.n0 + 64 * c, o.ow0, o.oh0, o.img0);
+                  bulk_commit();
+                  if (tmr && c + kMkOutBufs - 1 < nch) {
+                    bulk_wait_read<1>();  // buffer of chunk ocnt-1 (the next residual's) is free
+                    issue_res((ocnt + kMkOutBufs - 1) % kMkOutBufs, c + kMkOutBufs - 1);
+                  }
+                }
               }
             }
           }
@@ -1023,7 +1036,12 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-        // one release per layer and CTA: all of its tasks' stores (cumulative over the bar.sync)
+        // one release per layer and CTA: all of its tasks' stores (the TMA stores complete,
+        // the threads' own stores cumulative over the bar.sync)
+        if (et == 0) {
+          bulk_wait_all();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         named_bar(1, 128);
         if (et == 0) red_release_add(counters + L, (uint32_t)done);
       } else {
@@ -1095,7 +1113,7 @@ cudaError_t configure_mk() {
 }
 
 uint32_t mk_smem_bytes(uint32_t ring_bytes, int n_layers) {
-  return 1024 + ring_bytes + kMkBarBytes + 2 * 256 * 4 + 128 * 17 * 4 + 4 * 4096 +
+  return 1024 + ring_bytes + kMkOutBufs * kMkOutBufBytes + kMkBarBytes + 2 * 256 * 4 +
          n_layers * (uint32_t)sizeof(MkLayer);
 }
 

@@ -474,6 +474,25 @@ std::string Runtime::build_plan(Arch& a, int batch) {
         plan_conv(d, op.cout, G, !fuse_pool && !d.pool_pw);
         d.tmap = (int)p.tmaps.size();
         p.tmaps.push_back(tm);
+        d.tmap_out = d.tmap_res = -1;
+        if (!d.pool_pw && !fuse_pool && d.splits == 1) {
+          // TMA-store epilogue: 64-column boxes over the output (and residual) tiles
+          auto out_map = [&](CUtensorMap* m, const void* base) {
+            return d.mode == 0 ? make_tmap_2d(m, base, (uint64_t)op.cout, (uint64_t)d.m_total, 128)
+                               : make_tmap_nhwc(m, base, batch, op.out_h, op.out_w, op.cout, d.box_w,
+                                                d.box_h, d.box_n, 1);
+          };
+          CUtensorMap mo;
+          if (!out_map(&mo, out)) return "tensor map (output) failed";
+          d.tmap_out = (int)p.tmaps.size();
+          p.tmaps.push_back(mo);
+          if (d.res) {
+            CUtensorMap mr;
+            if (!out_map(&mr, d.res)) return "tensor map (residual) failed";
+            d.tmap_res = (int)p.tmaps.size();
+            p.tmaps.push_back(mr);
+          }
+        }
         std::vector<int> rd = {op.in_buf}, wr;
         if (d.pool_pw) {
           wr.push_back(nxt->out_buf);
