@@ -224,35 +224,55 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
 // ------------------------------------------------------------------ SIMT layers
 // All run on the 128 epilogue threads of every CTA (et = 0..127, G CTAs).
 
-__device__ __noinline__ void simt_input(const MkLayer& d, const ActionBlock* ab, int cta, int G, int et) {
-  // fp32 [C=3][H][W] per request -> bf16 [n][H][W + 2*pad][4] (pixel data at column + pad).
-  const int W4 = d.W / 4;
-  const int items = d.batch * d.H * W4;
-  const int Wp = d.W + 2 * kMkPadW;
+// fp32 [C=3][H][W] per request -> bf16 [n][H][W + 2*pad][4] (pixel data at column + pad).
+// The CTA's image rows (a contiguous range of (n, h)) come in by bulk copies (plane-major,
+// up to 64 KB per phase into the epilogue staging buffers): generic loads would be capped by
+// the few KB of L1 the megakernel leaves; the conversion then reads shared memory only.
+__device__ __noinline__ void simt_input(const MkLayer& d, const ActionBlock* ab, int cta, int G,
+                                        int et, float* stage, uint32_t stage_addr, uint32_t bar,
+                                        uint32_t& phase) {
+  const int W = d.W, H = d.H, W4 = W / 4, Wp = W + 2 * kMkPadW;
+  const int rows_total = d.batch * H;
+  const int R = (rows_total + G - 1) / G;
+  const int r0 = cta * R, r1 = min(rows_total, r0 + R);
+  const int P = (int)(kMkOutBufs * kMkOutBufBytes / (3u * W * 4u));  // rows per phase
+  const long long plane = (long long)H * W;
   uint2* out = reinterpret_cast<uint2*>(d.out);
-  const long long plane = (long long)d.H * d.W;
-#pragma unroll 4
-  for (int it = cta * 128 + et; it < items; it += G * 128) {
-    const int w4 = it % W4;
-    const int t = it / W4;
-    const int h = t % d.H;
-    const int n = t / d.H;
-    const float* img = ab->in[n] + (long long)h * d.W + w4 * 4;
-    const float4 r = __ldcs(reinterpret_cast<const float4*>(img));
-    const float4 g = __ldcs(reinterpret_cast<const float4*>(img + plane));
-    const float4 b = __ldcs(reinterpret_cast<const float4*>(img + 2 * plane));
-    uint2* o = out + ((long long)n * d.H + h) * Wp + kMkPadW + w4 * 4;
-    uint4 p0, p1;
-    p0.x = pack_bf16x2(r.x, g.x);
-    p0.y = pack_bf16x2(b.x, 0.0f);
-    p0.z = pack_bf16x2(r.y, g.y);
-    p0.w = pack_bf16x2(b.y, 0.0f);
-    p1.x = pack_bf16x2(r.z, g.z);
-    p1.y = pack_bf16x2(b.z, 0.0f);
-    p1.z = pack_bf16x2(r.w, g.w);
-    p1.w = pack_bf16x2(b.w, 0.0f);
-    reinterpret_cast<uint4*>(o)[0] = p0;
-    reinterpret_cast<uint4*>(o)[1] = p1;
+  for (int pr = r0; pr < r1; pr += P) {
+    const int pe = min(r1, pr + P), nr = pe - pr;
+    if (et == 0) {
+      mbar_arrive_expect_tx(bar, (uint32_t)(3 * nr * W * 4));
+      for (int a = pr; a < pe;) {
+        const int n = a / H, h = a - n * H;
+        const int b = min(pe, (n + 1) * H);  // rows of this image in the phase
+        for (int p = 0; p < 3; ++p)
+          bulk_g2s(stage_addr + (uint32_t)((p * P + (a - pr)) * W * 4),
+                   ab->in[n] + p * plane + (long long)h * W, (uint32_t)((b - a) * W * 4), bar);
+        a = b;
+      }
+    }
+    mbar_wait_to<64>(bar, phase & 1, 12);
+    ++phase;
+    for (int it = et; it < nr * W4; it += 128) {
+      const int i = it / W4, w4 = it - i * W4;
+      const int a = pr + i, n = a / H, h = a - n * H;
+      const float4 r = *reinterpret_cast<const float4*>(stage + (0 * P + i) * W + w4 * 4);
+      const float4 g = *reinterpret_cast<const float4*>(stage + (1 * P + i) * W + w4 * 4);
+      const float4 b = *reinterpret_cast<const float4*>(stage + (2 * P + i) * W + w4 * 4);
+      uint2* o = out + ((long long)n * H + h) * Wp + kMkPadW + w4 * 4;
+      uint4 p0, p1;
+      p0.x = pack_bf16x2(r.x, g.x);
+      p0.y = pack_bf16x2(b.x, 0.0f);
+      p0.z = pack_bf16x2(r.y, g.y);
+      p0.w = pack_bf16x2(b.y, 0.0f);
+      p1.x = pack_bf16x2(r.z, g.z);
+      p1.y = pack_bf16x2(b.z, 0.0f);
+      p1.z = pack_bf16x2(r.w, g.w);
+      p1.w = pack_bf16x2(b.w, 0.0f);
+      reinterpret_cast<uint4*>(o)[0] = p0;
+      reinterpret_cast<uint4*>(o)[1] = p1;
+    }
+    named_bar(1, 128);  // the stage is read before the next phase overwrites it
   }
 }
 
@@ -319,54 +339,106 @@ __device__ __noinline__ void simt_avgpool(const MkLayer& d, int cta, int G, int 
   }
 }
 
-// logits[n][j] = pooled[n] . W[j] + bias[j]; pooled staged in (idle) ring smem.
-// One warp per class; C % 256 == 0, C <= 2048.
-__device__ void simt_fc(const MkLayer& d, const ActionBlock* ab, const uint8_t* hdr, float* sp,
-                        uint32_t bar, int cta, int G, int et) {
-  const float* pooled = reinterpret_cast<const float*>(d.in);
-  const int nb = d.batch, C = d.C;
-  // one bulk async copy of the pooled features [nb][C] into shared memory
-  if (et == 0) {
-    fence_proxy_async();
-    const uint32_t bytes = (uint32_t)(nb * C * 4);
-    mbar_arrive_expect_tx(bar, bytes);
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(sp)), "l"(pooled), "r"(bytes), "r"(bar)
-        : "memory");
-  }
-  mbar_wait_to<kEpiWaitNs>(bar, 0, 10);
-  const int warp = et >> 5, lane = et & 31;
+// logits[n][j] = pooled[n] . W[j] + bias[j]. Each CTA takes blocks of <= 8 classes. The
+// pooled features [batch][C] fp32 (into the idle ring) and the block's weight rows (into the
+// staging buffers) arrive by bulk copies; the 128 threads are (image n) x (128 / pow2(batch)
+// K parts, interleaved 8-element chunks): a thread reads its part of pooled[n] once per block
+// and accumulates all the block's classes from it, then the K parts reduce (shuffles, and
+// shared memory when an image spans several warps). C % 64 == 0, batch <= 16.
+__device__ __noinline__ void simt_fc(const MkLayer& d, const ActionBlock* ab, const uint8_t* hdr,
+                                     int cta, int G, int et, float* sp, uint32_t sp_addr,
+                                     const __nv_bfloat16* sw, uint32_t sw_addr, float* sred,
+                                     uint32_t bar, uint32_t& phase) {
+  const int C = d.C;
+  int nbp = 1;
+  while (nbp < d.batch) nbp <<= 1;
+  const int parts = 128 / nbp, n = et / parts, part = et % parts;
   const __nv_bfloat16* wbase =
       reinterpret_cast<const __nv_bfloat16* const*>(hdr + kHdrWeightOff)[d.wlayer];
   const float* bias = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[d.wlayer];
-  const int chunks = C / 256;
-  for (int j = cta * 4 + warp; j < d.classes; j += G * 4) {
-    const __nv_bfloat16* w = wbase + (long long)j * C;
-    float wf[64];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (i < chunks) bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(w + (i * 32 + lane) * 8)),
-                                    wf + i * 8);
+  const int ngroups = (d.classes + 7) / 8;
+  bool pooled_in = false;
+  for (int g = cta; g < ngroups; g += G) {
+    const int j0 = g * 8;
+    const int nj = min(8, d.classes - j0);
+    if (et == 0) {
+      fence_proxy_async();  // pooled was written by generic stores of other CTAs
+      const uint32_t wbytes = (uint32_t)(nj * C * 2);
+      const uint32_t pbytes = pooled_in ? 0u : (uint32_t)(d.batch * C * 4);
+      mbar_arrive_expect_tx(bar, wbytes + pbytes);
+      if (!pooled_in) bulk_g2s(sp_addr, d.in, pbytes, bar);
+      bulk_g2s(sw_addr, wbase + (size_t)j0 * C, wbytes, bar);
     }
-    const float b = __ldg(bias + j);
-    for (int n = 0; n < nb; ++n) {
-      const float* pn = sp + n * C;
-      float acc = 0.0f;
+    pooled_in = true;
+    // epilogue operands fetched while the copies fly (global latency, not on the tail)
+    float bj[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        if (i < chunks) {
-          const float4 p0 = *reinterpret_cast<const float4*>(pn + (i * 32 + lane) * 8);
-          const float4 p1 = *reinterpret_cast<const float4*>(pn + (i * 32 + lane) * 8 + 4);
-          acc += wf[i * 8 + 0] * p0.x + wf[i * 8 + 1] * p0.y + wf[i * 8 + 2] * p0.z +
-                 wf[i * 8 + 3] * p0.w + wf[i * 8 + 4] * p1.x + wf[i * 8 + 5] * p1.y +
-                 wf[i * 8 + 6] * p1.z + wf[i * 8 + 7] * p1.w;
+    for (int jj = 0; jj < 8; ++jj) bj[jj] = jj < nj ? __ldg(bias + j0 + jj) : 0.0f;
+    float* const outn = (part == 0 && n < d.batch) ? ab->out[n] : nullptr;
+#ifdef CW_KB_TRACE
+    const long long tf0 = clock64();
+#endif
+    mbar_wait_to<64>(bar, phase & 1, 10);
+    ++phase;
+#ifdef CW_KB_TRACE
+    const long long tf1 = clock64();
+#endif
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (n < d.batch) {
+      // interleaved 8-element K chunks: consecutive threads read consecutive 16-byte words
+      const float* pn = sp + n * C;
+#pragma unroll 2
+      for (int k = part * 8; k < C; k += parts * 8) {
+        const float4 p0 = *reinterpret_cast<const float4*>(pn + k);
+        const float4 p1 = *reinterpret_cast<const float4*>(pn + k + 4);
+        const float pv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+        // all 8 rows' words first (rows >= nj hold stale data: their sums are discarded)
+        uint4 wv[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) wv[jj] = *reinterpret_cast<const uint4*>(sw + jj * C + k);
+#pragma unroll
+        for (int e2 = 0; e2 < 4; ++e2) {
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const uint32_t u = e2 == 0 ? wv[jj].x : e2 == 1 ? wv[jj].y : e2 == 2 ? wv[jj].z : wv[jj].w;
+            acc[jj] = fmaf(__uint_as_float(u << 16), pv[2 * e2], acc[jj]);
+            acc[jj] = fmaf(__uint_as_float(u & 0xFFFF0000u), pv[2 * e2 + 1], acc[jj]);
+          }
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) ab->out[n][j] = acc + b;
     }
+    const int wl = parts < 32 ? parts : 32;  // lanes of one image within a warp
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      float v = acc[jj];
+      for (int o = wl >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      acc[jj] = v;
+    }
+    if (parts > 32) {  // one image spans parts / 32 warps: finish through shared memory
+      if ((et & 31) == 0)
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) sred[(et >> 5) * 8 + jj] = acc[jj];
+      named_bar(1, 128);
+      if ((et & 31) == 0) {
+        const int w0 = (et >> 5) / (parts >> 5) * (parts >> 5);
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          float v = 0.0f;
+          for (int w = w0; w < w0 + (parts >> 5); ++w) v += sred[w * 8 + jj];
+          acc[jj] = v;
+        }
+      }
+    }
+    if (outn) {
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        if (jj < nj) outn[j0 + jj] = acc[jj] + bj[jj];
+    }
+#ifdef CW_KB_TRACE
+    if (et == 0 && (cta == 0 || cta == 100))
+      printf("fc cta %d: copy wait %lld, compute %lld cycles\n", cta, tf1 - tf0, clock64() - tf1);
+#endif
+    named_bar(1, 128);  // weights read before the next block's copy
   }
 }
 
@@ -542,7 +614,17 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   const int cta = blockIdx.x;
 #ifdef CW_KB_TRACE
   __shared__ uint64_t kbt[4][64];  // debug: producer acquire / A issued, MMA full / committed
-  int kbp = 0, kbm = 0;
+  __shared__ uint64_t ket[2][64];  // debug: epilogue events (clock, tag)
+  int kbp = 0, kbm = 0, kbe = 0;
+#define CW_KET(tag_)                                                   \
+  do {                                                                 \
+    if (cta == 0 && et == 0 && kbe < 64) {                             \
+      ket[0][kbe] = clock64();                                         \
+      ket[1][kbe++] = (tag_);                                          \
+    }                                                                  \
+  } while (0)
+#else
+#define CW_KET(tag_) do {} while (0)
 #endif
   const int G = gridDim.x;
   const int nl = args.n_layers;
@@ -833,6 +915,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     const int et = threadIdx.x - 64;
     uint32_t ocnt = 0;  // TMA-epilogue chunks staged so far (buffer ocnt % kMkOutBufs)
     uint32_t rpar = 0;  // bit b: phase parity of the next residual landing in buffer b
+    uint32_t simt_phase = 0;  // completed phases of bar_simt (SIMT-layer bulk copies)
     // per-warp staging: 32 rows x 128 B, 16-byte chunks XOR-swizzled by row
     uint8_t* stg = reinterpret_cast<uint8_t*>(sstage) + (warp - 2) * 4096;
     auto stg_chunk = [stg](int r, int c) {
@@ -965,8 +1048,10 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                   issue_res((ocnt + j) % kMkOutBufs, j);
                 }
               }
+              CW_KET(100 + t / G);
               mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 8);
               tc_fence_after();
+              CW_KET(1);
               if (first && et == 0 && args.trace)
                 args.trace[((size_t)L * G + cta) * 4 + 2] = globaltimer();
               first = false;
@@ -981,6 +1066,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                   mbar_wait_to<64>(bar_res + 8 * b, (rpar >> b) & 1, 11);
                   rpar ^= 1u << b;
                 }
+                CW_KET(10 + c);
                 // two 32-column halves keep the accumulator registers at 32
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
@@ -991,10 +1077,12 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
 #pragma unroll
                   for (int kk = 0; kk < 4; ++kk) {
                     const int k = 4 * h + kk;
+                    const float4 b0 = *reinterpret_cast<const float4*>(bias + 64 * c + 8 * k);
+                    const float4 b1 = *reinterpret_cast<const float4*>(bias + 64 * c + 8 * k + 4);
+                    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
                     float f[8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                      f[e] = __uint_as_float(v[8 * kk + e]) + bias[64 * c + 8 * k + e];
+                    for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[8 * kk + e]) + bb[e];
                     if (tmr) {
                       float rf[8];
                       bf16x8_to_f32(*chunk(k), rf);
@@ -1015,8 +1103,10 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                 }
                 fence_proxy_async_smem();
                 // before the barrier: the store that last used the NEXT chunk's buffer has read it
+                CW_KET(20 + c);
                 if (et == 0) bulk_wait_read<kMkOutBufs - 2>();
                 named_bar(1, 128);
+                CW_KET(30 + c);
                 if (et == 0) {
                   const uint32_t src = obase + b * kMkOutBufBytes;
                   if (m2d) tma_store_2d(tmo, src, o.n0 + 64 * c, o.m0);
@@ -1038,12 +1128,15 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         }
         // one release per layer and CTA: all of its tasks' stores (the TMA stores complete,
         // the threads' own stores cumulative over the bar.sync)
+        CW_KET(90);
         if (et == 0) {
           bulk_wait_all();
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
+        CW_KET(91);
         named_bar(1, 128);
         if (et == 0) red_release_add(counters + L, (uint32_t)done);
+        CW_KET(92);
       } else {
         // SIMT layer (every CTA takes part; MK_REDUCE: its own task list)
         const MkLayer& d = sl[L];
@@ -1053,11 +1146,15 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         if (args.trace && et == 0) args.trace[((size_t)L * G + cta) * 4 + 1] = globaltimer();
         int done = 1;
         switch (d.kind) {
-          case MK_INPUT: simt_input(d, ab, cta, G, et); break;
+          case MK_INPUT:
+            simt_input(d, ab, cta, G, et, reinterpret_cast<float*>(obufs), obase, bar_simt, simt_phase);
+            break;
           case MK_MAXPOOL: simt_maxpool(d, cta, G, et); break;
           case MK_AVGPOOL: simt_avgpool(d, cta, G, et); break;
           case MK_FC:
-            simt_fc(d, ab, hdr, reinterpret_cast<float*>(smem), bar_simt, cta, G, et);
+            simt_fc(d, ab, hdr, cta, G, et, reinterpret_cast<float*>(smem), sbase,
+                    reinterpret_cast<const __nv_bfloat16*>(obufs), obase,
+                    reinterpret_cast<float*>(obufs + 3 * kMkOutBufBytes), bar_simt, simt_phase);
             break;
           case MK_REDUCE: {
             done = 0;
@@ -1076,6 +1173,10 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   tc_fence_before();
   __syncthreads();
 #ifdef CW_KB_TRACE
+  if (cta == 0 && threadIdx.x == 64) {
+    for (int i = 0; i < kbe; ++i)
+      printf("ep %2d tag %3d t %6lld\n", i, (int)ket[1][i], (long long)(ket[0][i] - ket[0][0]));
+  }
   if (cta == 0 && threadIdx.x == 0) {
     for (int i = 0; i < 40; ++i)
       printf("kb %2d acq %6lld issued %6lld full %6lld committed %6lld\n", i,

@@ -564,7 +564,8 @@ std::string Runtime::build_plan(Arch& a, int batch) {
         d.wlayer = op.layer;
         d.C = op.cin;
         d.classes = op.cout;
-        if (op.cin % 256 || op.cin > 2048) return "fc input features must be a multiple of 256, <= 2048";
+        if (op.cin % 64) return "fc input features must be a multiple of 64";
+        if (batch > 16) return "fc batch must be <= 16";
         fc_seen = true;
         err = push(d, (int)oi, {op.in_buf}, {});
         break;
@@ -605,7 +606,8 @@ std::string Runtime::build_plan(Arch& a, int batch) {
   }
   if (fc_seen) {
     const MkLayer& f = p.layers.back();
-    if ((size_t)batch * f.C * 4 > p.ring_bytes) return "fc staging exceeds smem";
+    if ((size_t)batch * f.C * 4 > p.ring_bytes) return "fc: pooled features exceed the ring";
+    if ((size_t)8 * f.C * 2 > (size_t)kMkOutBufs * kMkOutBufBytes) return "fc: weight block exceeds staging";
   }
   if (mk_blocks_per_sm(p.smem) < 1) return "megakernel does not fit on an SM";
   p.grid = G;
