@@ -40,6 +40,18 @@ constexpr int kMkProducers = CW_PRODUCERS;
 constexpr int kMkThreads = 192 + 32 * (kMkProducers - 1);
 constexpr uint32_t kMkATile = 128 * 128;   // A tile: 128 rows x 128 B
 constexpr int kMkPadW = 4;                 // MK_INPUT: zero pixels left of every row
+constexpr int kMkPadH = 3;                 // MK_INPUT: zero rows above and below every image
+// stem (mode 2): one task = 3 conv rows x kMkStemW conv columns (120 rows of the A tile);
+// its A operand (all 7 kernel rows) is ONE 5D TMA box of 7 sub-tiles of kMkStemSub bytes
+constexpr int kMkStemW = 40;
+constexpr uint32_t kMkStemSub = 3u * kMkStemW * 64u;  // 7680 B: 512-B aligned (64-B swizzle atoms)
+// staging-buffer map: resident stem weights [0, 28 KB) (written by the producer while the
+// input conversion still runs), input-conversion stage [32 KB, 64 KB), stem-pool / split-K
+// scratch at 32 KB, avg-pool scratch at 16 KB
+constexpr uint32_t kMkStemB = 0;
+constexpr uint32_t kMkInputStage = 32768;
+constexpr uint32_t kMkScratch = 32768;
+constexpr uint32_t kMkPoolStage = 49152;  // stem: pooled pixels of one tile (TMA-store source)
 constexpr uint32_t kMkTmemCols = 512;      // two accumulators of up to 256 columns
 constexpr int kMkMaxSlots = 16;            // smem ring slots (per-layer slot size)
 constexpr uint32_t kMkBarBytes = 512;
@@ -51,6 +63,7 @@ constexpr uint32_t kMkBarBytes = 512;
 #endif
 constexpr int kMkOutBufs = CW_OUT_BUFS;
 constexpr uint32_t kMkOutBufBytes = 16384;
+static_assert(kMkOutBufs >= 4, "the staging-buffer map (kMkStemB, kMkInputStage) needs 64 KB");
 #ifdef CW_KB_TRACE
 constexpr uint32_t kMkSmemCap = 224 * 1024;  // debug builds keep a static trace array
 #else

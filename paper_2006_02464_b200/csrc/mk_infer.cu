@@ -235,7 +235,7 @@ __device__ __noinline__ void simt_input(const MkLayer& d, const ActionBlock* ab,
   const int rows_total = d.batch * H;
   const int R = (rows_total + G - 1) / G;
   const int r0 = cta * R, r1 = min(rows_total, r0 + R);
-  const int P = (int)(kMkOutBufs * kMkOutBufBytes / (3u * W * 4u));  // rows per phase
+  const int P = (int)((kMkOutBufs * kMkOutBufBytes - kMkInputStage) / (3u * W * 4u));  // rows/phase
   const long long plane = (long long)H * W;
   uint2* out = reinterpret_cast<uint2*>(d.out);
   for (int pr = r0; pr < r1; pr += P) {
@@ -259,7 +259,7 @@ __device__ __noinline__ void simt_input(const MkLayer& d, const ActionBlock* ab,
       const float4 r = *reinterpret_cast<const float4*>(stage + (0 * P + i) * W + w4 * 4);
       const float4 g = *reinterpret_cast<const float4*>(stage + (1 * P + i) * W + w4 * 4);
       const float4 b = *reinterpret_cast<const float4*>(stage + (2 * P + i) * W + w4 * 4);
-      uint2* o = out + ((long long)n * H + h) * Wp + kMkPadW + w4 * 4;
+      uint2* o = out + ((long long)n * (H + 2 * kMkPadH) + h + kMkPadH) * Wp + kMkPadW + w4 * 4;
       uint4 p0, p1;
       p0.x = pack_bf16x2(r.x, g.x);
       p0.y = pack_bf16x2(b.x, 0.0f);
@@ -517,8 +517,14 @@ __device__ __noinline__ void simt_reduce(const MkLayer& d, const uint8_t* hdr, i
 // buffer, then each pooled pixel = max over its valid 3x3 window (identical to
 // pooling the bf16 conv output; padding = -inf = skipped).
 __device__ __noinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigin o, uint32_t taddr,
-                                           const float* bias, uint8_t* pb, int row, int et) {
+                                           const float* bias, uint8_t* pb, uint8_t* ps,
+                                           uint32_t ps_addr, const CUtensorMap* tmo, int row,
+                                           int et) {
   const MkLayer& d = *dp;
+#ifdef CW_KB_TRACE
+  const long long s0 = clock64();
+  long long s1 = 0, s2 = 0, s3 = 0;
+#endif
               {
     uint32_t v[64];
     tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(v));
@@ -529,10 +535,12 @@ __device__ __noinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigin o
     if (row < d.box_w * d.box_h) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
+        const float4 b0 = *reinterpret_cast<const float4*>(bias + 8 * k);
+        const float4 b1 = *reinterpret_cast<const float4*>(bias + 8 * k + 4);
+        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
         float f[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          f[e] = fmaxf(__uint_as_float(v[8 * k + e]) + bias[8 * k + e], 0.0f);
+        for (int e = 0; e < 8; ++e) f[e] = fmaxf(__uint_as_float(v[8 * k + e]) + bb[e], 0.0f);
         uint4 w;
         w.x = pack_bf16x2(f[0], f[1]);
         w.y = pack_bf16x2(f[2], f[3]);
@@ -542,39 +550,66 @@ __device__ __noinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigin o
       }
     }
   }
+#ifdef CW_KB_TRACE
+  s1 = clock64();
+#endif
+  if (et == 0) bulk_wait_read<0>();  // the previous tile's store has read the pooled stage
   named_bar(1, 128);
+#ifdef CW_KB_TRACE
+  s2 = clock64();
+#endif
   const int pw0 = (o.ow0 + 1) / 2, ph = (o.oh0 + 1) / 2;
-  __nv_bfloat16* pout = reinterpret_cast<__nv_bfloat16*>(d.out);
-  for (int it = et; it < d.pool_pw * 8; it += 128) {
+  // pooled pixels -> staging rows (pool_pw x 128 B, 128-byte swizzle) -> one TMA store
+  // (columns past the image are clipped by the map)
+  const int bw = d.box_w, npix = d.pool_pw * 8;
+  // validity of the tile's 3 conv rows and of its conv columns (image borders = -inf)
+  uint32_t rmask = 0;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    if (o.oh0 + r >= 0 && o.oh0 + r < d.oh) rmask |= 1u << r;
+  const int ow0 = o.ow0, ow = d.ow;
+  for (int it = et; it < npix; it += 128) {
     const int j = it >> 3, k = it & 7;
-    if (pw0 + j >= d.OW) continue;
+    uint4 v[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int cq = 0; cq < 3; ++cq) {
+        const int prow = r * bw + 2 * j + cq;  // always inside the staged tile
+        v[r * 3 + cq] = *reinterpret_cast<const uint4*>(pb + prow * 128 + ((k ^ (prow & 7)) << 4));
+      }
     float mx[8], f[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const int cr = o.oh0 + r;
-      if (cr < 0 || cr >= d.oh) continue;
+    for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int cq = 0; cq < 3; ++cq) {
-        const int c = 2 * j + cq, cc = o.ow0 + c;
-        if (cc < 0 || cc >= d.ow) continue;
-        const int prow = r * d.box_w + c;
-        bf16x8_to_f32(*reinterpret_cast<const uint4*>(pb + prow * 128 + ((k ^ (prow & 7)) << 4)), f);
+        const int cc = ow0 + 2 * j + cq;
+        const bool ok = (rmask >> r & 1) && cc >= 0 && cc < ow;
+        bf16x8_to_f32(v[r * 3 + cq], f);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) mx[e] = fmaxf(mx[e], f[e]);
+        for (int e = 0; e < 8; ++e) mx[e] = ok ? fmaxf(mx[e], f[e]) : mx[e];
       }
-    }
     uint4 w;
     w.x = pack_bf16x2(mx[0], mx[1]);
     w.y = pack_bf16x2(mx[2], mx[3]);
     w.z = pack_bf16x2(mx[4], mx[5]);
     w.w = pack_bf16x2(mx[6], mx[7]);
-    *reinterpret_cast<uint4*>(
-        pout + (((size_t)o.img0 * d.OH + ph) * d.OW + pw0 + j) * d.n_out + k * 8) = w;
+    *reinterpret_cast<uint4*>(ps + j * 128 + ((k ^ (j & 7)) << 4)) = w;
   }
+  fence_proxy_async_smem();
+  named_bar(1, 128);
+  if (et == 0) {
+    tma_store_4d(tmo, ps_addr, 0, pw0, ph, o.img0);
+    bulk_commit();
+  }
+#ifdef CW_KB_TRACE
+  s3 = clock64();
+  if (blockIdx.x == 0 && et == 0 && o.oh0 < 8)
+    printf("stem epi: stage %lld, bar %lld, pool %lld\n", s1 - s0, s2 - s1, s3 - s2);
+#endif
 }
-
 // ------------------------------------------------------------------ the kernel
 
 __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_constant__ MkArgs args) {
@@ -601,12 +636,13 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   const uint32_t bar_tempty = bar_tfull + 2 * 8;          // 2 x 8 B
   const uint32_t bar_simt = bar_tempty + 2 * 8;           // SIMT-layer bulk copies
   const uint32_t bar_res = bar_simt + 8;                  // kMkOutBufs x 8 B: residual chunks
+  const uint32_t bar_stemb = bar_res + 8 * kMkOutBufs;    // resident stem weights
   uint8_t* bar_area = obufs + kMkOutBufs * kMkOutBufBytes;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_area + kMkBarBytes - 32);
   uint32_t* gen_slot = tmem_slot + 1;
   float* sbias = reinterpret_cast<float*>(bar_area + kMkBarBytes);
   float* sred = reinterpret_cast<float*>(obufs + kMkOutBufBytes);  // [128][17] f32 (avg pool)
-  uint4* sstage = reinterpret_cast<uint4*>(obufs);                 // stem pool / split-K staging
+  uint4* sstage = reinterpret_cast<uint4*>(obufs + kMkScratch);    // stem pool / split-K staging
   MkLayer* sl = reinterpret_cast<MkLayer*>(sbias + 2 * 256);
 
   const int warp = threadIdx.x >> 5;
@@ -647,6 +683,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     }
     mbar_init(bar_simt, 1);
     for (int b = 0; b < kMkOutBufs; ++b) mbar_init(bar_res + 8 * b, 1);
+    mbar_init(bar_stemb, 1);
     fence_mbar_init();
     *gen_slot = *reinterpret_cast<const volatile uint32_t*>(args.gen);
   }
@@ -694,6 +731,35 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           if (kMkProducers > 1) named_bar(2, 32 * kMkProducers);
           cur_slots = ns;
           cur_bytes = d.slot_bytes;
+        }
+        if (d.mode == 2) {
+          // stem: weights once per layer (resident in the staging buffers), then per task ONE
+          // 5D box = the 7 kernel-row sub-tiles of the task's 3 x kMkStemW conv pixels
+          if (elect_one()) {
+            mbar_arrive_expect_tx(bar_stemb, 7u * 64u * 64u);
+            for (int r = 0; r < 7; ++r)
+              tma_load_2d(obase + kMkStemB + r * 4096u, tb, bar_stemb, r * 32, 0);
+          }
+          __syncwarp();
+          wait_deps(sl, L, counters, gen1, 2);
+          fence_proxy_async();
+          if (args.trace && lane == 0 && pw == 0)
+            args.trace[((size_t)L * G + cta) * 4 + 1] = globaltimer();
+          int slot = 0;
+          for (; t < d.tasks; t += G) {
+            const TileOrigin o = tile_origin(d, t);
+            if (slot % kMkProducers == pw) {
+              mbar_wait_to<CW_HINT_EMPTY>(bar_empty + 8 * slot, ((par >> slot) & 1) ^ 1, 3);
+              par ^= 1u << slot;
+              if (elect_one()) {
+                mbar_arrive_expect_tx(bar_full + 8 * slot, 7u * kMkStemSub);
+                tma_load_5d(sbase + slot * sb, ta, bar_full + 8 * slot, 0, o.ow0, o.oh0, 0, o.img0);
+              }
+              __syncwarp();
+            }
+            if (++slot == ns) slot = 0;
+          }
+          continue;
         }
         const uint32_t a_bytes = a_rows(d) * (uint32_t)d.kblk * 2u;
 #ifdef CW_MK_EXPERIMENTS
@@ -850,6 +916,38 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         const uint32_t sdesc = sb >> 4, subdesc = (uint32_t)d.sub_bytes >> 4;
         int slot = 0;
         bool first = true;
+        if (d.mode == 2) {
+          // stem: 7 kernel rows x 2 K=16 steps per task, A sub-tiles kMkStemSub apart in the
+          // slot, B resident (4 KB per kernel row)
+          const uint64_t bst = sw64_kmajor_desc(obase + kMkStemB);
+          mbar_wait_to<CW_HINT_FULL>(bar_stemb, 0, 5);
+          for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
+            mbar_wait_to<CW_HINT_TEMPTY>(bar_tempty + 8 * acc, acc_phase ^ 1, 4);
+            tc_fence_after();
+            const uint32_t dtm = tmem + acc * 256;
+            mbar_wait_to<CW_HINT_FULL>(bar_full + 8 * slot, (par >> slot) & 1, 5);
+            par ^= 1u << slot;
+            if (first) {
+              if (lane == 0 && args.trace) args.trace[((size_t)L * G + cta) * 4 + 3] = globaltimer();
+              first = false;
+            }
+            tc_fence_after();
+            const uint64_t ad = adesc0 + slot * sdesc;
+            if (elect_one()) {
+#pragma unroll
+              for (int r = 0; r < 7; ++r) {
+                mma_bf16(dtm, ad + r * (kMkStemSub >> 4), bst + r * (4096 >> 4), idesc, r != 0);
+                mma_bf16(dtm, ad + r * (kMkStemSub >> 4) + 2, bst + r * (4096 >> 4) + 2, idesc, 1);
+              }
+              mma_commit(bar_empty + 8 * slot);
+              mma_commit(bar_tfull + 8 * acc);
+            }
+            __syncwarp();
+            if (++slot == ns) slot = 0;
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          }
+          continue;
+        }
         for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
           const int z = t % d.splits;
           const int kb0 = z * d.kb_per_split;
@@ -980,10 +1078,15 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
             if (done > 0 && !bias_fixed)
               for (int i = et; i < d.bn; i += 128) bias[i] = __ldg(bias_all + o.n0 + i);
             if (d.pool_pw) {
+              CW_KET(200);
               mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 8);
+              CW_KET(201);
               tc_fence_after();
               named_bar(1, 128);  // bias staged; the previous tile's pooling reads are done
-              epi_stem_pool(sl + L, o, taddr, bias, reinterpret_cast<uint8_t*>(sstage), row, et);
+              epi_stem_pool(sl + L, o, taddr, bias, reinterpret_cast<uint8_t*>(sstage),
+                            obufs + kMkPoolStage, obase + kMkPoolStage, args.tmaps + d.tmap_out,
+                            row, et);
+              CW_KET(202);
             } else if (d.pool_out) {
               // Last conv: + bias (+ residual), ReLU, then a deterministic in-CTA
               // global average pool (the tile holds whole images).
@@ -1147,7 +1250,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         int done = 1;
         switch (d.kind) {
           case MK_INPUT:
-            simt_input(d, ab, cta, G, et, reinterpret_cast<float*>(obufs), obase, bar_simt, simt_phase);
+            simt_input(d, ab, cta, G, et, reinterpret_cast<float*>(obufs + kMkInputStage),
+                       obase + kMkInputStage, bar_simt, simt_phase);
             break;
           case MK_MAXPOOL: simt_maxpool(d, cta, G, et); break;
           case MK_AVGPOOL: simt_avgpool(d, cta, G, et); break;

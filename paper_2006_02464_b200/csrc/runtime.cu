@@ -194,8 +194,8 @@ std::string Runtime::register_arch(int id, const CwOp* ops, int n_ops, int n_lay
     if (op.out_buf < 0) continue;
     size_t bytes = 0;
     switch (op.kind) {
-      case OP_STEM:  // NHWC4 rows with kMkPadW zero pixels on both sides
-        bytes = (size_t)max_b * op.in_h * (op.in_w + 2 * kMkPadW) * 4 * 2;
+      case OP_STEM:  // NHWC4 rows with kMkPadW zero pixels on both sides, kMkPadH zero rows
+        bytes = (size_t)max_b * (op.in_h + 2 * kMkPadH) * (op.in_w + 2 * kMkPadW) * 4 * 2;
         break;
       case OP_CONV: bytes = (size_t)max_b * op.out_h * op.out_w * op.cout * 2; break;
       case OP_MAXPOOL: bytes = (size_t)max_b * op.out_h * op.out_w * op.cin * 2; break;
@@ -419,28 +419,23 @@ std::string Runtime::build_plan(Arch& a, int batch) {
           d.mode = 2;
           d.kblk = 32;
           d.num_kb = 7;
-          const bool fuse_max = nxt && nxt->kind == OP_MAXPOOL && nxt->in_buf == op.out_buf &&
-                                getenv("CW_NO_STEM_POOL") == nullptr;
-          if (fuse_max) {
-            // tiles of 20 pooled columns of one pooled row: 3 x 41 conv pixels (123 <= 128 rows)
-            d.pool_pw = 20;
-            d.OH = nxt->out_h;
-            d.OW = nxt->out_w;
-            d.box_w = 2 * d.pool_pw + 1;
-            d.box_h = 3;
-            d.box_n = 1;
-            d.tiles_w = (d.OW + d.pool_pw - 1) / d.pool_pw;
-            d.tiles_h = d.OH;
-            d.m_tiles = d.tiles_w * d.tiles_h * batch;
-            d.out = a.bufs[nxt->out_buf];
-          } else {
-            box_dims(batch, op.out_h, op.out_w, &d.box_w, &d.box_h, &d.box_n);
-            d.tiles_w = (op.out_w + d.box_w - 1) / d.box_w;
-            d.tiles_h = (op.out_h + d.box_h - 1) / d.box_h;
-            d.m_tiles = d.tiles_w * d.tiles_h * ((batch + d.box_n - 1) / d.box_n);
-          }
-          if (!make_tmap_stem(&tm, in, batch, op.in_h, op.in_w + 2 * kMkPadW, op.out_w, d.box_w,
-                              d.box_h, d.box_n))
+          const bool fuse_max = nxt && nxt->kind == OP_MAXPOOL && nxt->in_buf == op.out_buf;
+          if (!fuse_max || nxt->out_h * 2 != op.out_h)
+            return "the stem conv must be followed by a 3x3/s2 max pool";
+          // tiles of 19 pooled columns of one pooled row: 3 x 40 conv pixels (120 rows), all
+          // 7 kernel rows in one slot (sub-tiles kMkStemSub apart), weights resident
+          d.pool_pw = (kMkStemW - 1) / 2;
+          d.OH = nxt->out_h;
+          d.OW = nxt->out_w;
+          d.box_w = kMkStemW;
+          d.box_h = 3;
+          d.box_n = 1;
+          d.tiles_w = (d.OW + d.pool_pw - 1) / d.pool_pw;
+          d.tiles_h = d.OH;
+          d.m_tiles = d.tiles_w * d.tiles_h * batch;
+          d.out = a.bufs[nxt->out_buf];
+          if (!make_tmap_stem(&tm, in, batch, op.in_h + 2 * kMkPadH, op.in_w + 2 * kMkPadW,
+                              op.out_w, op.out_h, d.box_w, d.box_h))
             return "tensor map (stem) failed";
         } else if (!fuse_pool && op.kh == 1 && op.kw == 1 && op.stride == 1 && op.pad == 0) {
           d.mode = 0;
@@ -475,7 +470,13 @@ std::string Runtime::build_plan(Arch& a, int batch) {
         d.tmap = (int)p.tmaps.size();
         p.tmaps.push_back(tm);
         d.tmap_out = d.tmap_res = -1;
-        if (!d.pool_pw && !fuse_pool && d.splits == 1) {
+        if (d.pool_pw) {  // stem: pooled output tiles of pool_pw pixels
+          CUtensorMap mo;
+          if (!make_tmap_nhwc(&mo, d.out, batch, d.OH, d.OW, op.cout, d.pool_pw, 1, 1, 1))
+            return "tensor map (stem output) failed";
+          d.tmap_out = (int)p.tmaps.size();
+          p.tmaps.push_back(mo);
+        } else if (!fuse_pool && d.splits == 1) {
           // TMA-store epilogue: 64-column boxes over the output (and residual) tiles
           auto out_map = [&](CUtensorMap* m, const void* base) {
             return d.mode == 0 ? make_tmap_2d(m, base, (uint64_t)op.cout, (uint64_t)d.m_total, 128)
@@ -589,6 +590,16 @@ std::string Runtime::build_plan(Arch& a, int batch) {
   if (const char* e = getenv("CW_KPACK_MINSLOTS")) min_slots = atoi(e);
   for (auto& d : p.layers) {
     if (d.kind != MK_CONV) continue;
+    if (d.mode == 2) {  // stem: one slot = the 7 kernel-row A sub-tiles (weights resident)
+      d.kpack = 7;
+      d.sub_bytes = (int)kMkStemSub;
+      d.b_off = 0;
+      d.slot_bytes = (int)((7 * kMkStemSub + 1023) / 1024 * 1024);
+      d.slots = std::min<int>(kMkMaxSlots, p.ring_bytes / d.slot_bytes);
+      d.slots -= d.slots % kMkProducers;
+      if (d.slots < 2) return "ring too small for the stem";
+      continue;
+    }
     const uint32_t rows = d.mode == 0 ? 128u : (uint32_t)(d.box_w * d.box_h * d.box_n);
     const uint32_t a_bytes = rows * d.kblk * 2;
     d.b_off = (int)((a_bytes + 1023) / 1024 * 1024);

@@ -22,8 +22,9 @@ bool make_tmap_nhwc(CUtensorMap* out, const void* base, uint64_t n, uint64_t h, 
 bool make_tmap_2d_sw64(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows,
                        uint32_t box_rows);
 
-// Overlapping 8-pixel windows over NHWC4 rows for the 7x7/s2 stem (see tmap.cpp).
-bool make_tmap_stem(CUtensorMap* out, const void* base, uint64_t n, uint64_t h, uint64_t wp,
-                    uint64_t windows, uint32_t box_w, uint32_t box_h, uint32_t box_n);
+// Overlapping 8-pixel windows over NHWC4 rows for the 7x7/s2 stem (see tmap.cpp): a 5D map
+// (window elements, window, conv row, kernel row, image) over rows padded by 3 zero rows.
+bool make_tmap_stem(CUtensorMap* out, const void* base, uint64_t n, uint64_t hp, uint64_t wp,
+                    uint64_t windows, uint64_t conv_rows, uint32_t box_w, uint32_t box_h);
 
 }  // namespace cw
