@@ -33,11 +33,18 @@ constexpr int kMkMaxDeps = 6;
 #ifndef CW_PRODUCERS
 #define CW_PRODUCERS 1
 #endif
-// TMA producer warps: warp 0 (and warp 6): producer p fills the ring slots s with s % P == p, so
+// TMA producer warps: warp 0 (and warp 2): producer p fills the ring slots s with s % P == p, so
 // the issue path of P k-blocks runs in parallel (one warp's path is ~570 cycles per k-block).
 constexpr int kMkProducers = CW_PRODUCERS;
-// warp 0 (+6) TMA, warp 1 MMA, warps 2-5 epilogue / SIMT
-constexpr int kMkThreads = 192 + 32 * (kMkProducers - 1);
+// Warpgroup 0: warp 0 (+2) TMA, warp 1 MMA (registers lowered to kMkRegsCtl). Warpgroups 1-2:
+// eight epilogue / SIMT warps (registers raised to kMkRegsEpi), two per TMEM lane quarter:
+// epilogue group g = (warp - 4) / 4 takes columns [32g, 32g + 32) of every 64-column chunk.
+constexpr int kMkThreads = 384;
+constexpr int kMkEpiWarp0 = 4;
+constexpr int kMkEpiThreads = 256;
+constexpr int kMkRegsCtl = 120;
+constexpr int kMkRegsEpi = 192;
+static_assert(kMkRegsCtl * 128 + kMkRegsEpi * 256 <= 65536, "register file");
 constexpr uint32_t kMkATile = 128 * 128;   // A tile: 128 rows x 128 B
 constexpr int kMkPadW = 4;                 // MK_INPUT: zero pixels left of every row
 constexpr int kMkPadH = 3;                 // MK_INPUT: zero rows above and below every image

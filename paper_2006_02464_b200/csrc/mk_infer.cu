@@ -222,13 +222,13 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
 }
 
 // ------------------------------------------------------------------ SIMT layers
-// All run on the 128 epilogue threads of every CTA (et = 0..127, G CTAs).
+// All run on the kMkEpiThreads epilogue threads of every CTA (et = 0..255, G CTAs).
 
 // fp32 [C=3][H][W] per request -> bf16 [n][H][W + 2*pad][4] (pixel data at column + pad).
 // The CTA's image rows (a contiguous range of (n, h)) come in by bulk copies (plane-major,
 // up to 64 KB per phase into the epilogue staging buffers): generic loads would be capped by
 // the few KB of L1 the megakernel leaves; the conversion then reads shared memory only.
-__device__ __noinline__ void simt_input(const MkLayer& d, const ActionBlock* ab, int cta, int G,
+__device__ __forceinline__ void simt_input(const MkLayer& d, const ActionBlock* ab, int cta, int G,
                                         int et, float* stage, uint32_t stage_addr, uint32_t bar,
                                         uint32_t& phase) {
   const int W = d.W, H = d.H, W4 = W / 4, Wp = W + 2 * kMkPadW;
@@ -253,7 +253,7 @@ __device__ __noinline__ void simt_input(const MkLayer& d, const ActionBlock* ab,
     }
     mbar_wait_to<64>(bar, phase & 1, 12);
     ++phase;
-    for (int it = et; it < nr * W4; it += 128) {
+    for (int it = et; it < nr * W4; it += kMkEpiThreads) {
       const int i = it / W4, w4 = it - i * W4;
       const int a = pr + i, n = a / H, h = a - n * H;
       const float4 r = *reinterpret_cast<const float4*>(stage + (0 * P + i) * W + w4 * 4);
@@ -272,15 +272,15 @@ __device__ __noinline__ void simt_input(const MkLayer& d, const ActionBlock* ab,
       reinterpret_cast<uint4*>(o)[0] = p0;
       reinterpret_cast<uint4*>(o)[1] = p1;
     }
-    named_bar(1, 128);  // the stage is read before the next phase overwrites it
+    named_bar(1, kMkEpiThreads);  // the stage is read before the next phase overwrites it
   }
 }
 
-__device__ __noinline__ void simt_maxpool(const MkLayer& d, int cta, int G, int et) {
+__device__ __forceinline__ void simt_maxpool(const MkLayer& d, int cta, int G, int et) {
   const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(d.in);
   const int chunks = d.C / 8;
   const int total = d.batch * d.OH * d.OW * chunks;
-  for (int t = cta * 128 + et; t < total; t += G * 128) {
+  for (int t = cta * kMkEpiThreads + et; t < total; t += G * kMkEpiThreads) {
     const int j = t % chunks;
     const int p = t / chunks;
     const int ow = p % d.OW;
@@ -316,13 +316,13 @@ __device__ __noinline__ void simt_maxpool(const MkLayer& d, int cta, int G, int 
   }
 }
 
-__device__ __noinline__ void simt_avgpool(const MkLayer& d, int cta, int G, int et) {
+__device__ __forceinline__ void simt_avgpool(const MkLayer& d, int cta, int G, int et) {
   const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(d.in);
   const int chunks = d.C / 8;
   const int total = d.batch * chunks;
   const int HW = d.H * d.W;
   float* pooled = reinterpret_cast<float*>(d.out);
-  for (int t = cta * 128 + et; t < total; t += G * 128) {
+  for (int t = cta * kMkEpiThreads + et; t < total; t += G * kMkEpiThreads) {
     const int j = t % chunks;
     const int n = t / chunks;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, f[8];
@@ -345,14 +345,14 @@ __device__ __noinline__ void simt_avgpool(const MkLayer& d, int cta, int G, int 
 // K parts, interleaved 8-element chunks): a thread reads its part of pooled[n] once per block
 // and accumulates all the block's classes from it, then the K parts reduce (shuffles, and
 // shared memory when an image spans several warps). C % 64 == 0, batch <= 16.
-__device__ __noinline__ void simt_fc(const MkLayer& d, const ActionBlock* ab, const uint8_t* hdr,
+__device__ __forceinline__ void simt_fc(const MkLayer& d, const ActionBlock* ab, const uint8_t* hdr,
                                      int cta, int G, int et, float* sp, uint32_t sp_addr,
                                      const __nv_bfloat16* sw, uint32_t sw_addr, float* sred,
                                      uint32_t bar, uint32_t& phase) {
   const int C = d.C;
   int nbp = 1;
   while (nbp < d.batch) nbp <<= 1;
-  const int parts = 128 / nbp, n = et / parts, part = et % parts;
+  const int parts = kMkEpiThreads / nbp, n = et / parts, part = et % parts;
   const __nv_bfloat16* wbase =
       reinterpret_cast<const __nv_bfloat16* const*>(hdr + kHdrWeightOff)[d.wlayer];
   const float* bias = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[d.wlayer];
@@ -418,7 +418,7 @@ __device__ __noinline__ void simt_fc(const MkLayer& d, const ActionBlock* ab, co
       if ((et & 31) == 0)
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) sred[(et >> 5) * 8 + jj] = acc[jj];
-      named_bar(1, 128);
+      named_bar(1, kMkEpiThreads);
       if ((et & 31) == 0) {
         const int w0 = (et >> 5) / (parts >> 5) * (parts >> 5);
 #pragma unroll
@@ -438,12 +438,12 @@ __device__ __noinline__ void simt_fc(const MkLayer& d, const ActionBlock* ab, co
     if (et == 0 && (cta == 0 || cta == 100))
       printf("fc cta %d: copy wait %lld, compute %lld cycles\n", cta, tf1 - tf0, clock64() - tf1);
 #endif
-    named_bar(1, 128);  // weights read before the next block's copy
+    named_bar(1, kMkEpiThreads);  // weights read before the next block's copy
   }
 }
 
 // Split-K reduction of one task: rows [part*red_rows, +red_rows) of one tile.
-__device__ __noinline__ void simt_reduce(const MkLayer& d, const uint8_t* hdr, int task, int et) {
+__device__ __forceinline__ void simt_reduce(const MkLayer& d, const uint8_t* hdr, int task, int et) {
   const int R = d.red_parts;
   const int tile = task / R;
   const int r0 = (task - tile * R) * d.red_rows;
@@ -452,7 +452,7 @@ __device__ __noinline__ void simt_reduce(const MkLayer& d, const uint8_t* hdr, i
   const int c4n = d.bn / 4;
   const int S = d.splits;
   const float* part = d.partial + (size_t)tile * S * 128 * d.bn;
-  for (int idx = et; idx < d.red_rows * c4n; idx += 128) {
+  for (int idx = et; idx < d.red_rows * c4n; idx += kMkEpiThreads) {
     const int rr = r0 + idx / c4n;
     const int c = (idx % c4n) * 4;
     long long m;
@@ -516,37 +516,43 @@ __device__ __noinline__ void simt_reduce(const MkLayer& d, const uint8_t* hdr, i
 // (3 conv rows x 2*pool_pw+1 columns) -> bias, ReLU, bf16 into the CTA staging
 // buffer, then each pooled pixel = max over its valid 3x3 window (identical to
 // pooling the bf16 conv output; padding = -inf = skipped).
-__device__ __noinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigin o, uint32_t taddr,
+__device__ __forceinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigin o, uint32_t taddr,
                                            const float* bias, uint8_t* pb, uint8_t* ps,
                                            uint32_t ps_addr, const CUtensorMap* tmo, int row,
-                                           int et) {
+                                           int grp, int et) {
   const MkLayer& d = *dp;
 #ifdef CW_KB_TRACE
   const long long s0 = clock64();
   long long s1 = 0, s2 = 0, s3 = 0;
 #endif
-              {
-    uint32_t v[64];
-    tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(v));
-    tmem_ld16(taddr + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
-    tmem_ld16(taddr + 32, *reinterpret_cast<uint32_t(*)[16]>(v + 32));
-    tmem_ld16(taddr + 48, *reinterpret_cast<uint32_t(*)[16]>(v + 48));
+  {
+    // this thread's row, its group's 32 columns (chunks 4 grp .. 4 grp + 3)
+    uint32_t v[32];
+    tmem_ld16(taddr + 32 * grp, *reinterpret_cast<uint32_t(*)[16]>(v));
+    tmem_ld16(taddr + 32 * grp + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
     tmem_ld_wait();
     if (row < d.box_w * d.box_h) {
+      uint4 wv[4];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = 4 * grp + kk;
         const float4 b0 = *reinterpret_cast<const float4*>(bias + 8 * k);
         const float4 b1 = *reinterpret_cast<const float4*>(bias + 8 * k + 4);
         const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
         float f[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = fmaxf(__uint_as_float(v[8 * k + e]) + bb[e], 0.0f);
-        uint4 w;
-        w.x = pack_bf16x2(f[0], f[1]);
-        w.y = pack_bf16x2(f[2], f[3]);
-        w.z = pack_bf16x2(f[4], f[5]);
-        w.w = pack_bf16x2(f[6], f[7]);
-        *reinterpret_cast<uint4*>(pb + row * 128 + ((k ^ (row & 7)) << 4)) = w;
+        for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[8 * kk + e]);
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) fadd2(f[e], f[e + 1], bb[e], bb[e + 1]);
+        wv[kk].x = pack_bf16x2_relu(f[0], f[1]);
+        wv[kk].y = pack_bf16x2_relu(f[2], f[3]);
+        wv[kk].z = pack_bf16x2_relu(f[4], f[5]);
+        wv[kk].w = pack_bf16x2_relu(f[6], f[7]);
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = 4 * grp + kk;
+        *reinterpret_cast<uint4*>(pb + row * 128 + ((k ^ (row & 7)) << 4)) = wv[kk];
       }
     }
   }
@@ -554,7 +560,7 @@ __device__ __noinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigin o
   s1 = clock64();
 #endif
   if (et == 0) bulk_wait_read<0>();  // the previous tile's store has read the pooled stage
-  named_bar(1, 128);
+  named_bar(1, kMkEpiThreads);
 #ifdef CW_KB_TRACE
   s2 = clock64();
 #endif
@@ -568,7 +574,7 @@ __device__ __noinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigin o
   for (int r = 0; r < 3; ++r)
     if (o.oh0 + r >= 0 && o.oh0 + r < d.oh) rmask |= 1u << r;
   const int ow0 = o.ow0, ow = d.ow;
-  for (int it = et; it < npix; it += 128) {
+  for (int it = et; it < npix; it += kMkEpiThreads) {
     const int j = it >> 3, k = it & 7;
     uint4 v[9];
 #pragma unroll
@@ -599,7 +605,7 @@ __device__ __noinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigin o
     *reinterpret_cast<uint4*>(ps + j * 128 + ((k ^ (j & 7)) << 4)) = w;
   }
   fence_proxy_async_smem();
-  named_bar(1, 128);
+  named_bar(1, kMkEpiThreads);
   if (et == 0) {
     tma_store_4d(tmo, ps_addr, 0, pw0, ph, o.img0);
     bulk_commit();
@@ -641,7 +647,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_area + kMkBarBytes - 32);
   uint32_t* gen_slot = tmem_slot + 1;
   float* sbias = reinterpret_cast<float*>(bar_area + kMkBarBytes);
-  float* sred = reinterpret_cast<float*>(obufs + kMkOutBufBytes);  // [128][17] f32 (avg pool)
+  float* sred = reinterpret_cast<float*>(obufs + kMkOutBufBytes);  // 2 x [128][17] f32 (avg pool)
   uint4* sstage = reinterpret_cast<uint4*>(obufs + kMkScratch);    // stem pool / split-K staging
   MkLayer* sl = reinterpret_cast<MkLayer*>(sbias + 2 * 256);
 
@@ -679,7 +685,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(bar_tfull + 8 * a, 1);
-      mbar_init(bar_tempty + 8 * a, 4);
+      mbar_init(bar_tempty + 8 * a, kMkEpiThreads / 32);
     }
     mbar_init(bar_simt, 1);
     for (int b = 0; b < kMkOutBufs; ++b) mbar_init(bar_res + 8 * b, 1);
@@ -696,7 +702,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   const uint8_t* hdr = ab->hdr;
   uint32_t* counters = args.counters;
 
-  if (warp == 0 || warp == 6) {
+  if (warp < kMkEpiWarp0) {
+  setmaxnreg_dec<kMkRegsCtl>();  // warpgroup 0: TMA producer(s) and the MMA issuer
+  if (warp == 0 || (kMkProducers > 1 && warp == 2)) {
     const int pw = warp == 0 ? 0 : 1;  // producer index
     {
       // ======================= TMA producer (whole warp converged; one elected lane issues)
@@ -1006,16 +1014,19 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         }
       }
     }
-  } else if (warp >= 2 && warp <= 5) {
-    // ======================= epilogue + SIMT layers (warps 2..5)
+  }
+  } else {
+    setmaxnreg_inc<kMkRegsEpi>();  // warpgroups 1-2: epilogue
+    // ======================= epilogue + SIMT layers (warps 4..11)
     const int q = warp & 3;  // TMEM lane quarter
+    const int grp = (warp - kMkEpiWarp0) >> 2;  // column half of every 64-column chunk
     const int row = q * 32 + lane;
-    const int et = threadIdx.x - 64;
+    const int et = threadIdx.x - kMkEpiWarp0 * 32;
     uint32_t ocnt = 0;  // TMA-epilogue chunks staged so far (buffer ocnt % kMkOutBufs)
     uint32_t rpar = 0;  // bit b: phase parity of the next residual landing in buffer b
     uint32_t simt_phase = 0;  // completed phases of bar_simt (SIMT-layer bulk copies)
     // per-warp staging: 32 rows x 128 B, 16-byte chunks XOR-swizzled by row
-    uint8_t* stg = reinterpret_cast<uint8_t*>(sstage) + (warp - 2) * 4096;
+    uint8_t* stg = reinterpret_cast<uint8_t*>(sstage) + (warp - kMkEpiWarp0) * 4096;
     auto stg_chunk = [stg](int r, int c) {
       return reinterpret_cast<uint4*>(stg + r * 128 + ((c ^ (r & 7)) << 4));
     };
@@ -1023,7 +1034,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     uint32_t acc_phase = 0;
     for (int L = 0; L < nl; ++L) {
       if (sl[L].kind == MK_CONV) {
-        const MkLayer d = sl[L];
+        const MkLayer& d = sl[L];  // shared-memory plan: fields reload after asm clobbers (cheap LDS)
         int t = first_task(d, cta, G);
         if (t >= d.tasks) continue;
         const float* bias_all = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[d.wlayer];
@@ -1031,14 +1042,14 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           // folded-BN bias of the first task's columns (weights: no dependency); a
           // layer with one N tile uses the same columns for every task: both buffers
           const int n0 = (t / d.splits % d.n_tiles) * d.bn;
-          for (int i = et; i < d.bn; i += 128) {
+          for (int i = et; i < d.bn; i += kMkEpiThreads) {
             const float bv = __ldg(bias_all + n0 + i);
             sbias[acc * 256 + i] = bv;
             if (d.n_tiles == 1) sbias[(acc ^ 1) * 256 + i] = bv;
           }
         }
         if (et == 0) wait_deps(sl, L, counters, gen1, 6);
-        named_bar(1, 128);
+        named_bar(1, kMkEpiThreads);
         bool first = true;
         int done = 0;
         for (; t < d.tasks; t += G, ++done) {
@@ -1054,7 +1065,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
             mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 7);
             tc_fence_after();
             float* part = d.partial + ((size_t)tile * d.splits + z) * 128 * d.bn;
-            for (int c = 0; c < d.bn; c += 32) {
+            for (int c = 32 * grp; c < d.bn; c += 64) {
               uint32_t v[32];
               tmem_ld16(taddr + c, *reinterpret_cast<uint32_t(*)[16]>(v));
               tmem_ld16(taddr + c + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
@@ -1076,16 +1087,16 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
             float* bias = sbias + acc * 256;
             const bool bias_fixed = d.n_tiles == 1;  // staged once for the layer
             if (done > 0 && !bias_fixed)
-              for (int i = et; i < d.bn; i += 128) bias[i] = __ldg(bias_all + o.n0 + i);
+              for (int i = et; i < d.bn; i += kMkEpiThreads) bias[i] = __ldg(bias_all + o.n0 + i);
             if (d.pool_pw) {
               CW_KET(200);
               mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 8);
               CW_KET(201);
               tc_fence_after();
-              named_bar(1, 128);  // bias staged; the previous tile's pooling reads are done
+              named_bar(1, kMkEpiThreads);  // bias staged; the previous tile's pooling reads are done
               epi_stem_pool(sl + L, o, taddr, bias, reinterpret_cast<uint8_t*>(sstage),
                             obufs + kMkPoolStage, obase + kMkPoolStage, args.tmaps + d.tmap_out,
-                            row, et);
+                            row, grp, et);
               CW_KET(202);
             } else if (d.pool_out) {
               // Last conv: + bias (+ residual), ReLU, then a deterministic in-CTA
@@ -1095,8 +1106,12 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                                    : nullptr;
               mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 8);
               tc_fence_after();
-              if (!bias_fixed) named_bar(1, 128);  // bias staged
-              for (int c = 0; c < d.bn; c += 16) {
+              if (!bias_fixed) named_bar(1, kMkEpiThreads);  // bias staged
+              // the two column groups take alternate 16-column steps, each with its own
+              // [128][17] reduction scratch
+              float* sr = sred + grp * (128 * 17);
+              const int etl = et & 127;
+              for (int c = 16 * grp; c < d.bn; c += 32) {
                 uint32_t v[16];
                 tmem_ld16(taddr + c, v);
                 tmem_ld_wait();
@@ -1115,18 +1130,18 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                   if (d.relu) f[i] = fmaxf(f[i], 0.0f);
-                  sred[row * 17 + i] = valid ? f[i] : 0.0f;
+                  sr[row * 17 + i] = valid ? f[i] : 0.0f;
                 }
-                named_bar(1, 128);
+                named_bar(1, kMkEpiThreads);
                 const int hw = d.oh * d.ow;
-                if (et < 16 * d.box_n) {
-                  const int img = et >> 4, col = et & 15;
+                if (etl < 16 * d.box_n) {
+                  const int img = etl >> 4, col = etl & 15;
                   float s = 0.0f;
-                  for (int r = img * hw; r < (img + 1) * hw; ++r) s += sred[r * 17 + col];
+                  for (int r = img * hw; r < (img + 1) * hw; ++r) s += sr[r * 17 + col];
                   if (o.img0 + img < d.nimg)
                     d.pool_out[(size_t)(o.img0 + img) * d.n_out + o.n0 + c + col] = s * d.pool_scale;
                 }
-                named_bar(1, 128);
+                named_bar(1, kMkEpiThreads);
               }
             } else {
               // TMA epilogue, 64-column chunks through the staging buffers (running chunk
@@ -1138,7 +1153,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
               const CUtensorMap* tmo = args.tmaps + d.tmap_out;
               const CUtensorMap* tmr = d.res ? args.tmaps + d.tmap_res : nullptr;
               const int nch = d.bn >> 6;
-              const bool m2d = d.mode == 0;
+              const bool m2d = d.mode == 0, relu = d.relu != 0;
               auto issue_res = [&](uint32_t b, int c) {
                 const uint32_t dst = obase + b * kMkOutBufBytes, bar = bar_res + 8 * b;
                 mbar_arrive_expect_tx(bar, a_rows(d) * 128u);  // the box: tile rows x 64 cols
@@ -1158,7 +1173,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
               if (first && et == 0 && args.trace)
                 args.trace[((size_t)L * G + cta) * 4 + 2] = globaltimer();
               first = false;
-              if (!bias_fixed) named_bar(1, 128);  // bias staged
+              if (!bias_fixed) named_bar(1, kMkEpiThreads);  // bias staged
               for (int c = 0; c < nch; ++c, ++ocnt) {
                 const uint32_t b = ocnt % kMkOutBufs;
                 uint8_t* buf = obufs + b * kMkOutBufBytes;
@@ -1170,45 +1185,57 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                   rpar ^= 1u << b;
                 }
                 CW_KET(10 + c);
-                // two 32-column halves keep the accumulator registers at 32
+                // this thread's row: its group's 32 columns of the chunk (groups 4 grp .. +3)
+                uint32_t v[32];
+                tmem_ld16(taddr + 64 * c + 32 * grp, *reinterpret_cast<uint32_t(*)[16]>(v));
+                tmem_ld16(taddr + 64 * c + 32 * grp + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+                uint4 rv[4];
+                if (tmr) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  uint32_t v[32];
-                  tmem_ld16(taddr + 64 * c + 32 * h, *reinterpret_cast<uint32_t(*)[16]>(v));
-                  tmem_ld16(taddr + 64 * c + 32 * h + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
-                  tmem_ld_wait();
+                  for (int kk = 0; kk < 4; ++kk) rv[kk] = *chunk(4 * grp + kk);
+                }
+                tmem_ld_wait();
+                CW_KET(40 + c);
+                // all groups into registers first: a shared store between them would order every
+                // later bias load behind it (possible aliasing) and serialise them
+                uint4 wv[4];
 #pragma unroll
-                  for (int kk = 0; kk < 4; ++kk) {
-                    const int k = 4 * h + kk;
-                    const float4 b0 = *reinterpret_cast<const float4*>(bias + 64 * c + 8 * k);
-                    const float4 b1 = *reinterpret_cast<const float4*>(bias + 64 * c + 8 * k + 4);
-                    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-                    float f[8];
+                for (int kk = 0; kk < 4; ++kk) {
+                  const int k = 4 * grp + kk;
+                  const float4 b0 = *reinterpret_cast<const float4*>(bias + 64 * c + 8 * k);
+                  const float4 b1 = *reinterpret_cast<const float4*>(bias + 64 * c + 8 * k + 4);
+                  const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                  float f[8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[8 * kk + e]) + bb[e];
-                    if (tmr) {
-                      float rf[8];
-                      bf16x8_to_f32(*chunk(k), rf);
+                  for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[8 * kk + e]);
 #pragma unroll
-                      for (int e = 0; e < 8; ++e) f[e] += rf[e];
-                    }
-                    if (d.relu) {
+                  for (int e = 0; e < 8; e += 2) fadd2(f[e], f[e + 1], bb[e], bb[e + 1]);
+                  if (tmr) {
+                    float rf[8];
+                    bf16x8_to_f32(rv[kk], rf);
 #pragma unroll
-                      for (int e = 0; e < 8; ++e) f[e] = fmaxf(f[e], 0.0f);
-                    }
-                    uint4 w;
-                    w.x = pack_bf16x2(f[0], f[1]);
-                    w.y = pack_bf16x2(f[2], f[3]);
-                    w.z = pack_bf16x2(f[4], f[5]);
-                    w.w = pack_bf16x2(f[6], f[7]);
-                    *chunk(k) = w;
+                    for (int e = 0; e < 8; e += 2) fadd2(f[e], f[e + 1], rf[e], rf[e + 1]);
+                  }
+                  if (relu) {
+                    wv[kk].x = pack_bf16x2_relu(f[0], f[1]);
+                    wv[kk].y = pack_bf16x2_relu(f[2], f[3]);
+                    wv[kk].z = pack_bf16x2_relu(f[4], f[5]);
+                    wv[kk].w = pack_bf16x2_relu(f[6], f[7]);
+                  } else {
+                    wv[kk].x = pack_bf16x2(f[0], f[1]);
+                    wv[kk].y = pack_bf16x2(f[2], f[3]);
+                    wv[kk].z = pack_bf16x2(f[4], f[5]);
+                    wv[kk].w = pack_bf16x2(f[6], f[7]);
                   }
                 }
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) *chunk(4 * grp + kk) = wv[kk];
+                CW_KET(50 + c);
                 fence_proxy_async_smem();
                 // before the barrier: the store that last used the NEXT chunk's buffer has read it
                 CW_KET(20 + c);
                 if (et == 0) bulk_wait_read<kMkOutBufs - 2>();
-                named_bar(1, 128);
+                named_bar(1, kMkEpiThreads);
                 CW_KET(30 + c);
                 if (et == 0) {
                   const uint32_t src = obase + b * kMkOutBufBytes;
@@ -1237,7 +1264,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         CW_KET(91);
-        named_bar(1, 128);
+        named_bar(1, kMkEpiThreads);
         if (et == 0) red_release_add(counters + L, (uint32_t)done);
         CW_KET(92);
       } else {
@@ -1245,7 +1272,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         const MkLayer& d = sl[L];
         if (d.kind == MK_REDUCE && first_task(d, cta, G) >= d.tasks) continue;
         if (et == 0) wait_deps(sl, L, counters, gen1, 9);
-        named_bar(1, 128);
+        named_bar(1, kMkEpiThreads);
         if (args.trace && et == 0) args.trace[((size_t)L * G + cta) * 4 + 1] = globaltimer();
         int done = 1;
         switch (d.kind) {
@@ -1268,7 +1295,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           default: break;
         }
         if (args.trace && et == 0) args.trace[((size_t)L * G + cta) * 4 + 2] = globaltimer();
-        named_bar(1, 128);
+        named_bar(1, kMkEpiThreads);
         if (et == 0) red_release_add(counters + L, (uint32_t)done);
       }
       if (args.trace && et == 0) args.trace[((size_t)L * G + cta) * 4] = globaltimer();

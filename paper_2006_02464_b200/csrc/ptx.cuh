@@ -29,6 +29,16 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// Per-warpgroup register budget (all 4 warps of the warpgroup execute it)
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 // One elected lane of a converged warp (keeps warp-uniform operands of the
 // tcgen05 / TMA instructions in uniform registers: no per-use R2UR waterfall).
 __device__ __forceinline__ bool elect_one() {
@@ -204,6 +214,20 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t M, uint32_t N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// packed fp32x2 add (sm_100a FADD2): two accumulator columns per instruction
+__device__ __forceinline__ void fadd2(float& a0, float& a1, float b0, float b1) {
+  uint64_t x = (uint64_t)__float_as_uint(a0) | ((uint64_t)__float_as_uint(a1) << 32);
+  const uint64_t y = (uint64_t)__float_as_uint(b0) | ((uint64_t)__float_as_uint(b1) << 32);
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(y));
+  a0 = __uint_as_float((uint32_t)x);
+  a1 = __uint_as_float((uint32_t)(x >> 32));
+}
+// bf16x2 {lo = a, hi = b} with ReLU fused into the conversion (max(round(x), 0) == round(max(x, 0)))
+__device__ __forceinline__ uint32_t pack_bf16x2_relu(float a, float b) {
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));
+  return d;
+}
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
