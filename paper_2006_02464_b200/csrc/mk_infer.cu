@@ -443,7 +443,12 @@ __device__ __forceinline__ void simt_fc(const MkLayer& d, const ActionBlock* ab,
 }
 
 // Split-K reduction of one task: rows [part*red_rows, +red_rows) of one tile.
-__device__ __forceinline__ void simt_reduce(const MkLayer& d, const uint8_t* hdr, int task, int et) {
+// Split-K reduction of one task: rows [part*red_rows, +red_rows) of one tile. The S partial
+// row blocks (contiguous in [tile][split][128][bn]) arrive by bulk copies into the staging
+// buffers; the sum + bias (+ residual) (+ ReLU) goes out as bf16.
+__device__ __forceinline__ void simt_reduce(const MkLayer& d, const uint8_t* hdr, int task, int et,
+                                            const float* stage, uint32_t stage_addr, uint32_t bar,
+                                            uint32_t& phase) {
   const int R = d.red_parts;
   const int tile = task / R;
   const int r0 = (task - tile * R) * d.red_rows;
@@ -451,42 +456,30 @@ __device__ __forceinline__ void simt_reduce(const MkLayer& d, const uint8_t* hdr
   const float* bias = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[d.wlayer] + o.n0;
   const int c4n = d.bn / 4;
   const int S = d.splits;
-  const float* part = d.partial + (size_t)tile * S * 128 * d.bn;
-  for (int idx = et; idx < d.red_rows * c4n; idx += kMkEpiThreads) {
-    const int rr = r0 + idx / c4n;
-    const int c = (idx % c4n) * 4;
+  const int rr = min(d.red_rows, 128 - r0);
+  const uint32_t blk = (uint32_t)(rr * d.bn * 4);
+  if (et == 0) {
+    fence_proxy_async();  // the partials were written by other CTAs
+    mbar_arrive_expect_tx(bar, blk * (uint32_t)S);
+    const float* part = d.partial + ((size_t)tile * S * 128 + r0) * d.bn;
+    for (int z = 0; z < S; ++z)
+      bulk_g2s(stage_addr + z * blk, part + (size_t)z * 128 * d.bn, blk, bar);
+  }
+  mbar_wait_to<64>(bar, phase & 1, 15);
+  ++phase;
+  for (int idx = et; idx < rr * c4n; idx += kMkEpiThreads) {
+    const int i = idx / c4n;
+    const int c = (idx - i * c4n) * 4;
     long long m;
-    if (!row_pixel(d, o, rr, &m)) continue;
+    if (!row_pixel(d, o, r0 + i, &m)) continue;
     float4 acc = __ldg(reinterpret_cast<const float4*>(bias + c));
-    const float* src = part + (size_t)rr * d.bn + c;
-    const size_t zs = (size_t)128 * d.bn;
-    int z = 0;
-    for (; z + 8 <= S; z += 8) {  // 8 independent L2 loads in flight
-      float4 p[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) p[u] = __ldcg(reinterpret_cast<const float4*>(src + (z + u) * zs));
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        acc.x += p[u].x;
-        acc.y += p[u].y;
-        acc.z += p[u].z;
-        acc.w += p[u].w;
-      }
-    }
-    if (z < S) {
-      float4 p[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (z + u < S) p[u] = __ldcg(reinterpret_cast<const float4*>(src + (z + u) * zs));
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (z + u < S) {
-          acc.x += p[u].x;
-          acc.y += p[u].y;
-          acc.z += p[u].z;
-          acc.w += p[u].w;
-        }
-      }
+    const float* src = stage + i * d.bn + c;
+    for (int z = 0; z < S; ++z) {
+      const float4 p = *reinterpret_cast<const float4*>(src + z * (blk / 4));
+      acc.x += p.x;
+      acc.y += p.y;
+      acc.z += p.z;
+      acc.w += p.w;
     }
     const size_t oidx = (size_t)m * d.n_out + o.n0 + c;
     if (d.res) {
@@ -499,17 +492,17 @@ __device__ __forceinline__ void simt_reduce(const MkLayer& d, const uint8_t* hdr
       acc.z += b.x;
       acc.w += b.y;
     }
-    if (d.relu) {
-      acc.x = fmaxf(acc.x, 0.0f);
-      acc.y = fmaxf(acc.y, 0.0f);
-      acc.z = fmaxf(acc.z, 0.0f);
-      acc.w = fmaxf(acc.w, 0.0f);
-    }
     uint2 ov;
-    ov.x = pack_bf16x2(acc.x, acc.y);
-    ov.y = pack_bf16x2(acc.z, acc.w);
+    if (d.relu) {
+      ov.x = pack_bf16x2_relu(acc.x, acc.y);
+      ov.y = pack_bf16x2_relu(acc.z, acc.w);
+    } else {
+      ov.x = pack_bf16x2(acc.x, acc.y);
+      ov.y = pack_bf16x2(acc.z, acc.w);
+    }
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(d.out) + oidx) = ov;
   }
+  named_bar(1, kMkEpiThreads);  // the stage is read before the next task's copies
 }
 
 // Stem conv with the 3x3/s2/p1 max pool fused: the tile's conv pixels
@@ -1060,27 +1053,31 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           const bool valid = row_pixel(d, o, row, &m);
           const uint32_t taddr = tmem + acc * 256 + ((uint32_t)(q * 32) << 16);
           if (d.splits > 1) {
-            // fp32 partial tile: 32-column chunks through the warp's staging buffer,
-            // stored row-contiguous (8 lanes x 16 B = one 128-byte line per row).
+            // fp32 partial tile: 32-column chunks through the staging buffers (same protocol
+            // as the TMA epilogue), drained by TMA stores into [tile][split][128][bn]
             mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 7);
             tc_fence_after();
-            float* part = d.partial + ((size_t)tile * d.splits + z) * 128 * d.bn;
-            for (int c = 32 * grp; c < d.bn; c += 64) {
-              uint32_t v[32];
-              tmem_ld16(taddr + c, *reinterpret_cast<uint32_t(*)[16]>(v));
-              tmem_ld16(taddr + c + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+            const CUtensorMap* tmp = args.tmaps + d.tmap_out;
+            const int prow = (tile * d.splits + z) * 128;
+            for (int c = 0; c < d.bn; c += 32, ++ocnt) {
+              const uint32_t b = ocnt % kMkOutBufs;
+              uint8_t* buf = obufs + b * kMkOutBufBytes;
+              uint32_t v[16];
+              tmem_ld16(taddr + c + 16 * grp, v);
               tmem_ld_wait();
 #pragma unroll
-              for (int k = 0; k < 8; ++k)
-                *stg_chunk(lane, k) = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-              __syncwarp();
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const int r = i * 4 + (lane >> 3);
-                __stcg(reinterpret_cast<uint4*>(part + (size_t)(q * 32 + r) * d.bn + c) + (lane & 7),
-                       *stg_chunk(r, lane & 7));
+              for (int kk = 0; kk < 4; ++kk) {
+                const int k = 4 * grp + kk;
+                *reinterpret_cast<uint4*>(buf + row * 128 + ((k ^ (row & 7)) << 4)) =
+                    make_uint4(v[4 * kk], v[4 * kk + 1], v[4 * kk + 2], v[4 * kk + 3]);
               }
-              __syncwarp();
+              fence_proxy_async_smem();
+              if (et == 0) bulk_wait_read<kMkOutBufs - 2>();
+              named_bar(1, kMkEpiThreads);
+              if (et == 0) {
+                tma_store_2d(tmp, obase + b * kMkOutBufBytes, c, prow);
+                bulk_commit();
+              }
             }
           } else {
             // folded-BN bias of this tile's columns, staged while the MMAs run
@@ -1289,7 +1286,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
             break;
           case MK_REDUCE: {
             done = 0;
-            for (int t = first_task(d, cta, G); t < d.tasks; t += G, ++done) simt_reduce(d, hdr, t, et);
+            for (int t = first_task(d, cta, G); t < d.tasks; t += G, ++done)
+              simt_reduce(d, hdr, t, et, reinterpret_cast<const float*>(obufs), obase, bar_simt,
+                          simt_phase);
             break;
           }
           default: break;

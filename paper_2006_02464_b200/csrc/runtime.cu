@@ -521,6 +521,13 @@ std::string Runtime::build_plan(Arch& a, int batch) {
           const int rows = d.mode == 0 ? 128 : d.box_w * d.box_h * d.box_n;
           int parts = 1;
           while (parts * 2 <= rows && (size_t)tiles * parts * 2 <= (size_t)G) parts *= 2;
+          // a task's S partial row blocks are bulk-copied into the 64 KB staging buffers
+          while (parts < rows && (size_t)d.splits * ((rows + parts - 1) / parts) * d.bn * 4 >
+                                     (size_t)kMkOutBufs * kMkOutBufBytes)
+            parts *= 2;
+          if ((size_t)d.splits * ((rows + parts - 1) / parts) * d.bn * 4 >
+              (size_t)kMkOutBufs * kMkOutBufBytes)
+            return "split-K reduce rows exceed the staging buffers";
           r.red_rows = (rows + parts - 1) / parts;
           r.red_parts = (rows + r.red_rows - 1) / r.red_rows;
           r.tasks = (int)tiles * r.red_parts;
@@ -625,9 +632,20 @@ std::string Runtime::build_plan(Arch& a, int batch) {
   // ---- device copies
   if (partial_need) {
     CW_TRY(cudaMalloc(&p.d_partial, partial_need));
-    for (auto& d : p.layers)
-      if (d.kind == MK_CONV && d.splits > 1) d.partial = p.d_partial;
-      else if (d.kind == MK_REDUCE) d.partial = p.d_partial;
+    for (auto& d : p.layers) {
+      if (d.kind == MK_CONV && d.splits > 1) {
+        // the split conv TMA-stores fp32 partial chunks: [tiles * S * 128][bn], 32-column boxes
+        d.partial = p.d_partial;
+        CUtensorMap mp;
+        const uint64_t rows = (uint64_t)d.m_tiles * d.n_tiles * d.splits * 128;
+        if (!make_tmap_2d_f32(&mp, p.d_partial, (uint64_t)d.bn, rows, 128))
+          return "tensor map (split-K partials) failed";
+        d.tmap_out = (int)p.tmaps.size();
+        p.tmaps.push_back(mp);
+      } else if (d.kind == MK_REDUCE) {
+        d.partial = p.d_partial;
+      }
+    }
   }
   CW_TRY(cudaMalloc(&p.d_layers, sizeof(MkLayer) * nl));
   CW_TRY(cudaMemcpy(p.d_layers, p.layers.data(), sizeof(MkLayer) * nl, cudaMemcpyHostToDevice));

@@ -18,6 +18,10 @@ bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows,
 bool make_tmap_nhwc(CUtensorMap* out, const void* base, uint64_t n, uint64_t h, uint64_t w,
                     uint64_t c, uint32_t box_w, uint32_t box_h, uint32_t box_n, uint32_t stride);
 
+// [rows][cols] fp32 row-major matrix, box = 32 (cols) x box_rows, 128B swizzle.
+bool make_tmap_2d_f32(CUtensorMap* out, const void* base, uint64_t cols, uint64_t rows,
+                      uint32_t box_rows);
+
 // [rows][k] bf16 row-major matrix, box = 32 (k) x box_rows, 64B swizzle (stem weights).
 bool make_tmap_2d_sw64(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows,
                        uint32_t box_rows);
