@@ -52,11 +52,11 @@ constexpr int kMkPadH = 3;                 // MK_INPUT: zero rows above and belo
 // its A operand (all 7 kernel rows) is ONE 5D TMA box of 7 sub-tiles of kMkStemSub bytes
 constexpr int kMkStemW = 40;
 constexpr uint32_t kMkStemSub = 3u * kMkStemW * 64u;  // 7680 B: 512-B aligned (64-B swizzle atoms)
-// staging-buffer map: input-conversion stage [0, 64 KB), stem-pool / split-K scratch at 32 KB,
-// avg-pool scratch at 16 KB. The resident stem weights (kMkStemBBytes) sit at the END of the
-// ring (written by the producer while the input conversion still runs).
-constexpr uint32_t kMkStemBBytes = 7 * 4096;
-constexpr uint32_t kMkInputStage = 0;
+// staging-buffer map: resident stem weights [0, 28 KB) (written by the producer while the
+// input conversion still runs), input-conversion stage [32 KB, 64 KB), stem-pool / split-K
+// scratch at 32 KB, avg-pool scratch at 16 KB
+constexpr uint32_t kMkStemB = 0;
+constexpr uint32_t kMkInputStage = 32768;
 constexpr uint32_t kMkScratch = 32768;
 constexpr uint32_t kMkPoolStage = 49152;  // stem: pooled pixels of one tile (TMA-store source)
 constexpr uint32_t kMkTmemCols = 512;      // two accumulators of up to 256 columns
@@ -70,7 +70,7 @@ constexpr uint32_t kMkBarBytes = 512;
 #endif
 constexpr int kMkOutBufs = CW_OUT_BUFS;
 constexpr uint32_t kMkOutBufBytes = 16384;
-static_assert(kMkOutBufs >= 4, "the staging-buffer map (input stage, scratch, pool stage) needs 64 KB");
+static_assert(kMkOutBufs >= 4, "the staging-buffer map (kMkStemB, kMkInputStage) needs 64 KB");
 #ifdef CW_KB_TRACE
 constexpr uint32_t kMkSmemCap = 224 * 1024;  // debug builds keep a static trace array
 #else

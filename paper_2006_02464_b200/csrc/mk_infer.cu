@@ -228,35 +228,20 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
 // The CTA's image rows (a contiguous range of (n, h)) come in by bulk copies (plane-major,
 // up to 64 KB per phase into the epilogue staging buffers): generic loads would be capped by
 // the few KB of L1 the megakernel leaves; the conversion then reads shared memory only.
-// fp32 [C=3][H][W] per request -> bf16 [n][H + 2 pad][W + 2 pad][4] (data at row + kMkPadH,
-// column + kMkPadW). The CTA's image rows (a contiguous range of (n, h)) come in by bulk
-// copies (plane-major) and leave by one bulk store per converted row, through the 64 KB
-// staging buffers: generic loads / stores would be capped by the few KB of L1 the
-// megakernel leaves.
 __device__ __forceinline__ void simt_input(const MkLayer& d, const ActionBlock* ab, int cta, int G,
-                                        int et, uint8_t* stage, uint32_t stage_addr, uint32_t bar,
+                                        int et, float* stage, uint32_t stage_addr, uint32_t bar,
                                         uint32_t& phase) {
   const int W = d.W, H = d.H, W4 = W / 4, Wp = W + 2 * kMkPadW;
   const int rows_total = d.batch * H;
   const int R = (rows_total + G - 1) / G;
   const int r0 = cta * R, r1 = min(rows_total, r0 + R);
-  const uint32_t in_row = 3u * W * 4u, out_row = (uint32_t)W * 8u;
-  const int P = (int)(kMkOutBufs * kMkOutBufBytes / (in_row + out_row));  // rows per phase
-  const float* planes = reinterpret_cast<const float*>(stage);
-  uint8_t* ostage = stage + P * in_row;
-  const uint32_t ostage_addr = stage_addr + P * in_row;
+  const int P = (int)((kMkOutBufs * kMkOutBufBytes - kMkInputStage) / (3u * W * 4u));  // rows/phase
   const long long plane = (long long)H * W;
-  uint8_t* out = reinterpret_cast<uint8_t*>(d.out);
-#ifdef CW_KB_TRACE
-  long long tq[12];
-  int nq = 0;
-  tq[nq++] = clock64();
-#endif
+  uint2* out = reinterpret_cast<uint2*>(d.out);
   for (int pr = r0; pr < r1; pr += P) {
     const int pe = min(r1, pr + P), nr = pe - pr;
     if (et == 0) {
-      bulk_wait_read<0>();  // the previous phase's row stores have read the stage
-      mbar_arrive_expect_tx(bar, (uint32_t)nr * in_row);
+      mbar_arrive_expect_tx(bar, (uint32_t)(3 * nr * W * 4));
       for (int a = pr; a < pe;) {
         const int n = a / H, h = a - n * H;
         const int b = min(pe, (n + 1) * H);  // rows of this image in the phase
@@ -268,14 +253,13 @@ __device__ __forceinline__ void simt_input(const MkLayer& d, const ActionBlock* 
     }
     mbar_wait_to<64>(bar, phase & 1, 12);
     ++phase;
-#ifdef CW_KB_TRACE
-    if (nq < 12) tq[nq++] = clock64();
-#endif
     for (int it = et; it < nr * W4; it += kMkEpiThreads) {
       const int i = it / W4, w4 = it - i * W4;
-      const float4 r = *reinterpret_cast<const float4*>(planes + (0 * P + i) * W + w4 * 4);
-      const float4 g = *reinterpret_cast<const float4*>(planes + (1 * P + i) * W + w4 * 4);
-      const float4 b = *reinterpret_cast<const float4*>(planes + (2 * P + i) * W + w4 * 4);
+      const int a = pr + i, n = a / H, h = a - n * H;
+      const float4 r = *reinterpret_cast<const float4*>(stage + (0 * P + i) * W + w4 * 4);
+      const float4 g = *reinterpret_cast<const float4*>(stage + (1 * P + i) * W + w4 * 4);
+      const float4 b = *reinterpret_cast<const float4*>(stage + (2 * P + i) * W + w4 * 4);
+      uint2* o = out + ((long long)n * (H + 2 * kMkPadH) + h + kMkPadH) * Wp + kMkPadW + w4 * 4;
       uint4 p0, p1;
       p0.x = pack_bf16x2(r.x, g.x);
       p0.y = pack_bf16x2(b.x, 0.0f);
@@ -285,34 +269,11 @@ __device__ __forceinline__ void simt_input(const MkLayer& d, const ActionBlock* 
       p1.y = pack_bf16x2(b.z, 0.0f);
       p1.z = pack_bf16x2(r.w, g.w);
       p1.w = pack_bf16x2(b.w, 0.0f);
-      uint4* o = reinterpret_cast<uint4*>(ostage + i * out_row + w4 * 32);
-      o[0] = p0;
-      o[1] = p1;
+      reinterpret_cast<uint4*>(o)[0] = p0;
+      reinterpret_cast<uint4*>(o)[1] = p1;
     }
-    fence_proxy_async_smem();
-    named_bar(1, kMkEpiThreads);
-    if (et == 0) {
-      for (int i = 0; i < nr; ++i) {
-        const int a = pr + i, n = a / H, h = a - n * H;
-        bulk_s2g(out + (((long long)n * (H + 2 * kMkPadH) + h + kMkPadH) * Wp + kMkPadW) * 8,
-                 ostage_addr + i * out_row, out_row);
-      }
-      bulk_commit();
-    }
-#ifdef CW_KB_TRACE
-    if (nq < 12) tq[nq++] = clock64();
-#endif
+    named_bar(1, kMkEpiThreads);  // the stage is read before the next phase overwrites it
   }
-  if (et == 0) {  // the rows are in memory before the layer is published
-    bulk_wait_all();
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-  }
-#ifdef CW_KB_TRACE
-  if (et == 0 && (cta == 0 || cta == 77)) {
-    tq[nq++] = clock64();
-    for (int i = 1; i < nq; ++i) printf("input cta %d step %d: %lld\n", cta, i, tq[i] - tq[i - 1]);
-  }
-#endif
 }
 
 __device__ __forceinline__ void simt_maxpool(const MkLayer& d, int cta, int G, int et) {
@@ -778,7 +739,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           if (elect_one()) {
             mbar_arrive_expect_tx(bar_stemb, 7u * 64u * 64u);
             for (int r = 0; r < 7; ++r)
-              tma_load_2d(sbase + ring_bytes - kMkStemBBytes + r * 4096u, tb, bar_stemb, r * 32, 0);
+              tma_load_2d(obase + kMkStemB + r * 4096u, tb, bar_stemb, r * 32, 0);
           }
           __syncwarp();
           wait_deps(sl, L, counters, gen1, 2);
@@ -959,7 +920,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         if (d.mode == 2) {
           // stem: 7 kernel rows x 2 K=16 steps per task, A sub-tiles kMkStemSub apart in the
           // slot, B resident (4 KB per kernel row)
-          const uint64_t bst = sw64_kmajor_desc(sbase + ring_bytes - kMkStemBBytes);
+          const uint64_t bst = sw64_kmajor_desc(obase + kMkStemB);
           mbar_wait_to<CW_HINT_FULL>(bar_stemb, 0, 5);
           for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
             mbar_wait_to<CW_HINT_TEMPTY>(bar_tempty + 8 * acc, acc_phase ^ 1, 4);
@@ -1313,8 +1274,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         int done = 1;
         switch (d.kind) {
           case MK_INPUT:
-            simt_input(d, ab, cta, G, et, obufs + kMkInputStage, obase + kMkInputStage, bar_simt,
-                       simt_phase);
+            simt_input(d, ab, cta, G, et, reinterpret_cast<float*>(obufs + kMkInputStage),
+                       obase + kMkInputStage, bar_simt, simt_phase);
             break;
           case MK_MAXPOOL: simt_maxpool(d, cta, G, et); break;
           case MK_AVGPOOL: simt_avgpool(d, cta, G, et); break;

@@ -602,7 +602,7 @@ std::string Runtime::build_plan(Arch& a, int batch) {
       d.sub_bytes = (int)kMkStemSub;
       d.b_off = 0;
       d.slot_bytes = (int)((7 * kMkStemSub + 1023) / 1024 * 1024);
-      d.slots = std::min<int>(kMkMaxSlots, (p.ring_bytes - kMkStemBBytes) / d.slot_bytes);
+      d.slots = std::min<int>(kMkMaxSlots, p.ring_bytes / d.slot_bytes);
       d.slots -= d.slots % kMkProducers;
       if (d.slots < 2) return "ring too small for the stem";
       continue;
