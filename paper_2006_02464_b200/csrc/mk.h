@@ -101,7 +101,12 @@ struct MkLayer {
   const void* in;         // SIMT input
 };
 
-static_assert(sizeof(MkLayer) % 16 == 0, "MkLayer is copied to smem in 16-byte units");
+static_assert(sizeof(MkLayer) % 16 == 0, "MkLayer is copied in 16-byte units");
+// The plan's layer table lives in a __constant__ bank (mk_infer.cu), refreshed by a
+// device-to-device memcpy node at the head of every INFER graph: uniform (ULDC) operand
+// reads for the producer / MMA loops and no shared memory, whatever the depth of the net.
+constexpr int kMkMaxPlanLayers = 250;
+static_assert(kMkMaxPlanLayers * sizeof(MkLayer) <= 64000, "constant bank (64 KB)");
 
 struct MkArgs {
   const MkLayer* layers;

@@ -38,6 +38,8 @@
 
 namespace cw {
 
+__constant__ MkLayer c_plan[kMkMaxPlanLayers];  // the running INFER's plan (see mk.h)
+
 constexpr uint64_t kMkTimeoutNs = 2000000000ull;  // 2 s: far above any INFER
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
@@ -642,7 +644,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   float* sbias = reinterpret_cast<float*>(bar_area + kMkBarBytes);
   float* sred = reinterpret_cast<float*>(obufs + kMkOutBufBytes);  // 2 x [128][17] f32 (avg pool)
   uint4* sstage = reinterpret_cast<uint4*>(obufs + kMkScratch);    // stem pool / split-K staging
-  MkLayer* sl = reinterpret_cast<MkLayer*>(sbias + 2 * 256);
+  const MkLayer* sl = c_plan;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -664,13 +666,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   const int G = gridDim.x;
   const int nl = args.n_layers;
 
-  // ---- prologue: stage the plan in smem, barriers, TMEM
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(args.layers);
-    uint4* dst = reinterpret_cast<uint4*>(sl);
-    const int n16 = nl * (int)sizeof(MkLayer) / 16;
-    for (int i = threadIdx.x; i < n16; i += kMkThreads) dst[i] = __ldg(src + i);
-  }
+  // ---- prologue: barriers, TMEM
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMkMaxSlots; ++s) {
       mbar_init(bar_full + 8 * s, 1);
@@ -1027,7 +1023,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     uint32_t acc_phase = 0;
     for (int L = 0; L < nl; ++L) {
       if (sl[L].kind == MK_CONV) {
-        const MkLayer& d = sl[L];  // shared-memory plan: fields reload after asm clobbers (cheap LDS)
+        const MkLayer& d = sl[L];  // constant-bank plan
         int t = first_task(d, cta, G);
         if (t >= d.tasks) continue;
         const float* bias_all = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[d.wlayer];
@@ -1344,8 +1340,8 @@ cudaError_t configure_mk() {
 }
 
 uint32_t mk_smem_bytes(uint32_t ring_bytes, int n_layers) {
-  return 1024 + ring_bytes + kMkOutBufs * kMkOutBufBytes + kMkBarBytes + 2 * 256 * 4 +
-         n_layers * (uint32_t)sizeof(MkLayer);
+  (void)n_layers;  // the plan is in the constant bank
+  return 1024 + ring_bytes + kMkOutBufs * kMkOutBufBytes + kMkBarBytes + 2 * 256 * 4;
 }
 
 int mk_blocks_per_sm(uint32_t smem) {
@@ -1354,6 +1350,14 @@ int mk_blocks_per_sm(uint32_t smem) {
       cudaSuccess)
     return 0;
   return n;
+}
+
+cudaError_t copy_plan(const MkLayer* d_layers, int n, cudaStream_t st) {
+  if (n > kMkMaxPlanLayers) return cudaErrorInvalidValue;
+  void* dst = nullptr;
+  cudaError_t e = cudaGetSymbolAddress(&dst, c_plan);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyAsync(dst, d_layers, sizeof(MkLayer) * n, cudaMemcpyDeviceToDevice, st);
 }
 
 cudaError_t launch_mk(const MkArgs& a, int grid, uint32_t smem, cudaStream_t st) {

@@ -350,7 +350,7 @@ struct DepTracker {
 constexpr int kBufPartial = 1000;  // pseudo-buffer: the split-K partial workspace
 }  // namespace
 
-std::string Runtime::build_plan(Arch& a, int batch) {
+std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
   Plan& p = a.plans[batch];
   p.batch = batch;
   p.layers.clear();
@@ -365,7 +365,7 @@ std::string Runtime::build_plan(Arch& a, int batch) {
   auto push = [&](MkLayer& d, int oi, const std::vector<int>& rd,
                   const std::vector<int>& wr) -> std::string {
     const int L = (int)p.layers.size();
-    if (L >= kMaxLayers) return "plan has too many layers";
+    if (L >= kMkMaxPlanLayers) return "plan has too many layers";
     std::string err = deps.add(d, L, rd, wr);
     if (!err.empty()) return err;
     d.rot = rot;
@@ -466,7 +466,7 @@ std::string Runtime::build_plan(Arch& a, int batch) {
             return "tensor map (nhwc) failed";
         }
         // (the fused pool runs in the epilogue of whole-image tiles: no split-K there)
-        plan_conv(d, op.cout, G, !fuse_pool && !d.pool_pw);
+        plan_conv(d, op.cout, G, allow_split && !fuse_pool && !d.pool_pw);
         d.tmap = (int)p.tmaps.size();
         p.tmaps.push_back(tm);
         d.tmap_out = d.tmap_res = -1;
@@ -675,11 +675,13 @@ std::string Runtime::capture(Arch& a, Plan& p) {
   args.trace = p.d_trace;
   if (const char* e = getenv("CW_MK_FLAGS")) args.flags = (uint32_t)atoi(e);  // experiments only
   CW_TRY(cudaStreamBeginCapture(s_cap_, cudaStreamCaptureModeThreadLocal));
+  cudaError_t ce = copy_plan(p.d_layers, (int)p.layers.size(), s_cap_);
   launch_gate(ab_, ring_, kRing - 1, ctr_, exec_recs_, s_cap_);
   cudaError_t le = launch_mk(args, p.grid, p.smem, s_cap_);
   launch_mk_done(ab_, kRing - 1, exec_recs_, p.d_gen, s_cap_);
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(s_cap_, &g);
+  CW_TRY(ce);
   CW_TRY(le);
   CW_TRY(e);
   p.graph = g;
@@ -706,6 +708,8 @@ std::string Runtime::build_plans() {
     }
     for (auto& [b, p] : a.plans) {
       std::string err = build_plan(a, b);
+      // a deep net whose split-K reduce layers overflow the plan table: no split-K
+      if (err == "plan has too many layers") err = build_plan(a, b, false);
       if (!err.empty()) return err;
       err = capture(a, p);
       if (!err.empty()) return err;

@@ -174,7 +174,7 @@ class Runtime {
   std::string set_input_pool(const float* data, int n, int64_t bytes);
 
  private:
-  std::string build_plan(Arch& a, int batch);
+  std::string build_plan(Arch& a, int batch, bool allow_split = true);
   std::string capture(Arch& a, Plan& p);
   int num_sms_ = 148;
   std::vector<uint64_t> last_trace_;

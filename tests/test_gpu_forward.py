@@ -36,3 +36,23 @@ def test_resnet50_logits_match_oracle(gpu, r50, batch):
     c = resnet_oracle.compare(got, ref)
     assert c["ok"], c
     assert ns > 0
+
+
+@pytest.mark.parametrize("name", ["resnet18", "resnet34", "resnet101", "resnet152"])
+@pytest.mark.parametrize("batch", [1, 8])
+def test_resnet_family_logits_match_oracle(gpu, name, batch):
+    """The other torchvision ResNets of the zoo (basic blocks with 3x3 residual convs, deep
+    bottleneck stacks whose plans hold 100+ layers) through the same megakernel."""
+    spec = arch.build_arch(name)
+    params = arch.make_params(spec, seed=1)
+    blob = arch.pack_blob(spec, arch.fold(spec, params))
+    x = arch.make_inputs(batch, spec, first=7 * batch)
+    with DeviceRuntime(device=gpu, pages_total=blob.pages + 2, io_slots=16) as rt:
+        rt.register_arch(0, spec, batches=(batch,))
+        rt.register_blob(0, 0, blob)
+        rt.build()
+        rt.load(0, list(range(blob.pages + 1, 0, -1))[:blob.pages])
+        got, _ = rt.infer(0, blob.pages + 1, x)
+    ref = resnet_oracle.logits(resnet_oracle.torchvision_model(name, params), x)
+    c = resnet_oracle.compare(got, ref)
+    assert c["ok"], c
