@@ -758,6 +758,76 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           }
           continue;
         }
+        if (d.mode == 3) {
+          // 3x3 / stride 1: a slot = (kernel row r, channel block): ONE A box (columns -1 ..
+          // box_w - 2 of the input rows, OOB zero fill = padding) + the B tiles of taps q = 0..2
+          const uint32_t a3 = a_rows(d) * 128u, b3 = (uint32_t)d.bn * 128u;
+          const uint32_t tx3 = a3 + 3u * b3;
+          const uint32_t b_off = (uint32_t)d.b_off, b_box = 64u * 128u;
+          const int nbox = wide ? 1 : d.bn / 64;
+          int slot = 0;
+          bool waited = false;
+          for (; t < d.tasks; t += G) {
+            const int tile = t / d.splits;
+            const int z = t - tile * d.splits;
+            const TileOrigin o = tile_origin(d, tile);
+            const int g0 = z * d.kb_per_split / 3;
+            const int g1 = min(d.num_kb, (z + 1) * d.kb_per_split) / 3;
+            const int ng = g1 - g0;
+            auto load_b = [&](int g, int s) {
+              const int r = g / d.cin_kb, cb = g - r * d.cin_kb;
+              if (elect_one())
+                for (int q = 0; q < 3; ++q)
+                  for (int j = 0; j < nbox; ++j)
+                    tma_load_2d(sbase + s * sb + b_off + q * b3 + j * b_box, tb, bar_full + 8 * s,
+                                ((r * 3 + q) * d.cin_kb + cb) * 64, o.n0 + 64 * j);
+              __syncwarp();
+            };
+            auto load_a = [&](int g, int s) {
+              const int r = g / d.cin_kb, cb = g - r * d.cin_kb;
+              if (elect_one())
+                tma_load_4d(sbase + s * sb, ta, bar_full + 8 * s, cb * 64, o.ow0 - 1, o.oh0 + r - 1,
+                            o.img0);
+              __syncwarp();
+            };
+            auto acquire = [&](int s) {
+              mbar_wait_to<CW_HINT_EMPTY>(bar_empty + 8 * s, ((par >> s) & 1) ^ 1, 3);
+              par ^= 1u << s;
+              if (elect_one()) mbar_arrive_expect_tx(bar_full + 8 * s, tx3);
+              __syncwarp();
+            };
+            int c = 0;
+            if (!waited) {  // weights first (no dependency), then the inputs
+              const int pre = ng < ns ? ng : ns;
+              int s = slot;
+              for (int k = 0; k < pre; ++k) {
+                if (s % kMkProducers == pw) {
+                  acquire(s);
+                  load_b(g0 + k, s);
+                }
+                if (++s == ns) s = 0;
+              }
+              wait_deps(sl, L, counters, gen1, 2);
+              fence_proxy_async();
+              waited = true;
+              if (args.trace && lane == 0 && pw == 0)
+                args.trace[((size_t)L * G + cta) * 4 + 1] = globaltimer();
+              for (; c < pre; ++c) {
+                if (slot % kMkProducers == pw) load_a(g0 + c, slot);
+                if (++slot == ns) slot = 0;
+              }
+            }
+            for (; c < ng; ++c) {
+              if (slot % kMkProducers == pw) {
+                acquire(slot);
+                load_b(g0 + c, slot);
+                load_a(g0 + c, slot);
+              }
+              if (++slot == ns) slot = 0;
+            }
+          }
+          continue;
+        }
         const uint32_t a_bytes = a_rows(d) * (uint32_t)d.kblk * 2u;
 #ifdef CW_MK_EXPERIMENTS
         const bool no_a = args.flags & 2, no_b = args.flags & 4;
@@ -941,6 +1011,46 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
             }
             __syncwarp();
             if (++slot == ns) slot = 0;
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          }
+          continue;
+        }
+        if (d.mode == 3) {
+          // per slot: taps q = 0..2 of one (kernel row, channel block): the A operand is the
+          // shared box read from row q (start + q x 128 B: the 128-byte swizzle follows the
+          // absolute address bits, so an unaligned start needs no base-offset field)
+          const uint32_t b3 = (uint32_t)d.bn * 128u;
+          for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
+            const int z = t % d.splits;
+            const int ng = min(d.num_kb, (z + 1) * d.kb_per_split) / 3 - z * d.kb_per_split / 3;
+            mbar_wait_to<CW_HINT_TEMPTY>(bar_tempty + 8 * acc, acc_phase ^ 1, 4);
+            tc_fence_after();
+            const uint32_t dtm = tmem + acc * 256;
+            for (int i = 0; i < ng; ++i) {
+              mbar_wait_to<CW_HINT_FULL>(bar_full + 8 * slot, (par >> slot) & 1, 5);
+              par ^= 1u << slot;
+              if (first) {
+                if (lane == 0 && args.trace) args.trace[((size_t)L * G + cta) * 4 + 3] = globaltimer();
+                first = false;
+              }
+              tc_fence_after();
+              const uint32_t sa = sbase + slot * sb;
+              if (elect_one()) {
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                  const uint64_t ad = sw128_kmajor_desc(sa + q * 128u);  // swizzle from address bits
+                  const uint64_t bd = sw128_kmajor_desc(sa + d.b_off + q * b3);
+                  mma_bf16(dtm, ad, bd, idesc, (i | q) != 0);
+#pragma unroll
+                  for (int k = 1; k < 4; ++k) mma_bf16(dtm, ad + 2 * k, bd + 2 * k, idesc, 1);
+                }
+                mma_commit(bar_empty + 8 * slot);
+              }
+              __syncwarp();
+              if (++slot == ns) slot = 0;
+            }
+            if (elect_one()) mma_commit(bar_tfull + 8 * acc);
+            __syncwarp();
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           }
           continue;

@@ -272,7 +272,8 @@ static void plan_conv(MkLayer& d, int cout, int G, bool allow_split) {
     const double t_kb = std::max({0.30, 0.08 * n_tma + 0.1, (a_bytes + bn * d.kblk * 2.0) / 140e3});
     for (int s = 1; s <= 32; ++s) {
       if (s > 1 && (!allow_split || d.num_kb / s < 2)) break;
-      const int per = (d.num_kb + s - 1) / s;
+      int per = (d.num_kb + s - 1) / s;
+      if (d.mode == 3) per = (per + 2) / 3 * 3;  // whole (kernel row, channel block) groups
       const int splits = (d.num_kb + per - 1) / per;
       if (splits != s) continue;
       const int tasks = tiles * s;
@@ -301,6 +302,7 @@ static void plan_conv(MkLayer& d, int cout, int G, bool allow_split) {
   d.n_tiles = cout / best_bn;
   d.splits = best_s;
   d.kb_per_split = (d.num_kb + best_s - 1) / best_s;
+  if (d.mode == 3) d.kb_per_split = (d.kb_per_split + 2) / 3 * 3;
   d.tasks = d.m_tiles * d.n_tiles * best_s;
 }
 
@@ -445,6 +447,21 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
           d.m_tiles = (d.m_total + 127) / 128;
           if (!make_tmap_2d(&tm, in, (uint64_t)op.kpad, (uint64_t)d.m_total, 128))
             return "tensor map (2d) failed";
+        } else if (!fuse_pool && op.kh == 3 && op.kw == 3 && op.stride == 1 && op.pad == 1 &&
+                   op.cin % 64 == 0 && op.out_w + 2 <= 128 && getenv("CW_NO_MODE3") == nullptr) {
+          // 3x3 / stride 1: tiles of full rows widened by the 2 padding columns, so the three
+          // horizontal taps of a kernel row are ONE TMA box read at row shifts 0, 1, 2 (the
+          // two extra columns per row are junk outputs, clipped by the store map)
+          d.mode = 3;
+          d.kblk = 64;
+          d.num_kb = op.kpad / 64;
+          d.cin_kb = op.cin / 64;
+          box_dims(batch, op.out_h, op.out_w + 2, &d.box_w, &d.box_h, &d.box_n);
+          d.tiles_w = 1;
+          d.tiles_h = (op.out_h + d.box_h - 1) / d.box_h;
+          d.m_tiles = d.tiles_h * ((batch + d.box_n - 1) / d.box_n);
+          if (!make_tmap_nhwc(&tm, in, batch, op.in_h, op.in_w, op.cin, d.box_w, d.box_h, d.box_n, 1))
+            return "tensor map (nhwc, mode 3) failed";
         } else {
           if (op.cin % 64) return "conv Cin must be a multiple of 64";
           d.mode = 1;
@@ -605,6 +622,17 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
       d.slots = std::min<int>(kMkMaxSlots, p.ring_bytes / d.slot_bytes);
       d.slots -= d.slots % kMkProducers;
       if (d.slots < 2) return "ring too small for the stem";
+      continue;
+    }
+    if (d.mode == 3) {  // one slot = the shared A box (+2 rows read by the shifts) + 3 B tiles
+      const uint32_t rows = (uint32_t)(d.box_w * d.box_h * d.box_n);
+      d.kpack = 3;
+      d.b_off = (int)((std::max(rows, 128u) * 128u + 256u + 1023u) / 1024u * 1024u);
+      d.sub_bytes = d.bn * 128;
+      d.slot_bytes = (int)((d.b_off + 3u * d.bn * 128u + 1023u) / 1024u * 1024u);
+      d.slots = std::min<int>(kMkMaxSlots, p.ring_bytes / d.slot_bytes);
+      d.slots -= d.slots % kMkProducers;
+      if (d.slots < 2) return "ring too small for a mode-3 conv tile";
       continue;
     }
     const uint32_t rows = d.mode == 0 ? 128u : (uint32_t)(d.box_w * d.box_h * d.box_n);
