@@ -203,6 +203,20 @@ replicas resnet50 {copies - 1}
 
 # ----------------------------------------------------------------------------- our arm
 
+def ncu_traffic(b: int):
+    """DRAM bytes (read + write) per launch of the INFER megakernel at batch b, from the
+    committed `ncu --set full` capture summary (tools/ncu_capture.sh + tools/ncu_summary.py)."""
+    path = os.path.join(REPO, "profiles", "r1_ncu_full_mk_infer_summary.json")
+    try:
+        s = json.load(open(path))[f"b{b}"]
+        mb = sum(float(s[k].split()[0]) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        unit = s["dram__bytes_read.sum"].split()[1]
+        scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1.0)
+        return mb * scale, f"profiles/{os.path.basename(path)} (b={b})"
+    except (OSError, KeyError, ValueError, IndexError):
+        return None, None
+
+
 def run_ours(args, d: Dist) -> dict | None:
     from paper_2006_02464_b200 import arch
     from paper_2006_02464_b200.device import DeviceRuntime
@@ -274,9 +288,10 @@ def run_ours(args, d: Dist) -> dict | None:
             if k == 1:
                 conv_t += max(0.0, t - prev)
             prev = max(prev, t)
+        traffic, traffic_src = ncu_traffic(b)
         out["roofline"] = {
             "bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
-            "frac": achieved / bf16_peak, "traffic": None,
+            "frac": achieved / bf16_peak, "traffic": traffic, "traffic_source": traffic_src,
             "kernel": "mk_infer_kernel (persistent tcgen05/TMA megakernel, whole forward)",
             "flops_per_launch": flops,
             "launches_per_infer": int(launches),

@@ -139,6 +139,14 @@ std::string Runtime::calibrate_clock() {
     if (t1 - t0 < 2000) est.push_back((int64_t)g - (t0 + t1) / 2 + 300);
   }
   CW_TRY(cudaStreamSynchronize(s_cap_));
+  if (est.empty()) {
+    // The publisher did not run concurrently with this thread (e.g. kernels serialised under
+    // a profiler): a coarse offset from one stamp (error ~ the synchronise latency).
+    vs[2] = 0;
+    launch_stamp(vs + 2, 1, s_cap_);
+    CW_TRY(cudaStreamSynchronize(s_cap_));
+    if (vs[2] != 0) est.push_back((int64_t)vs[2] - realtime_ns());
+  }
   cudaFreeHost(slot);
   if (est.empty()) return "clock calibration failed";
   std::nth_element(est.begin(), est.begin() + est.size() / 2, est.end());

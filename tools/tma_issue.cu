@@ -13,7 +13,8 @@
 
 using namespace cw;
 
-__global__ void __launch_bounds__(64, 1) probe(const __grid_constant__ CUtensorMap tm, int n, int variant,
+__global__ void __launch_bounds__(64, 1) probe(const __grid_constant__ CUtensorMap tm,
+                                               const __grid_constant__ CUtensorMap tm4, int n, int variant,
                                                const int* coords, long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* base = sm + ((1024 - (smem_u32(sm) & 1023)) & 1023);
@@ -53,11 +54,21 @@ __global__ void __launch_bounds__(64, 1) probe(const __grid_constant__ CUtensorM
           tma_load_2d(dst + 16384, &tm, fb, ((c_base + 2 * i) & 7) * 64, 128);
         }
         __syncwarp();
-      } else {
+      } else if (variant == 2) {
         if (elect_one()) {
           mbar_arrive_expect_tx(fb, 32768);
           tma_load_2d(dst, &tm, fb, (i & 7) * 64, 0);
           tma_load_2d(dst + 16384, &tm, fb, (i & 7) * 64, 128);
+        }
+        __syncwarp();
+      } else {
+        // 4D NHWC boxes (64 ch x 14 w x 9 h x 1 n = 126 rows, 16128 B), 3x3 tap shifts
+        const int tap = i % 9, q = tap % 3 - 1, r = tap / 3 - 1;
+        const int img = (i / 9) & 15, h0 = ((i / 144) & 1) * 9 - 1;
+        if (elect_one()) {
+          mbar_arrive_expect_tx(fb, 2 * 16128);
+          tma_load_4d(dst, &tm4, fb, 0, q, h0 + r + 1, img);
+          tma_load_4d(dst + 16384, &tm4, fb, 64 * (variant - 3), q, h0 + r + 1, (img + 1) & 15);
         }
         __syncwarp();
       }
@@ -96,6 +107,15 @@ int main() {
   cuuint32_t es[2] = {1, 1};
   enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUtensorMap tm4;
+  {
+    cuuint64_t d4[4] = {256, 14, 14, 16};
+    cuuint64_t s4[3] = {256 * 2, 14 * 256 * 2, 14 * 14 * 256 * 2};
+    cuuint32_t b4[4] = {64, 14, 9, 1};
+    cuuint32_t e4[4] = {1, 1, 1, 1};
+    enc(&tm4, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, buf, d4, s4, b4, e4, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   int* coords;
   cudaMalloc(&coords, 64);
   cudaMemset(coords, 0, 64);
@@ -103,10 +123,10 @@ int main() {
   cudaMalloc(&d, 8);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
   for (int grid : {1, 148})
-    for (int v : {0, 1, 2}) {
+    for (int v : {0, 1, 2, 3, 4}) {
       const int n = 2048;
-      probe<<<grid, 64, 140 * 1024>>>(tm, 16, v, coords, d);
-      probe<<<grid, 64, 140 * 1024>>>(tm, n, v, coords, d);
+      probe<<<grid, 64, 140 * 1024>>>(tm, tm4, 16, v, coords, d);
+      probe<<<grid, 64, 140 * 1024>>>(tm, tm4, n, v, coords, d);
       long long c = 0;
       if (cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
         printf("error\n");
