@@ -266,6 +266,9 @@ static void box_dims(int nimg, int oh, int ow, int* bw, int* bh, int* bn) {
 //   * a split-K reduce layer costs ~3 us plus its partial-tile traffic.
 // Epilogue of task i overlaps the MMAs of task i+1 (two TMEM accumulators).
 static void plan_conv(MkLayer& d, int cout, int G, bool allow_split) {
+  // a split layer adds a reduce layer and one more whole-GPU dependency (~6 us in the
+  // network, measured with tools/sweep_bn.sh + op_profile; CW_SPLIT_US overrides)
+  static const double split_us = getenv("CW_SPLIT_US") ? atof(getenv("CW_SPLIT_US")) : 6.0;
   static const int kBn[3] = {256, 128, 64};
   const double rows = d.mode == 0 ? 128.0 : (double)(d.box_w * d.box_h * d.box_n);
   const double a_bytes = rows * d.kblk * 2;
@@ -289,7 +292,7 @@ static void plan_conv(MkLayer& d, int cout, int G, bool allow_split) {
       const double t_main = per * t_kb;
       const double t_epi = rows * bn * (s > 1 ? 4.0 : 2.0) / 20e3 + 0.8;  // + per-task fixed cost
       double t = waves * std::max(t_main, t_epi) + std::min(t_main, t_epi) + 1.5;
-      if (s > 1) t += 3.0 + (double)tiles * 128 * bn * (4.0 * s + 2.0) / (G * 40e3);
+      if (s > 1) t += split_us + (double)tiles * 128 * bn * (4.0 * s + 2.0) / (G * 40e3);
       if (t < best - 1e-9) {
         best = t;
         best_bn = bn;
