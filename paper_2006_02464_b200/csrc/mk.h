@@ -62,6 +62,7 @@ constexpr uint32_t kMkPoolStage = 49152;  // stem: pooled pixels of one tile (TM
 constexpr uint32_t kMkTmemCols = 512;      // two accumulators of up to 256 columns
 constexpr int kMkMaxSlots = 16;            // smem ring slots (per-layer slot size)
 constexpr uint32_t kMkBarBytes = 512;
+constexpr int kMkMaxCout = 2048;  // shared-memory bias of one layer (fp32)
 // Epilogue staging: kMkOutBufs buffers of one 128-row x 64-column bf16 chunk (16 KB, 128-byte
 // swizzle): a chunk's residual lands there by TMA, the epilogue rewrites it in place with the
 // output, and a TMA store drains it. Also the stem-pool / split-K / avg-pool scratch.

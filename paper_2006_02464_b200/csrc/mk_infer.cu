@@ -1138,14 +1138,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         if (t >= d.tasks) continue;
         const float* bias_all = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[d.wlayer];
         if (d.splits == 1) {
-          // folded-BN bias of the first task's columns (weights: no dependency); a
-          // layer with one N tile uses the same columns for every task: both buffers
-          const int n0 = (t / d.splits % d.n_tiles) * d.bn;
-          for (int i = et; i < d.bn; i += kMkEpiThreads) {
-            const float bv = __ldg(bias_all + n0 + i);
-            sbias[acc * 256 + i] = bv;
-            if (d.n_tiles == 1) sbias[(acc ^ 1) * 256 + i] = bv;
-          }
+          // the layer's whole folded-BN bias (weights: no dependency), once per layer: no
+          // per-task global loads or barriers (the previous layer ended on a barrier)
+          for (int i = et; i < d.n_out; i += kMkEpiThreads) sbias[i] = __ldg(bias_all + i);
         }
         if (et == 0) wait_deps(sl, L, counters, gen1, 6);
         named_bar(1, kMkEpiThreads);
@@ -1186,11 +1181,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
               }
             }
           } else {
-            // folded-BN bias of this tile's columns, staged while the MMAs run
-            float* bias = sbias + acc * 256;
-            const bool bias_fixed = d.n_tiles == 1;  // staged once for the layer
-            if (done > 0 && !bias_fixed)
-              for (int i = et; i < d.bn; i += kMkEpiThreads) bias[i] = __ldg(bias_all + o.n0 + i);
+            // folded-BN bias of this tile's columns (staged for the whole layer)
+            const float* bias = sbias + o.n0;
+            constexpr bool bias_fixed = true;
             if (d.pool_pw) {
               CW_KET(200);
               mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 8);
@@ -1409,7 +1402,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   tc_fence_before();
   __syncthreads();
 #ifdef CW_KB_TRACE
-  if (cta == 0 && threadIdx.x == 64) {
+  if (cta == 0 && threadIdx.x == kMkEpiWarp0 * 32) {
     for (int i = 0; i < kbe; ++i)
       printf("ep %2d tag %3d t %6lld\n", i, (int)ket[1][i], (long long)(ket[0][i] - ket[0][0]));
   }
@@ -1451,7 +1444,7 @@ cudaError_t configure_mk() {
 
 uint32_t mk_smem_bytes(uint32_t ring_bytes, int n_layers) {
   (void)n_layers;  // the plan is in the constant bank
-  return 1024 + ring_bytes + kMkOutBufs * kMkOutBufBytes + kMkBarBytes + 2 * 256 * 4;
+  return 1024 + ring_bytes + kMkOutBufs * kMkOutBufBytes + kMkBarBytes + kMkMaxCout * 4;
 }
 
 int mk_blocks_per_sm(uint32_t smem) {

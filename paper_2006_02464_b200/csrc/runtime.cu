@@ -408,6 +408,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
         break;
       }
       case OP_CONV: {
+        if (op.cout > kMkMaxCout) return "conv Cout exceeds kMkMaxCout (shared-memory bias)";
         d.kind = MK_CONV;
         d.wlayer = op.layer;
         d.n_out = op.cout;
