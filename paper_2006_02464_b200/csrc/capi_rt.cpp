@@ -1,4 +1,5 @@
 // extern "C" surface of the device runtime (include/cw.h, cw_rt_*).
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <cstring>
 #include <string>
@@ -130,29 +131,36 @@ int cw_rt_exec_many(cw_runtime* rt, int arch_id, int batch, const int32_t* hdr_p
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   std::vector<uint64_t> seqs(n);
-  cudaEventRecord(e0, r.exec_stream());
-  for (int i = 0; i < n; ++i) {
-    // Never run more than half the descriptor ring ahead of the device.
-    const uint64_t next = r.exec_issued();
-    if (next >= Runtime::kRing / 2) {
-      const uint64_t need = next - Runtime::kRing / 2;
-      while (r.exec_record(need)->seq_started != need + 1) {
+  // The exec records live in a ring of kRing entries: harvest each INFER's record once it is
+  // done and before its slot is reused (at most kRing / 2 INFERs in flight).
+  int harvested = 0;
+  const int part = getenv("CW_EXEC_PART") ? atoi(getenv("CW_EXEC_PART")) : 0;
+  auto harvest = [&](int upto) {
+    for (; harvested < upto; ++harvested) {
+      cw::ExecRecord* rec = r.exec_record(seqs[harvested]);
+      while (rec->seq_done != seqs[harvested] + 1) {
+      }
+      if (exec_ns) {  // CW_EXEC_PART (diagnostics): 1 = megakernel span, 2 = gate -> megakernel
+        exec_ns[harvested] = part == 1   ? (int64_t)(rec->t_mk1 - rec->t_mk0)
+                             : part == 2 ? (int64_t)(rec->t_mk0 - rec->t_start)
+                                         : (int64_t)(rec->t_end - rec->t_start);
       }
     }
+  };
+  cudaEventRecord(e0, r.exec_stream());
+  for (int i = 0; i < n; ++i) {
+    if (i >= Runtime::kRing / 2) harvest(i - Runtime::kRing / 2 + 1);
     std::string err = r.exec_async(arch_id, batch, hdr_pages[i], slots.data(), 0, ~0ull, -1, &seqs[i]);
     if (!err.empty()) return cw::fail(err);
   }
   cudaEventRecord(e1, r.exec_stream());
   if (cudaEventSynchronize(e1) != cudaSuccess) return cw::fail("exec_many sync failed");
+  harvest(n);
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   if (wall_ns) *wall_ns = (int64_t)(ms * 1e6);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  for (int i = 0; i < n; ++i) {
-    cw::ExecRecord* rec = r.exec_record(seqs[i]);
-    if (exec_ns) exec_ns[i] = (int64_t)(rec->t_end - rec->t_start);
-  }
   return 0;
 }
 

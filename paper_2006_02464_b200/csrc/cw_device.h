@@ -34,6 +34,8 @@ struct ActionBlock {
   int32_t skip;                // 1: window missed, every kernel returns immediately
   int32_t batch;
   uint64_t seq;
+  unsigned long long mk_t0;    // megakernel: earliest CTA start / latest CTA end (%globaltimer)
+  unsigned long long mk_t1;
 };
 
 // Host -> device descriptor ring entry (mapped pinned memory).
@@ -58,6 +60,8 @@ struct alignas(64) ExecRecord {
   volatile int32_t pad_;
   volatile uint64_t seq_out;       // == seq once the Output copy completed
   volatile uint64_t t_out;
+  volatile uint64_t t_mk0;         // megakernel span inside [t_start, t_end] (diagnostics)
+  volatile uint64_t t_mk1;
 };
 
 }  // namespace cw

@@ -622,6 +622,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     clk_trace[0] = globaltimer();
     clk_trace[1] = clock64();
   }
+  if (threadIdx.x == 0) atomicMin(const_cast<unsigned long long*>(&ab->mk_t0), globaltimer());
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw_addr & 1023u)) & 1023u);
@@ -1422,6 +1423,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     clk_trace[3] = clock64();
     clk_trace[2] = globaltimer();
   }
+  if (threadIdx.x == 0) atomicMax(const_cast<unsigned long long*>(&ab->mk_t1), globaltimer());
 }
 
 // Bumps the plan generation after a completed (non-skipped) INFER and stamps Exec end.
@@ -1430,6 +1432,8 @@ __global__ void mk_done_kernel(const ActionBlock* ab, uint32_t ring_mask, ExecRe
   const uint64_t i = ab->seq;
   if (!ab->skip) *gen += 1u;
   ExecRecord* r = &recs[i & ring_mask];
+  r->t_mk0 = ab->mk_t0;
+  r->t_mk1 = ab->mk_t1;
   r->t_end = globaltimer();
   __threadfence_system();
   r->seq_done = i + 1;

@@ -40,6 +40,8 @@ __global__ void gate_kernel(ActionBlock* ab, const ActionDesc* ring, uint32_t ri
     }
     ab->batch = d->batch;
     ab->seq = i;
+    ab->mk_t0 = ~0ull;
+    ab->mk_t1 = 0ull;
     uint64_t t = globaltimer();
     while (t < d->earliest_gt) t = globaltimer();
     const int rej = t > d->latest_gt;
