@@ -36,6 +36,9 @@ struct ActionBlock {
   uint64_t seq;
   unsigned long long mk_t0;    // megakernel: earliest CTA start / latest CTA end (%globaltimer)
   unsigned long long mk_t1;
+  uint64_t t_start;            // gate: Exec start (%globaltimer); copied to the host record by
+  int32_t rejected;            // mk_done, off the gate -> megakernel critical path
+  int32_t pad_;
 };
 
 // Host -> device descriptor ring entry (mapped pinned memory).

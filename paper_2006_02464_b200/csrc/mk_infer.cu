@@ -31,6 +31,8 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <utility>
 
 #include "cw_device.h"
 #include "mk.h"
@@ -615,6 +617,9 @@ __device__ __forceinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigi
 
 __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_constant__ MkArgs args) {
   const ActionBlock* ab = args.ab;
+  // programmatic dependent launch: the CTAs become resident while the gate still runs; the
+  // action block (and everything before it) is visible after the wait
+  griddep_wait();
   if (ab->skip) return;  // window missed: the gate kernel already recorded the rejection
   uint64_t* clk_trace =
       args.trace ? args.trace + ((size_t)args.n_layers * gridDim.x + blockIdx.x) * 4 : nullptr;
@@ -1424,17 +1429,23 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     clk_trace[2] = globaltimer();
   }
   if (threadIdx.x == 0) atomicMax(const_cast<unsigned long long*>(&ab->mk_t1), globaltimer());
+  griddep_trigger();
 }
 
 // Bumps the plan generation after a completed (non-skipped) INFER and stamps Exec end.
 __global__ void mk_done_kernel(const ActionBlock* ab, uint32_t ring_mask, ExecRecord* recs,
                                uint32_t* gen) {
+  griddep_wait();  // the megakernel has completed
   const uint64_t i = ab->seq;
   if (!ab->skip) *gen += 1u;
   ExecRecord* r = &recs[i & ring_mask];
+  const uint64_t t_end = globaltimer();
+  r->t_start = ab->t_start;
+  r->rejected = ab->rejected;
   r->t_mk0 = ab->mk_t0;
   r->t_mk1 = ab->mk_t1;
-  r->t_end = globaltimer();
+  r->t_end = t_end;
+  r->seq_started = i + 1;
   __threadfence_system();
   r->seq_done = i + 1;
 }
@@ -1467,14 +1478,36 @@ cudaError_t copy_plan(const MkLayer* d_layers, int n, cudaStream_t st) {
   return cudaMemcpyAsync(dst, d_layers, sizeof(MkLayer) * n, cudaMemcpyDeviceToDevice, st);
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may start before its
+// predecessor in the stream completes; it synchronises with griddepcontrol.wait.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, uint32_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 cudaError_t launch_mk(const MkArgs& a, int grid, uint32_t smem, cudaStream_t st) {
-  mk_infer_kernel<<<grid, kMkThreads, smem, st>>>(a);
-  return cudaGetLastError();
+  if (getenv("CW_NO_PDL")) {
+    mk_infer_kernel<<<grid, kMkThreads, smem, st>>>(a);
+    return cudaGetLastError();
+  }
+  return launch_pdl(mk_infer_kernel, dim3(grid), dim3(kMkThreads), smem, st, a);
 }
 
 void launch_mk_done(const ActionBlock* ab, uint32_t mask, ExecRecord* recs, uint32_t* gen,
                     cudaStream_t st) {
-  mk_done_kernel<<<1, 1, 0, st>>>(ab, mask, recs, gen);
+  if (getenv("CW_NO_PDL")) mk_done_kernel<<<1, 1, 0, st>>>(ab, mask, recs, gen);
+  else launch_pdl(mk_done_kernel, dim3(1), dim3(1), 0, st, ab, mask, recs, gen);
 }
 
 }  // namespace cw

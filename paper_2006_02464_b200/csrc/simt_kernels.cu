@@ -46,13 +46,12 @@ __global__ void gate_kernel(ActionBlock* ab, const ActionDesc* ring, uint32_t ri
     while (t < d->earliest_gt) t = globaltimer();
     const int rej = t > d->latest_gt;
     ab->skip = rej;
-    ExecRecord* r = &recs[i & ring_mask];
-    r->t_start = t;
-    r->rejected = rej;
-    __threadfence_system();
-    r->seq_started = i + 1;
-    __threadfence();
+    ab->t_start = t;   // the host record is written by mk_done (no PCIe fence on this path)
+    ab->rejected = rej;
+    (void)recs;
   }
+  __syncthreads();
+  griddep_trigger();  // the megakernel (PDL) may proceed past its griddepcontrol.wait
 }
 
 __global__ void out_done_kernel(ExecRecord* rec, uint64_t seq) {
