@@ -14,3 +14,7 @@ with DeviceRuntime(pages_total=8, io_slots=16) as rt:
     for i, r in enumerate(pl): print(i, [int(x) for x in r])
     out, _ = rt.infer(0, 0, arch.make_inputs(b, spec))
     print("ok", out.shape)
+    if len(sys.argv) > 3:
+        for _ in range(int(sys.argv[3])):
+            out, _ = rt.infer(0, 0, arch.make_inputs(b, spec))
+        print("ok2")
