@@ -103,6 +103,12 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const void* tmap, uint
 }
 
 // Non-tensor bulk copy global -> shared (16-byte aligned, size % 16 == 0), mbarrier completion.
+// 1D bulk copy shared -> global (bulk async-group of the issuing thread).
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+               "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),

@@ -554,8 +554,13 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
           while (parts < rows && (size_t)d.splits * ((rows + parts - 1) / parts) * d.bn * 4 >
                                      (size_t)kMkOutBufs * kMkOutBufBytes)
             parts *= 2;
+          // and its bf16 output rows are staged in the bias area for the bulk stores
+          while (parts < rows && (size_t)((rows + parts - 1) / parts) * d.bn * 2 >
+                                     (size_t)kMkMaxCout * 4)
+            parts *= 2;
           if ((size_t)d.splits * ((rows + parts - 1) / parts) * d.bn * 4 >
-              (size_t)kMkOutBufs * kMkOutBufBytes)
+                  (size_t)kMkOutBufs * kMkOutBufBytes ||
+              (size_t)((rows + parts - 1) / parts) * d.bn * 2 > (size_t)kMkMaxCout * 4)
             return "split-K reduce rows exceed the staging buffers";
           r.red_rows = (rows + parts - 1) / parts;
           r.red_parts = (rows + r.red_rows - 1) / r.red_rows;

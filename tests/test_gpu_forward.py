@@ -56,3 +56,26 @@ def test_resnet_family_logits_match_oracle(gpu, name, batch):
     ref = resnet_oracle.logits(resnet_oracle.torchvision_model(name, params), x)
     c = resnet_oracle.compare(got, ref)
     assert c["ok"], c
+
+
+@pytest.mark.parametrize("batch", [1, 16])
+def test_layer_handoff_repeatable_under_alternating_inputs(gpu, r50, batch):
+    """Layer-to-layer handoff stress (the conv layers publish their completion counts with
+    a relaxed add after their TMA stores completed, see red_after_bulk_add in mk_infer.cu):
+    hundreds of INFERs alternating two inputs must reproduce each input's first logits bit
+    for bit. A consumer that read a producer's tile before it landed would see the other
+    input's (or an earlier layer's) activations in the reused arena and diverge."""
+    spec, blob, _ = r50
+    xs = [arch.make_inputs(batch, spec, first=11 + k * batch) for k in range(2)]
+    with DeviceRuntime(device=gpu, pages_total=8, io_slots=16) as rt:
+        rt.register_arch(0, spec, batches=(batch,))
+        rt.register_blob(0, 0, blob)
+        rt.build()
+        rt.load(0, list(range(blob.pages)))
+        first = [rt.infer(0, 0, x)[0].copy() for x in xs]
+        assert not np.array_equal(first[0], first[1])
+        bad = 0
+        for i in range(400 if batch == 1 else 200):
+            got, _ = rt.infer(0, 0, xs[i & 1])
+            bad += not np.array_equal(got, first[i & 1])
+    assert bad == 0, f"{bad} INFERs differ from the first run of their input"
