@@ -365,6 +365,71 @@ __device__ __forceinline__ void simt_avgpool(const MkLayer& d, int cta, int G, i
 // K parts, interleaved 8-element chunks): a thread reads its part of pooled[n] once per block
 // and accumulates all the block's classes from it, then the K parts reduce (shuffles, and
 // shared memory when an image spans several warps). C % 64 == 0, batch <= 16.
+// Warp reduce-scatter of V per-lane partial sums (V = 8 or 16, a power of two <= 32):
+// log2(V) halving exchanges (offsets 16, 8, ...) then full exchanges, so every value is
+// summed over the 32 lanes with V - 1 + 5 - log2(V) shuffles instead of 5 V. Lane l ends
+// with value index fc_rs_index<V>(l).
+template <int V>
+__device__ __forceinline__ float fc_reduce_scatter(float (&v)[V], int lane) {
+  int o = 16;
+#pragma unroll
+  for (int h = V / 2; h >= 1; h /= 2, o >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int i = 0; i < h; ++i) {
+      const float send = up ? v[i] : v[i + h];
+      const float keep = up ? v[i + h] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  float r = v[0];
+  for (; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
+template <int V>
+__device__ __forceinline__ int fc_rs_index(int lane) {
+  int idx = 0, o = 16;
+  for (int h = V / 2; h >= 1; h /= 2, o >>= 1) idx += (lane & o) ? h : 0;
+  return idx;
+}
+
+// Partial dot products of NI images x 8 classes over this thread's interleaved 8-element K
+// chunks (consecutive threads read consecutive 16-byte words of the staged rows).
+template <int NI>
+__device__ __forceinline__ void fc_mac(const float* const (&pn)[NI], const __nv_bfloat16* sw, int C,
+                                       int k0, int kstep, float (&acc)[NI * 8]) {
+#pragma unroll
+  for (int i = 0; i < NI * 8; ++i) acc[i] = 0.0f;
+#pragma unroll 2
+  for (int k = k0; k < C; k += kstep) {
+    uint4 wv[8];  // all 8 rows' words first (rows >= nj hold stale data: sums discarded)
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) wv[jj] = *reinterpret_cast<const uint4*>(sw + jj * C + k);
+#pragma unroll
+    for (int ii = 0; ii < NI; ++ii) {
+      const float4 p0 = *reinterpret_cast<const float4*>(pn[ii] + k);
+      const float4 p1 = *reinterpret_cast<const float4*>(pn[ii] + k + 4);
+      const float pv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+      for (int e2 = 0; e2 < 4; ++e2) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const uint32_t u = e2 == 0 ? wv[jj].x : e2 == 1 ? wv[jj].y : e2 == 2 ? wv[jj].z : wv[jj].w;
+          float& a = acc[ii * 8 + jj];
+          a = fmaf(__uint_as_float(u << 16), pv[2 * e2], a);
+          a = fmaf(__uint_as_float(u & 0xFFFF0000u), pv[2 * e2 + 1], a);
+        }
+      }
+    }
+  }
+}
+
+// Fully connected layer over the pooled features (fp32 [batch][C]) with bf16 weights
+// [classes][C]: CTA g takes classes 8g..8g+7; the pooled block and the weight rows are
+// bulk-copied into shared memory. Batch <= 8: an image per group of 256/nbp threads, each
+// thread 8 classes x its K chunks, warp reduce-scatter, then the image's warps through
+// shared memory. Batch 9..16: a warp per image pair (images w and w+8), 2 x 8 sums per
+// thread: half the shared-memory weight reads per FMA.
 __device__ __forceinline__ void simt_fc(const MkLayer& d, const ActionBlock* ab, const uint8_t* hdr,
                                      int cta, int G, int et, float* sp, uint32_t sp_addr,
                                      const __nv_bfloat16* sw, uint32_t sw_addr, float* sred,
@@ -372,7 +437,7 @@ __device__ __forceinline__ void simt_fc(const MkLayer& d, const ActionBlock* ab,
   const int C = d.C;
   int nbp = 1;
   while (nbp < d.batch) nbp <<= 1;
-  const int parts = kMkEpiThreads / nbp, n = et / parts, part = et % parts;
+  const int lane = et & 31, warp = et >> 5;
   const __nv_bfloat16* wbase =
       reinterpret_cast<const __nv_bfloat16* const*>(hdr + kHdrWeightOff)[d.wlayer];
   const float* bias = reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[d.wlayer];
@@ -390,11 +455,6 @@ __device__ __forceinline__ void simt_fc(const MkLayer& d, const ActionBlock* ab,
       bulk_g2s(sw_addr, wbase + (size_t)j0 * C, wbytes, bar);
     }
     pooled_in = true;
-    // epilogue operands fetched while the copies fly (global latency, not on the tail)
-    float bj[8];
-#pragma unroll
-    for (int jj = 0; jj < 8; ++jj) bj[jj] = jj < nj ? __ldg(bias + j0 + jj) : 0.0f;
-    float* const outn = (part == 0 && n < d.batch) ? ab->out[n] : nullptr;
 #ifdef CW_KB_TRACE
     const long long tf0 = clock64();
 #endif
@@ -403,62 +463,42 @@ __device__ __forceinline__ void simt_fc(const MkLayer& d, const ActionBlock* ab,
 #ifdef CW_KB_TRACE
     const long long tf1 = clock64();
 #endif
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (n < d.batch) {
-      // interleaved 8-element K chunks: consecutive threads read consecutive 16-byte words
-      const float* pn = sp + n * C;
-#pragma unroll 2
-      for (int k = part * 8; k < C; k += parts * 8) {
-        const float4 p0 = *reinterpret_cast<const float4*>(pn + k);
-        const float4 p1 = *reinterpret_cast<const float4*>(pn + k + 4);
-        const float pv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-        // all 8 rows' words first (rows >= nj hold stale data: their sums are discarded)
-        uint4 wv[8];
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) wv[jj] = *reinterpret_cast<const uint4*>(sw + jj * C + k);
-#pragma unroll
-        for (int e2 = 0; e2 < 4; ++e2) {
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            const uint32_t u = e2 == 0 ? wv[jj].x : e2 == 1 ? wv[jj].y : e2 == 2 ? wv[jj].z : wv[jj].w;
-            acc[jj] = fmaf(__uint_as_float(u << 16), pv[2 * e2], acc[jj]);
-            acc[jj] = fmaf(__uint_as_float(u & 0xFFFF0000u), pv[2 * e2 + 1], acc[jj]);
-          }
+    if (nbp > 8) {
+      // warp w: images w and w + 8 (the second may not exist: its sums are discarded)
+      const int n1 = warp + 8 < d.batch ? warp + 8 : warp;
+      const float* const pn[2] = {sp + warp * C, sp + n1 * C};
+      float acc[16];
+      fc_mac<2>(pn, sw, C, lane * 8, 256, acc);
+      const float v = fc_reduce_scatter<16>(acc, lane);
+      const int idx = fc_rs_index<16>(lane), jj = idx & 7, n = warp + (idx >> 3) * 8;
+      if ((lane & 1) == 0 && jj < nj && n < d.batch && warp < d.batch)
+        ab->out[n][j0 + jj] = v + __ldg(bias + j0 + jj);
+    } else {
+      const int parts = kMkEpiThreads / nbp, n = et / parts, part = et % parts;
+      const float* const pn[1] = {sp + (n < d.batch ? n : 0) * C};
+      float acc[8];
+      fc_mac<1>(pn, sw, C, part * 8, parts * 8, acc);
+      const float v = fc_reduce_scatter<8>(acc, lane);
+      const int jj = fc_rs_index<8>(lane);
+      if (parts == 32) {
+        if ((lane & 3) == 0 && jj < nj && n < d.batch)
+          ab->out[n][j0 + jj] = v + __ldg(bias + j0 + jj);
+      } else {  // an image spans parts / 32 warps: finish through shared memory
+        if ((lane & 3) == 0) sred[warp * 8 + jj] = v;
+        named_bar(1, kMkEpiThreads);
+        const int wpi = parts >> 5, ni = et >> 3, cj = et & 7;
+        if (ni < d.batch && cj < nj) {
+          float s = __ldg(bias + j0 + cj);
+          for (int w = ni * wpi; w < (ni + 1) * wpi; ++w) s += sred[w * 8 + cj];
+          ab->out[ni][j0 + cj] = s;
         }
       }
-    }
-    const int wl = parts < 32 ? parts : 32;  // lanes of one image within a warp
-#pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      float v = acc[jj];
-      for (int o = wl >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      acc[jj] = v;
-    }
-    if (parts > 32) {  // one image spans parts / 32 warps: finish through shared memory
-      if ((et & 31) == 0)
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) sred[(et >> 5) * 8 + jj] = acc[jj];
-      named_bar(1, kMkEpiThreads);
-      if ((et & 31) == 0) {
-        const int w0 = (et >> 5) / (parts >> 5) * (parts >> 5);
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          float v = 0.0f;
-          for (int w = w0; w < w0 + (parts >> 5); ++w) v += sred[w * 8 + jj];
-          acc[jj] = v;
-        }
-      }
-    }
-    if (outn) {
-#pragma unroll
-      for (int jj = 0; jj < 8; ++jj)
-        if (jj < nj) outn[j0 + jj] = acc[jj] + bj[jj];
     }
 #ifdef CW_KB_TRACE
     if (et == 0 && (cta == 0 || cta == 100))
       printf("fc cta %d: copy wait %lld, compute %lld cycles\n", cta, tf1 - tf0, clock64() - tf1);
 #endif
-    named_bar(1, kMkEpiThreads);  // weights read before the next block's copy
+    named_bar(1, kMkEpiThreads);  // weights (and sred) read before the next block's copy
   }
 }
 
