@@ -42,6 +42,11 @@ namespace cw {
 
 __constant__ MkLayer c_plan[kMkMaxPlanLayers];  // the running INFER's plan (see mk.h)
 
+// residual chunks land this many chunks ahead of their use (<= kMkOutBufs - 1)
+#ifndef CW_RES_DIST
+#define CW_RES_DIST 3
+#endif
+constexpr int kResDist = CW_RES_DIST;
 constexpr uint64_t kMkTimeoutNs = 2000000000ull;  // 2 s: far above any INFER
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
@@ -1336,7 +1341,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                 else tma_load_4d(dst, tmr, bar, o.n0 + 64 * c, o.ow0, o.oh0, o.img0);
               };
               if (tmr && et == 0) {
-                for (int j = 0; j < nch && j < kMkOutBufs - 1; ++j) {
+                for (int j = 0; j < nch && j < kResDist; ++j) {
                   bulk_wait_read_n(kMkOutBufs - 1 - j);  // the buffer's previous store has read it
                   issue_res((ocnt + j) % kMkOutBufs, j);
                 }
@@ -1417,9 +1422,10 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                   if (m2d) tma_store_2d(tmo, src, o.n0 + 64 * c, o.m0);
                   else tma_store_4d(tmo, src, o.n0 + 64 * c, o.ow0, o.oh0, o.img0);
                   bulk_commit();
-                  if (tmr && c + kMkOutBufs - 1 < nch) {
-                    bulk_wait_read<1>();  // buffer of chunk ocnt-1 (the next residual's) is free
-                    issue_res((ocnt + kMkOutBufs - 1) % kMkOutBufs, c + kMkOutBufs - 1);
+                  if (tmr && c + kResDist < nch) {
+                    // buffer of chunk c + kResDist - kMkOutBufs is free
+                    bulk_wait_read<kMkOutBufs - kResDist>();
+                    issue_res((ocnt + kResDist) % kMkOutBufs, c + kResDist);
                   }
                 }
               }
