@@ -171,6 +171,7 @@ int cw_rt_buffer_io(cw_runtime* rt, int arch_id, int buf, void* host, int64_t by
   if ((size_t)bytes > a->buf_bytes[buf]) return cw::fail("buffer too small");
   cudaError_t e = to_device ? cudaMemcpy(a->bufs[buf], host, bytes, cudaMemcpyHostToDevice)
                             : cudaMemcpy(host, a->bufs[buf], bytes, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && to_device) e = cudaStreamSynchronize(0);  // DMA landed (pageable)
   return e == cudaSuccess ? 0 : cw::fail(cudaGetErrorString(e));
 }
 

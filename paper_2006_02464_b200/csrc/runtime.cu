@@ -704,6 +704,8 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
   CW_TRY(cudaMemset(p.d_gen, 0, sizeof(uint32_t)));
   CW_TRY(cudaMalloc(&p.d_trace, sizeof(uint64_t) * (nl + 1) * G * 4));
   CW_TRY(cudaMemset(p.d_trace, 0, sizeof(uint64_t) * (nl + 1) * G * 4));
+  // pageable-source copies and legacy-stream memsets vs the non-blocking Exec stream
+  CW_TRY(cudaStreamSynchronize(0));
   return "";
 }
 
@@ -844,6 +846,9 @@ std::string Runtime::input_from_host(int arch, const int32_t* slots, const float
   const int64_t bytes = (int64_t)a->in_c * a->in_h * a->in_w * 4;
   for (int j = 0; j < batch; ++j)
     CW_TRY(cudaMemcpy(slot_in(slots[j]), host + j * (bytes / 4), bytes, cudaMemcpyHostToDevice));
+  // a pageable-memory cudaMemcpy may return before its DMA lands, and the Exec stream is
+  // non-blocking (no implicit ordering with the legacy stream)
+  CW_TRY(cudaStreamSynchronize(0));
   return "";
 }
 
