@@ -265,10 +265,17 @@ def run_ours(args, d: Dist) -> dict | None:
             rt.exec_many(0, bb, hp[:50])
             ex_b, wall_b = rt.exec_many(0, bb, hp[50:])
             p50 = pct(ex_b, 50)
+            # ~2 ms whole-GPU stalls hit any kernel on these boxes every few seconds (a plain
+            # FMA kernel shows them too: tools/stall_probe.cu, profiles/r1_tail.txt): counted
+            # and also excluded in a separately labelled percentile; the raw one stays
+            stall = ex_b > p50 + 1_000_000
+            calm = ex_b[~stall]
             sweep[str(bb)] = {
                 "img_s": bb * n / (wall_b / 1e9), "p50_us": p50 / 1e3,
                 "p99_us": pct(ex_b, 99) / 1e3, "p9999_us": pct(ex_b, 99.99) / 1e3,
                 "max_us": float(ex_b.max()) / 1e3, "p9999_over_p50": pct(ex_b, 99.99) / p50,
+                "platform_stalls": int(stall.sum()),
+                "p9999_over_p50_excl_stalls": pct(calm, 99.99) / p50,
                 "n": n, "roofline_us": max(spec.flops_per_image * bb / (bf16_peak * 1e12),
                                            (blob.data.nbytes + bb * 606112) / (hbm_peak * 1e9)) * 1e6}
         out["infer"] = sweep
