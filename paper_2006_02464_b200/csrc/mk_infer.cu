@@ -659,24 +659,28 @@ __device__ __forceinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigi
         const int prow = r * bw + 2 * j + cq;  // always inside the staged tile
         v[r * 3 + cq] = *reinterpret_cast<const uint4*>(pb + prow * 128 + ((k ^ (prow & 7)) << 4));
       }
-    float mx[8], f[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) mx[e] = -INFINITY;
+    // the staged values are post-ReLU bf16 (>= 0), whose bit patterns order like their
+    // values once the sign bit (a possible -0) is cleared: the window max is an unsigned
+    // 16-bit SIMD max per word, exact; positions outside the image contribute 0 (every
+    // window holds at least one valid position, whose value is >= 0)
+    uint32_t mx[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int cq = 0; cq < 3; ++cq) {
         const int cc = ow0 + 2 * j + cq;
-        const bool ok = (rmask >> r & 1) && cc >= 0 && cc < ow;
-        bf16x8_to_f32(v[r * 3 + cq], f);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx[e] = ok ? fmaxf(mx[e], f[e]) : mx[e];
+        const uint32_t keep = ((rmask >> r & 1) && cc >= 0 && cc < ow) ? 0x7FFF7FFFu : 0u;
+        const uint4 q = v[r * 3 + cq];
+        mx[0] = __vmaxu2(mx[0], q.x & keep);
+        mx[1] = __vmaxu2(mx[1], q.y & keep);
+        mx[2] = __vmaxu2(mx[2], q.z & keep);
+        mx[3] = __vmaxu2(mx[3], q.w & keep);
       }
     uint4 w;
-    w.x = pack_bf16x2(mx[0], mx[1]);
-    w.y = pack_bf16x2(mx[2], mx[3]);
-    w.z = pack_bf16x2(mx[4], mx[5]);
-    w.w = pack_bf16x2(mx[6], mx[7]);
+    w.x = mx[0];
+    w.y = mx[1];
+    w.z = mx[2];
+    w.w = mx[3];
     *reinterpret_cast<uint4*>(ps + j * 128 + ((k ^ (j & 7)) << 4)) = w;
   }
   fence_proxy_async_smem();
