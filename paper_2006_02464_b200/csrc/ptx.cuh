@@ -103,6 +103,10 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const void* tmap, uint
 }
 
 // Non-tensor bulk copy global -> shared (16-byte aligned, size % 16 == 0), mbarrier completion.
+// L2 prefetch of a global range (no shared memory, no completion tracking).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 // 1D bulk copy shared -> global (bulk async-group of the issuing thread).
 __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
