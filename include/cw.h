@@ -187,6 +187,47 @@ int64_t cw_engine_io_in_use(cw_engine* e, int gpu_index);
 int cw_engine_output(cw_engine* e, int gpu_index, int64_t output_ref, float* dst, int batch,
                      int classes);
 
+/* ------------------------------------------------------------------ cw_wire_* / cw_net_*
+ * The controller connection in native code. Replaces, per action,
+ * the Python path run_worker_server -> protocol.recv/decode -> on_action and
+ * _finish -> send_result -> protocol.send:
+ *   cw_wire_decode_action     protocol.py:177-229 (decode, tag 2) + Action invariants :91-104
+ *   cw_wire_encode_result     protocol.py:146-152 (ActionResult encode) + invariants :126-130
+ *   cw_wire_encode_handshake  protocol.py:133-139 (WorkerHandshake encode)
+ *   cw_net_serve              harness.py:525-575 (run_worker_server's accept-side loop)
+ * Decode errors (negative): */
+#define CW_WIRE_TRUNCATED (-1) /* protocol.py:53-55 TruncatedFrame */
+#define CW_WIRE_BAD_TAG (-2)   /* protocol.py:57-59 UnknownMessageType */
+#define CW_WIRE_INVALID (-3)   /* protocol.py:61-63 InvalidMessage */
+#define CW_WIRE_RESULT_FRAME 38 /* 4-byte length prefix + 34-byte ActionResult payload */
+
+int cw_wire_decode_action(const uint8_t* payload, int64_t n, cw_action* out);
+int cw_wire_encode_result(const cw_result* r, uint8_t* out /* CW_WIRE_RESULT_FRAME bytes */);
+int64_t cw_wire_encode_handshake(uint32_t worker_id, uint32_t gpu_count, uint64_t pages_total,
+                                 const uint32_t* ids, int32_t n, uint8_t* out, int64_t cap);
+
+/* One telemetry row per finished action (server.py TELEMETRY_HEADER). */
+typedef struct cw_net_record {
+  uint64_t action_id;
+  int32_t kind;
+  uint32_t model_id;
+  int32_t gpu_index;
+  int32_t batch_size;
+  int32_t status;
+  int32_t pad_;
+  int64_t start, end, device_duration;
+} cw_net_record;
+
+/* Serve one connected controller socket on a started engine: send the handshake
+ * frame, then read Action frames into cw_engine_submit on this thread while a native
+ * writer thread turns cw_engine_poll results into ActionResult frames. Returns 0 when the
+ * controller closes the connection (or sends a malformed frame), after the in-flight
+ * results drained for up to 2 s. Telemetry rows go to recs (up to rec_cap). Blocking.
+ * A sim-mode engine is run in wall time (virtual clock = CLOCK_REALTIME - epoch_ns). */
+int cw_net_serve(cw_engine* e, int fd, const uint8_t* handshake_frame, int64_t hs_len,
+                 int64_t epoch_ns, cw_net_record* recs, int64_t rec_cap, int64_t* n_recs,
+                 int64_t* n_actions);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,14 @@ class cw_result(C.Structure):
         ("output_ref", C.c_int64), ("pages_free", C.c_int64)]
 
 
+class cw_net_record(C.Structure):
+    _fields_ = [
+        ("action_id", C.c_uint64), ("kind", C.c_int32), ("model_id", C.c_uint32),
+        ("gpu_index", C.c_int32), ("batch_size", C.c_int32), ("status", C.c_int32),
+        ("pad_", C.c_int32), ("start", C.c_int64), ("end", C.c_int64),
+        ("device_duration", C.c_int64)]
+
+
 # (name, restype, argtypes) for every symbol include/cw.h declares.
 _P = C.c_void_p
 _I32P = C.POINTER(C.c_int32)
@@ -103,6 +111,13 @@ SIGNATURES = [
     ("cw_engine_pages", C.c_int, [_P, C.c_int, _I64P, _I32P, _I32P, C.c_int, _I32P]),
     ("cw_engine_io_in_use", C.c_int64, [_P, C.c_int]),
     ("cw_engine_output", C.c_int, [_P, C.c_int, C.c_int64, _P, C.c_int, C.c_int]),
+    ("cw_wire_decode_action", C.c_int, [C.c_char_p, C.c_int64, C.POINTER(cw_action)]),
+    ("cw_wire_encode_result", C.c_int, [C.POINTER(cw_result), C.c_char_p]),
+    ("cw_wire_encode_handshake", C.c_int64, [C.c_uint32, C.c_uint32, C.c_uint64,
+                                             C.POINTER(C.c_uint32), C.c_int32, C.c_char_p,
+                                             C.c_int64]),
+    ("cw_net_serve", C.c_int, [_P, C.c_int, C.c_char_p, C.c_int64, C.c_int64,
+                               C.POINTER(cw_net_record), C.c_int64, _I64P, _I64P]),
 ]
 
 

@@ -43,6 +43,8 @@ def main(argv=None) -> int:
     p.add_argument("--devices", default="", help="comma-separated CUDA devices, one per gpu")
     p.add_argument("--mode", choices=["cuda", "sim"], default="cuda")
     p.add_argument("--weights-seed", type=int, default=0)
+    p.add_argument("--native-net", action="store_true",
+                   help="serve the controller socket from native threads (csrc/net.cpp)")
     args = ap.parse_args(argv)
     if args.clock == "sim":
         print("worker: simulated clock mode only makes sense in-process", file=sys.stderr)
@@ -53,7 +55,7 @@ def main(argv=None) -> int:
                  telemetry_path=args.telemetry,
                  ready_fd=args.ready_fd if args.ready_fd >= 0 else None,
                  worker_id=args.worker_id, devices=devices, mode=args.mode,
-                 weights_seed=args.weights_seed)
+                 weights_seed=args.weights_seed, native=args.native_net)
     return 0
 
 

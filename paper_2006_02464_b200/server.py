@@ -18,7 +18,7 @@ import time
 
 from . import wire
 from .timebase import WallClock, WallLoop
-from .worker import DEFAULT_IO_CAPACITY, B200Worker
+from .worker import DEFAULT_IO_CAPACITY, B200Worker, WorkerActionRecord
 
 TELEMETRY_HEADER = ["action_id", "kind", "model_id", "gpu", "batch_size", "status", "start_ns",
                     "end_ns", "device_duration_ns"]
@@ -38,7 +38,10 @@ def serve(listen: str, catalog, gpu_count: int = 1, pages_per_gpu: int = 500, ji
           seed: int = 0, epoch_ns: int | None = None, telemetry_path: str = "",
           io_capacity: int = DEFAULT_IO_CAPACITY, ready_fd: int | None = None, *,
           worker_id: int = 0, devices=None, mode: str = "cuda", weights_seed: int = 0,
-          on_ready=None) -> None:
+          on_ready=None, native: bool = False) -> None:
+    """native=True: after the accept, the connection is served by cw_net_serve (csrc/net.cpp):
+    frames are decoded into the engine and results encoded back in native threads, with no
+    Python on the per-action path."""
     host, port = listen.rsplit(":", 1)
     lsock = socket.socket()
     lsock.setsockopt(socket.SOL_SOCKET, socket.SO_REUSEADDR, 1)
@@ -68,7 +71,8 @@ def serve(listen: str, catalog, gpu_count: int = 1, pages_per_gpu: int = 500, ji
     worker = B200Worker(worker_id, catalog, loop, send_result, gpu_count=gpu_count,
                         pages_per_gpu=pages_per_gpu, io_capacity=io_capacity, jitter=jitter,
                         seed=seed, keep_records=bool(telemetry_path), mode=mode, devices=devices,
-                        weights_seed=weights_seed, epoch_ns=clock.epoch_ns)
+                        weights_seed=weights_seed, epoch_ns=clock.epoch_ns,
+                        poll_results=not native)
     if ready_fd is not None:
         os.write(ready_fd, f"{bound}\n".encode())
         os.close(ready_fd)
@@ -76,6 +80,9 @@ def serve(listen: str, catalog, gpu_count: int = 1, pages_per_gpu: int = 500, ji
         on_ready(bound)
     conn, _ = lsock.accept()
     conn.setsockopt(socket.IPPROTO_TCP, socket.TCP_NODELAY, 1)
+    if native:
+        _serve_native(worker, conn, lsock, clock, loop, mode, telemetry_path)
+        return
     with wlock:
         conn_box["conn"] = conn
         wire.send(conn, worker.handshake())
@@ -109,6 +116,34 @@ def serve(listen: str, catalog, gpu_count: int = 1, pages_per_gpu: int = 500, ji
         finally:
             if telemetry_path:
                 _write_telemetry(telemetry_path, worker.records)
+
+
+def _serve_native(worker, conn, lsock, clock, loop, mode, telemetry_path) -> None:
+    import ctypes as C
+
+    from . import native_wire
+    from ._lib import check, cw_net_record, lib
+
+    hs = native_wire.encode_handshake(worker.handshake())
+    cap = 1 << 20 if telemetry_path else 0
+    recs = (cw_net_record * cap)() if cap else None
+    n_recs, n_act = C.c_int64(0), C.c_int64(0)
+    try:
+        if mode != "cuda":
+            loop.stop(join=True)  # the native loop drives the sim engine from here on
+        check(lib.cw_net_serve(worker.engine.h, conn.fileno(), hs, len(hs), clock.epoch_ns, recs,
+                               cap, C.byref(n_recs), C.byref(n_act)), "net_serve")
+    finally:
+        conn.close()
+        lsock.close()
+        try:
+            worker.close()
+        finally:
+            if telemetry_path:
+                rows = [WorkerActionRecord(r.action_id, r.kind, r.model_id, r.gpu_index,
+                                           r.batch_size, r.status, r.start, r.end,
+                                           r.device_duration) for r in recs[:n_recs.value]]
+                _write_telemetry(telemetry_path, rows)
 
 
 def _write_telemetry(path: str, records) -> None:

@@ -180,7 +180,7 @@ class B200Worker:
                  io_capacity: int = DEFAULT_IO_CAPACITY, jitter=None, seed: int = 0,
                  keep_records: bool = True, *, mode: str = "cuda", devices=None,
                  weights_seed: int = 0, input_pool: int = 64, epoch_ns: int | None = None,
-                 keep_outputs: bool = False):
+                 keep_outputs: bool = False, poll_results: bool = True):
         if mode not in ("cuda", "sim"):
             raise ValueError(f"mode must be 'cuda' or 'sim', not {mode!r}")
         if jitter is not None and getattr(jitter, "kind", "none") != "none" and \
@@ -247,9 +247,12 @@ class B200Worker:
                     rt.register_blob(bi, bi, blobs[base])
                 rt.set_input_pool(pool)
             self.engine.start()
+            # poll_results=False: the results are consumed elsewhere (server.serve(native=True)
+            # hands the engine to the native serving loop, csrc/net.cpp)
             self._poller = threading.Thread(target=self._poll_loop, name=f"b200-results-{worker_id}",
                                             daemon=True)
-            self._poller.start()
+            if poll_results:
+                self._poller.start()
         else:
             self._scheduled = -1
 

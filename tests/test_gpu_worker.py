@@ -149,3 +149,49 @@ def test_device_gate_window(gpu):
         t = time.time_ns() + off
         rej, t0, t1 = rt.exec_window(0, 1, 0, 0, t - 10**6)
         assert rej
+
+
+def test_native_net_server_cuda(gpu, tmp_path):
+    """The controller socket served by cw_net_serve (csrc/net.cpp) on the cuda engine: a raw
+    client speaks the wire format (handshake, LOAD, INFERs, UNLOAD) and gets the same
+    statuses as through the Python path, with real device durations."""
+    import socket
+
+    from paper_2006_02464_b200 import server, wire
+
+    epoch = time.time_ns()
+    ports, ready = [], threading.Event()
+    t = threading.Thread(target=server.serve, args=("127.0.0.1:0", catalog.parse(CAT)),
+                         kwargs=dict(pages_per_gpu=16, epoch_ns=epoch, mode="cuda",
+                                     devices=[gpu], telemetry_path=str(tmp_path / "w.csv"),
+                                     native=True,
+                                     on_ready=lambda p: (ports.append(p), ready.set())),
+                         daemon=True)
+    t.start()
+    assert ready.wait(120)
+    s = socket.create_connection(("127.0.0.1", ports[0]))
+    hs = wire.recv(s)
+    assert isinstance(hs, wire.WorkerHandshake) and hs.pages_total == 16
+
+    def run(aid, kind, model, batch=(), lo=0, hi=10**9):
+        t0 = time.time_ns() - epoch
+        wire.send(s, Action(aid, kind, model, t0 + lo, t0 + hi, tuple(batch), 0,
+                            1 if kind == ActionKind.INFER else 0))
+        r = wire.recv(s)
+        assert r.action_id == aid
+        return r
+
+    assert run(1, ActionKind.INFER, 0, (1,)).status == wire.ResultStatus.MODEL_NOT_LOADED
+    r = run(2, ActionKind.LOAD, 0)
+    assert r.status == wire.ResultStatus.SUCCESS and r.device_duration > 0
+    for aid, b in ((3, 1), (4, 16), (5, 8)):
+        r = run(aid, ActionKind.INFER, 0, tuple(range(b)))
+        assert r.status == wire.ResultStatus.SUCCESS and 0 < r.device_duration < 5_000_000
+    assert run(6, ActionKind.INFER, 0, (1, 2, 3)).status == wire.ResultStatus.MALFORMED_ACTION
+    assert run(7, ActionKind.INFER, 0, (1,), lo=-2, hi=-1).status == \
+        wire.ResultStatus.REJECTED_TOO_LATE
+    assert run(8, ActionKind.UNLOAD, 0).status == wire.ResultStatus.SUCCESS
+    s.close()
+    t.join(timeout=30)
+    rows = open(tmp_path / "w.csv").read().splitlines()
+    assert len(rows) == 1 + 8

@@ -52,7 +52,10 @@ def test_sim_harness_with_b200_sim_worker_matches_reference(sloserve, monkeypatc
     assert abs(ours["goodput_rps"] - ref["goodput_rps"]) <= 0.01 * ref["goodput_rps"]
 
 
-def test_reference_controller_over_tcp(sloserve, tmp_path):
+@pytest.mark.parametrize("native", [False, True], ids=["python-net", "native-net"])
+def test_reference_controller_over_tcp(sloserve, tmp_path, native):
+    """native-net: the connection is served by cw_net_serve (csrc/net.cpp), which also runs
+    the sim engine's event loop in wall time."""
     harness, workload = sloserve
     import time
 
@@ -66,6 +69,7 @@ def test_reference_controller_over_tcp(sloserve, tmp_path):
     t = threading.Thread(target=server.serve, args=("127.0.0.1:0", catalog.parse(cat_text)),
                          kwargs=dict(pages_per_gpu=100, epoch_ns=epoch, mode="sim",
                                      worker_id=0, telemetry_path=str(tmp_path / "w.csv"),
+                                     native=native,
                                      on_ready=lambda p: (ports.append(p), ready.set())),
                          daemon=True)
     t.start()
@@ -80,3 +84,5 @@ def test_reference_controller_over_tcp(sloserve, tmp_path):
     assert s.satisfaction >= 0.9, s.to_dict()
     t.join(timeout=60)  # the reference harness drops its reader socket ~10 s after the run
     assert (tmp_path / "w.csv").exists()
+    rows = open(tmp_path / "w.csv").read().splitlines()
+    assert rows[0].startswith("action_id,kind") and len(rows) > 50
