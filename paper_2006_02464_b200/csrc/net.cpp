@@ -177,8 +177,8 @@ int cw_net_serve(cw_engine* e, int fd, const uint8_t* handshake, int64_t hs_len,
           std::lock_guard<std::mutex> g(sim_mu);
           cw_engine_sim_run(e, wall());
         }
-        k = cw_engine_poll(e, res.data(), (int)res.size(), 0);
-        if (k == 0) std::this_thread::sleep_for(std::chrono::microseconds(50));
+        // (woken at once by results the reader's own sim_run produced)
+        k = cw_engine_poll(e, res.data(), (int)res.size(), 50);
       } else {
         k = cw_engine_poll(e, res.data(), (int)res.size(), 20000);
       }
@@ -240,7 +240,9 @@ int cw_net_serve(cw_engine* e, int fd, const uint8_t* handshake, int64_t hs_len,
     int src;
     if (sim) {
       std::lock_guard<std::mutex> g(sim_mu);
-      src = cw_engine_submit(e, &a, wall());
+      const int64_t t = wall();
+      src = cw_engine_submit(e, &a, t);
+      cw_engine_sim_run(e, t);  // deliver now (the Python path runs on_action at once too)
     } else {
       src = cw_engine_submit(e, &a, 0);
     }
