@@ -5,6 +5,9 @@
         [--gpus N] [--pages N] [--clock wall] [--jitter none] [--seed N]
         [--epoch-ns N] [--telemetry FILE]
         [--worker-id N] [--devices 0,1,...] [--mode cuda|sim] [--weights-seed N]
+        [--native-net] [--weights DIR]
+    python -m paper_2006_02464_b200 pack --arch resnet50 (--state-dict SD.npz | --random-seed N)
+        --out resnet50.cwm
 """
 
 from __future__ import annotations
@@ -45,7 +48,19 @@ def main(argv=None) -> int:
     p.add_argument("--weights-seed", type=int, default=0)
     p.add_argument("--native-net", action="store_true",
                    help="serve the controller socket from native threads (csrc/net.cpp)")
+    p.add_argument("--weights", default="",
+                   help="directory of <arch>.cwm model artifacts (default: random-init weights)")
+    k = sub.add_parser("pack", help="fold + pack a torchvision-named state dict (.npz) into a "
+                                    ".cwm model artifact")
+    k.add_argument("--arch", required=True)
+    k.add_argument("--state-dict", default="", help=".npz of named arrays (torchvision naming)")
+    k.add_argument("--random-seed", type=int, default=None,
+                   help="pack random-init weights instead (make_params seed)")
+    k.add_argument("--page-bytes", type=int, default=16 * 1024 * 1024)
+    k.add_argument("--out", required=True)
     args = ap.parse_args(argv)
+    if args.cmd == "pack":
+        return _pack(args)
     if args.clock == "sim":
         print("worker: simulated clock mode only makes sense in-process", file=sys.stderr)
         return 2
@@ -55,7 +70,26 @@ def main(argv=None) -> int:
                  telemetry_path=args.telemetry,
                  ready_fd=args.ready_fd if args.ready_fd >= 0 else None,
                  worker_id=args.worker_id, devices=devices, mode=args.mode,
-                 weights_seed=args.weights_seed, native=args.native_net)
+                 weights_seed=args.weights_seed, native=args.native_net,
+                 weights_dir=args.weights or None)
+    return 0
+
+
+def _pack(args) -> int:
+    import numpy as np
+
+    from . import arch, artifact
+    if args.state_dict:
+        with np.load(args.state_dict) as z:
+            sd = {k: z[k] for k in z.files}
+    elif args.random_seed is not None:
+        sd = arch.make_params(arch.build_arch(args.arch), seed=args.random_seed)
+    else:
+        print("pack: --state-dict or --random-seed is required", file=sys.stderr)
+        return 2
+    blob = artifact.from_state_dict(args.arch, sd, page_bytes=args.page_bytes)
+    artifact.save(args.out, args.arch, blob)
+    print(f"{args.out}: {args.arch}, {blob.pages} pages of {blob.page_bytes} B")
     return 0
 
 

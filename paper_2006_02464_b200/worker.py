@@ -24,6 +24,7 @@ modes
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 import time
 from dataclasses import dataclass
@@ -180,7 +181,8 @@ class B200Worker:
                  io_capacity: int = DEFAULT_IO_CAPACITY, jitter=None, seed: int = 0,
                  keep_records: bool = True, *, mode: str = "cuda", devices=None,
                  weights_seed: int = 0, input_pool: int = 64, epoch_ns: int | None = None,
-                 keep_outputs: bool = False, poll_results: bool = True):
+                 keep_outputs: bool = False, poll_results: bool = True,
+                 weights_dir: str | None = None):
         if mode not in ("cuda", "sim"):
             raise ValueError(f"mode must be 'cuda' or 'sim', not {mode!r}")
         if jitter is not None and getattr(jitter, "kind", "none") != "none" and \
@@ -229,6 +231,14 @@ class B200Worker:
         if mode == "cuda":
             blobs = {}
             for base, spec in specs.items():
+                if weights_dir:  # model artifacts (artifact.py): <dir>/<arch>.cwm
+                    from . import artifact
+                    name, blob = artifact.load(os.path.join(weights_dir, f"{base}.cwm"))
+                    if name != base or blob.page_bytes != cat.page_bytes:
+                        raise CwError(f"{base}.cwm: arch {name}, page_bytes {blob.page_bytes} "
+                                      f"(catalog: {base}, {cat.page_bytes})")
+                    blobs[base] = blob
+                    continue
                 params = arch_mod.make_params(spec, seed=weights_seed)
                 blobs[base] = arch_mod.pack_blob(spec, arch_mod.fold(spec, params),
                                                  page_bytes=cat.page_bytes)

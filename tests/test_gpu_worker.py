@@ -195,3 +195,29 @@ def test_native_net_server_cuda(gpu, tmp_path):
     t.join(timeout=30)
     rows = open(tmp_path / "w.csv").read().splitlines()
     assert len(rows) == 1 + 8
+
+
+def test_worker_serves_model_artifact(gpu, tmp_path):
+    """Weights from a .cwm model artifact (artifact.py) instead of the built-in random init:
+    the served logits are the oracle's for the artifact's parameters."""
+    from paper_2006_02464_b200 import artifact
+
+    spec = arch.build_arch("resnet50")
+    params = arch.make_params(spec, seed=7)
+    artifact.save(str(tmp_path / "resnet50.cwm"), "resnet50",
+                  artifact.from_state_dict("resnet50", params))
+    col = Collector()
+    w = B200Worker(0, catalog.parse(CAT), None, col, pages_per_gpu=16, mode="cuda",
+                   devices=[gpu], epoch_ns=time.time_ns(), keep_outputs=True,
+                   weights_dir=str(tmp_path))
+    try:
+        assert int(act(w, col, 1, ActionKind.LOAD, 0).status) == 1
+        assert int(act(w, col, 2, ActionKind.INFER, 0, range(8, 12)).status) == 1
+        time.sleep(0.05)
+        got = w.outputs[2]
+    finally:
+        w.close()
+    ref = resnet_oracle.logits(resnet_oracle.torchvision_model("resnet50", params),
+                               arch.make_inputs(4, spec, first=8))
+    c = resnet_oracle.compare(got, ref)
+    assert c["ok"], c
