@@ -659,7 +659,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
     // k-blocks per slot: 2 halves the per-k-block barrier / issue work of the producer and
     // MMA warps when the ring still holds >= 2 slots per producer
     int kpack = 2;
-    if (kpack_env > 0) kpack = std::min(kpack_env, 2);  // 3 broke b=1 parity: not supported
+    if (kpack_env > 0) kpack = std::min(kpack_env, 2);  // the MMA loop issues <= 2 per slot
     if ((int)(p.ring_bytes / (kpack * d.sub_bytes)) < min_slots) kpack = 1;
     d.kpack = kpack;
     d.slot_bytes = kpack * d.sub_bytes;
