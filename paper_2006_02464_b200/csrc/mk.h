@@ -121,6 +121,7 @@ struct MkArgs {
   // ready (producer), 2 first accumulator ready (epilogue), 3 first tile landed (MMA)
   uint64_t* trace;
   uint32_t flags;            // experiments only (CW_MK_FLAGS): 1 no MMA, 2 no A loads, 4 no B loads
+  int32_t pf_depth;          // weight layers L2-prefetched ahead of the running conv
 };
 
 }  // namespace cw

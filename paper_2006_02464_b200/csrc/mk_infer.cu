@@ -797,19 +797,24 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         {
           // the NEXT conv's weights into L2 (they stream from HBM: every INFER may run another
           // model copy), a 1/G slice per CTA: its first B tiles then hit L2, not HBM latency
-          int Ln = L + 1;
-          while (Ln < nl && sl[Ln].kind != MK_CONV && sl[Ln].kind != MK_FC) ++Ln;
-          if (Ln < nl && (sl[Ln].kind == MK_FC || sl[Ln].mode != 2) && elect_one()) {
-            const MkLayer& dn = sl[Ln];
-            const uint8_t* w = reinterpret_cast<const uint8_t* const*>(hdr + kHdrWeightOff)[dn.wlayer];
-            const uint32_t bytes = dn.kind == MK_FC
-                                       ? (uint32_t)dn.classes * (uint32_t)dn.C * 2u
-                                       : (uint32_t)dn.n_out * (uint32_t)(dn.num_kb * dn.kblk) * 2u;
-            const uint32_t per = ((bytes + G - 1) / G + 255u) & ~255u;
-            const uint32_t off = (uint32_t)cta * per;
-            if (off < bytes) bulk_prefetch_l2(w + off, min(per, bytes - off));
+          int Ln = L;
+          for (int ahead = 0; ahead < args.pf_depth; ++ahead) {
+            ++Ln;
+            while (Ln < nl && sl[Ln].kind != MK_CONV && sl[Ln].kind != MK_FC) ++Ln;
+            if (Ln >= nl) break;
+            if ((sl[Ln].kind == MK_FC || sl[Ln].mode != 2) && elect_one()) {
+              const MkLayer& dn = sl[Ln];
+              const uint8_t* w =
+                  reinterpret_cast<const uint8_t* const*>(hdr + kHdrWeightOff)[dn.wlayer];
+              const uint32_t bytes = dn.kind == MK_FC
+                                         ? (uint32_t)dn.classes * (uint32_t)dn.C * 2u
+                                         : (uint32_t)dn.n_out * (uint32_t)(dn.num_kb * dn.kblk) * 2u;
+              const uint32_t per = ((bytes + G - 1) / G + 255u) & ~255u;
+              const uint32_t off = (uint32_t)cta * per;
+              if (off < bytes) bulk_prefetch_l2(w + off, min(per, bytes - off));
+            }
+            __syncwarp();
           }
-          __syncwarp();
         }
 #endif
         const MkLayer d = sl[L];  // registers: the asm memory clobbers would force re-loads

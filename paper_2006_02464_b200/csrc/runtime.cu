@@ -721,6 +721,9 @@ std::string Runtime::capture(Arch& a, Plan& p) {
   args.gen = p.d_gen;
   args.trace = p.d_trace;
   if (const char* e = getenv("CW_MK_FLAGS")) args.flags = (uint32_t)atoi(e);  // experiments only
+  // two weight layers ahead at b=1 (short layers: 277 -> 272 us), one at larger batches
+  // (two: b=2 +2.5 us, b=16 +3 us)
+  args.pf_depth = p.batch == 1 ? 2 : 1;
   CW_TRY(cudaStreamBeginCapture(s_cap_, cudaStreamCaptureModeThreadLocal));
   cudaError_t ce = copy_plan(p.d_layers, (int)p.layers.size(), s_cap_);
   launch_gate(ab_, ring_, kRing - 1, ctr_, exec_recs_, s_cap_);
