@@ -1511,7 +1511,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         if (args.trace && et == 0) args.trace[((size_t)L * G + cta) * 4 + 2] = globaltimer();
         named_bar(1, kMkEpiThreads);
         if (et == 0) {
-          if (d.kind == MK_REDUCE) red_after_bulk_add(counters + L, (uint32_t)done);
+          // reduce rows left by bulk copies; the FC's logits are read by nothing in this
+          // grid (mk_done and the output copies are ordered after its completion)
+          if (d.kind == MK_REDUCE || d.kind == MK_FC) red_after_bulk_add(counters + L, (uint32_t)done);
           else red_release_add(counters + L, (uint32_t)done);  // generic stores
         }
       }
