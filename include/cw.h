@@ -138,6 +138,11 @@ typedef struct cw_engine_config {
   const cw_model_info* models;
   int64_t io_slots;        /* cuda: physical IOCache slots per GPU */
   int64_t in_bytes_max, out_bytes_max;
+  /* cuda: the executor thread is pinned to this CPU (-1: not pinned) and, when
+   * executor_rt_prio > 0, run SCHED_FIFO at that priority if the process may
+   * ("executor threads ... pinned, real-time priority"). */
+  int32_t executor_cpu;
+  int32_t executor_rt_prio;
 } cw_engine_config;
 
 typedef struct cw_action {
@@ -172,13 +177,28 @@ int cw_engine_start(cw_engine* e);
 void cw_engine_close(cw_engine* e);
 /* Thread-safe. cuda: processed by the engine thread; sim: delivered at virtual time `at`. */
 int cw_engine_submit(cw_engine* e, const cw_action* a, int64_t at);
-/* Blocks up to timeout_us for >= 1 result; returns the number written (<= max). */
+/* Blocks up to timeout_us for >= 1 result; returns the number written (<= max), or -1 once
+ * the engine has failed (a CUDA error is fatal to the engine: it is never reported as a
+ * protocol status) and every result issued before the failure has been returned. */
 int cw_engine_poll(cw_engine* e, cw_result* out, int max, int64_t timeout_us);
+/* 1 if a device error stopped the engine (cw_last_error() holds the first error). */
+int cw_engine_failed(cw_engine* e);
+/* cuda: how the executor thread runs: *cpu = pinned CPU or -1, *rt = 1 if SCHED_FIFO. */
+int cw_engine_executor_info(cw_engine* e, int32_t* cpu, int32_t* rt);
 /* sim: run the virtual-time event loop until no event is left at or before `until`. */
 int cw_engine_sim_run(cw_engine* e, int64_t until);
 int64_t cw_engine_now(cw_engine* e);
 /* sim: virtual time of the next pending event, -1 if none. */
 int64_t cw_engine_next_time(cw_engine* e);
+/* sim, driven by the caller's event loop (the reference SimLoop, timebase.py:55-99):
+ *   cw_engine_sim_deliver   on_action at virtual time `now` (worker.py:198-219), at once;
+ *   cw_engine_sim_take_new  (time, seq) of every engine event scheduled since the last call:
+ *                           the caller schedules one loop callback per event, mirroring the
+ *                           reference's loop.call_at (worker.py:246, 265, 276, 296);
+ *   cw_engine_sim_run_to    that callback: run engine events up to (time, seq). */
+int cw_engine_sim_deliver(cw_engine* e, const cw_action* a, int64_t now);
+int cw_engine_sim_take_new(cw_engine* e, int64_t* times, uint64_t* seqs, int max);
+int cw_engine_sim_run_to(cw_engine* e, int64_t t, uint64_t seq);
 /* Page accounting of one GPU (PageCache, worker.py:63-99). resident: (model, pages) pairs. */
 int cw_engine_pages(cw_engine* e, int gpu_index, int64_t* pages_free, int32_t* resident_models,
                     int32_t* resident_pages, int max_resident, int32_t* n_resident);

@@ -46,7 +46,8 @@ class cw_engine_config(C.Structure):
         ("n_models", C.c_int32), ("pages_per_gpu", C.c_int64), ("page_bytes", C.c_int64),
         ("io_capacity", C.c_int64), ("epoch_ns", C.c_int64),
         ("devices", C.POINTER(C.c_int32)), ("models", C.POINTER(cw_model_info)),
-        ("io_slots", C.c_int64), ("in_bytes_max", C.c_int64), ("out_bytes_max", C.c_int64)]
+        ("io_slots", C.c_int64), ("in_bytes_max", C.c_int64), ("out_bytes_max", C.c_int64),
+        ("executor_cpu", C.c_int32), ("executor_rt_prio", C.c_int32)]
 
 
 class cw_action(C.Structure):
@@ -108,6 +109,11 @@ SIGNATURES = [
     ("cw_engine_sim_run", C.c_int, [_P, C.c_int64]),
     ("cw_engine_now", C.c_int64, [_P]),
     ("cw_engine_next_time", C.c_int64, [_P]),
+    ("cw_engine_failed", C.c_int, [_P]),
+    ("cw_engine_executor_info", C.c_int, [_P, _I32P, _I32P]),
+    ("cw_engine_sim_deliver", C.c_int, [_P, C.POINTER(cw_action), C.c_int64]),
+    ("cw_engine_sim_take_new", C.c_int, [_P, _I64P, C.POINTER(C.c_uint64), C.c_int]),
+    ("cw_engine_sim_run_to", C.c_int, [_P, C.c_int64, C.c_uint64]),
     ("cw_engine_pages", C.c_int, [_P, C.c_int, _I64P, _I32P, _I32P, C.c_int, _I32P]),
     ("cw_engine_io_in_use", C.c_int64, [_P, C.c_int]),
     ("cw_engine_output", C.c_int, [_P, C.c_int, C.c_int64, _P, C.c_int, C.c_int]),

@@ -19,11 +19,16 @@ from concurrent.futures import ThreadPoolExecutor
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 REPO = os.path.dirname(PKG)
-# experiments only: CW_BUILD_TAG=x CW_NVCC_DEFS="-DFOO=1" builds libcw_x.so from build/obj_x
+# experiments only: CW_BUILD_TAG=x CW_NVCC_DEFS="-DCW_EXPERIMENTS ..." builds libcw_x.so
 _TAG = os.environ.get("CW_BUILD_TAG", "")
 LIB = os.path.join(PKG, f"libcw_{_TAG}.so" if _TAG else "libcw.so")
 OBJ = os.path.join(REPO, "build", f"obj_{_TAG}" if _TAG else "obj")
 DEFS = os.environ.get("CW_NVCC_DEFS", "").split() if _TAG else []
+# Variant built next to libcw.so by every build(): the megakernel with every layer published
+# by red.release (no relaxed-publication hardware assumption), for the parity test
+# tests/test_gpu_strict_release.py (loaded with CW_LIB=libcw_strict.so).
+STRICT_LIB = os.path.join(PKG, "libcw_strict.so")
+STRICT_OBJ = os.path.join(REPO, "build", "obj_strict")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -45,19 +50,20 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src: str, force: bool) -> str:
+def _compile(src: str, force: bool, obj_dir: str = OBJ, defs=None) -> str:
+    defs = DEFS if defs is None else defs
     path = os.path.join(CSRC, src)
-    obj = os.path.join(OBJ, src + ".o")
+    obj = os.path.join(obj_dir, src + ".o")
     if force or _stale(obj, [path] + _headers()):
         lang = [] if src.endswith(".cu") else ["-x", "cu"]
-        cmd = [NVCC, *ARCH, *COMMON, *DEFS, *lang, "-c", path, "-o", obj]
+        cmd = [NVCC, *ARCH, *COMMON, *defs, *lang, "-c", path, "-o", obj]
         if src == "mk_infer.cu":
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
         if src == "mk_infer.cu":
-            with open(os.path.join(OBJ, "mk_infer.ptxas.txt"), "w") as f:
+            with open(os.path.join(obj_dir, "mk_infer.ptxas.txt"), "w") as f:
                 f.write(r.stderr)
             _check_megakernel_spills(r.stderr)
     return obj
@@ -75,19 +81,26 @@ def _check_megakernel_spills(ptxas: str) -> None:
                 print(f"WARNING: megakernel spills: {nxt.strip()}", file=sys.stderr)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def _variant(lib: str, obj_dir: str, defs, force: bool) -> str:
+    os.makedirs(obj_dir, exist_ok=True)
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force), SOURCES))
-    if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB + ".tmp", *objs,
+        objs = list(ex.map(lambda s: _compile(s, force, obj_dir, defs), SOURCES))
+    if force or _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib + ".tmp", *objs,
                "-lpthread", "-lrt", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-        os.replace(LIB + ".tmp", LIB)
+        os.replace(lib + ".tmp", lib)
+    return lib
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    _variant(LIB, OBJ, DEFS, force)
+    if not _TAG:
+        _variant(STRICT_LIB, STRICT_OBJ, ["-DCW_STRICT_RELEASE"], force)
     if verbose:
-        print(f"built {LIB}")
+        print(f"built {LIB}" + ("" if _TAG else f" and {STRICT_LIB}"))
     return LIB
 
 

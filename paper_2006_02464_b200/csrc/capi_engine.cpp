@@ -32,10 +32,28 @@ int cw_engine_submit(cw_engine* e, const cw_action* a, int64_t at) {
 }
 
 int cw_engine_poll(cw_engine* e, cw_result* out, int max, int64_t timeout_us) {
-  return e->e.poll(out, max, timeout_us);
+  return e->e.poll(out, max, timeout_us);  // -1: the engine failed (cw_last_error says why)
 }
 
 int cw_engine_sim_run(cw_engine* e, int64_t until) { return e->e.sim_run(until); }
+
+int cw_engine_sim_deliver(cw_engine* e, const cw_action* a, int64_t now) {
+  if (a->batch_size < 0) return cw::fail("negative batch size");
+  return e->e.sim_deliver(*a, now) == 0 ? 0 : cw::fail("sim_deliver: not a sim engine");
+}
+
+int cw_engine_sim_run_to(cw_engine* e, int64_t t, uint64_t seq) { return e->e.sim_run_to(t, seq); }
+
+int cw_engine_sim_take_new(cw_engine* e, int64_t* times, uint64_t* seqs, int max) {
+  return e->e.sim_take_new(times, seqs, max);
+}
+
+int cw_engine_failed(cw_engine* e) { return e->e.failed() ? 1 : 0; }
+
+int cw_engine_executor_info(cw_engine* e, int32_t* cpu, int32_t* rt) {
+  e->e.executor_info(cpu, rt);
+  return 0;
+}
 
 int64_t cw_engine_now(cw_engine* e) { return e->e.now(); }
 

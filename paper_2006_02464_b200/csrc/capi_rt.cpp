@@ -7,6 +7,7 @@
 
 #include "../../include/cw.h"
 #include "capi_util.h"
+#include "experiments.h"
 #include "runtime.h"
 
 using cw::Runtime;
@@ -134,7 +135,7 @@ int cw_rt_exec_many(cw_runtime* rt, int arch_id, int batch, const int32_t* hdr_p
   // The exec records live in a ring of kRing entries: harvest each INFER's record once it is
   // done and before its slot is reused (at most kRing / 2 INFERs in flight).
   int harvested = 0;
-  const int part = getenv("CW_EXEC_PART") ? atoi(getenv("CW_EXEC_PART")) : 0;
+  const int part = cw::exp_env("CW_EXEC_PART") ? atoi(cw::exp_env("CW_EXEC_PART")) : 0;
   auto harvest = [&](int upto) {
     for (; harvested < upto; ++harvested) {
       cw::ExecRecord* rec = r.exec_record(seqs[harvested]);

@@ -5,6 +5,9 @@
 #include <cstring>
 #include <ctime>
 
+#include <pthread.h>
+#include <sched.h>
+
 namespace cw {
 
 static int64_t realtime_ns() {
@@ -66,6 +69,19 @@ std::string Engine::start() {
     }
     stop_ = false;
     thread_ = std::thread([this] { run_loop(); });
+    // executor threads pinned to a core, at real-time priority when allowed
+    if (cfg_.executor_cpu >= 0) {
+      cpu_set_t set;
+      CPU_ZERO(&set);
+      CPU_SET(cfg_.executor_cpu, &set);
+      if (pthread_setaffinity_np(thread_.native_handle(), sizeof(set), &set) == 0)
+        exec_cpu_ = cfg_.executor_cpu;
+    }
+    if (cfg_.executor_rt_prio > 0) {
+      sched_param sp{};
+      sp.sched_priority = cfg_.executor_rt_prio;
+      if (pthread_setschedparam(thread_.native_handle(), SCHED_FIFO, &sp) == 0) exec_rt_ = 1;
+    }
   }
   started_ = true;
   return "";
@@ -107,11 +123,13 @@ void Engine::call_at(int64_t t, Event ev) {
   ev.t = t < n ? n : t;
   ev.seq = ++ev_seq_;
   timers_.push(ev);
+  if (cfg_.mode == 0 && ev.type != EV_DELIVER) sim_new_.emplace_back(ev.t, ev.seq);
 }
 
 // ------------------------------------------------------------------ API
 
 int Engine::submit(const cw_action& a, int64_t at) {
+  if (failed_) return fail("engine failed after a device error; see the first error");
   if (cfg_.mode == 0) {
     auto* copy = new cw_action(a);
     Event ev{};
@@ -129,12 +147,53 @@ int Engine::submit(const cw_action& a, int64_t at) {
 
 int Engine::poll(cw_result* out, int max, int64_t timeout_us) {
   std::unique_lock<std::mutex> lk(out_mu_);
-  if (outbox_.empty() && timeout_us > 0)
-    out_cv_.wait_for(lk, std::chrono::microseconds(timeout_us), [&] { return !outbox_.empty(); });
+  if (outbox_.empty() && timeout_us > 0 && !failed_)
+    out_cv_.wait_for(lk, std::chrono::microseconds(timeout_us),
+                     [&] { return !outbox_.empty() || failed_; });
+  if (outbox_.empty() && failed_) return -1;
   int n = 0;
   while (n < max && !outbox_.empty()) {
     out[n++] = outbox_.front();
     outbox_.pop_front();
+  }
+  return n;
+}
+
+int Engine::sim_deliver(const cw_action& a, int64_t now) {
+  if (cfg_.mode != 0) return -1;
+  sim_now_ = std::max(sim_now_, now);
+  on_action(new cw_action(a));
+  return 0;
+}
+
+int Engine::sim_run_to(int64_t t, uint64_t seq) {
+  if (cfg_.mode != 0) return -1;
+  int n = 0;
+  while (!timers_.empty()) {
+    const Event& top = timers_.top();
+    if (top.t > t || (top.t == t && top.seq > seq)) break;
+    Event ev = top;
+    timers_.pop();
+    sim_now_ = std::max(sim_now_, ev.t);
+    ++n;
+    switch (ev.type) {
+      case EV_DELIVER: on_action(ev.a); break;
+      case EV_WAKE: wake(ev.gpu, ev.infer_exec); break;
+      case EV_LOAD_DONE: load_done(ev.gpu, ev.a, ev.started, sim_now_, ev.dur); break;
+      case EV_EXEC_DONE: exec_done(ev.gpu, ev.a, ev.started, ev.dur); break;
+      case EV_OUTPUT_DONE: output_done(ev.gpu, ev.a, ev.started, sim_now_, ev.dur); break;
+    }
+  }
+  return n;
+}
+
+int Engine::sim_take_new(int64_t* times, uint64_t* seqs, int max) {
+  int n = 0;
+  while (n < max && !sim_new_.empty()) {
+    times[n] = sim_new_.front().first;
+    seqs[n] = sim_new_.front().second;
+    sim_new_.pop_front();
+    ++n;
   }
   return n;
 }
@@ -461,10 +520,22 @@ bool Engine::device_input(int g, cw_action* a) {
   const int arch = models_[a->model_id].arch_id;
   std::string err = gpu.rt->rt.input_async(arch, slots.data(), a->request_ids, a->batch_size, 0,
                                            nullptr);
-  if (!err.empty()) set_error("input: " + err);
   gpu.action_input_seq[a->action_id] = gpu.rt->rt.last_input_seq();
   gpu.action_slots[a->action_id] = std::move(slots);
+  if (!err.empty()) {
+    fail_device("input: " + err);
+    return false;
+  }
   return true;
+}
+
+void Engine::fail_device(const std::string& what) {
+  set_error("engine failed (device error, no further actions run): " + what);
+  {
+    std::lock_guard<std::mutex> lk(out_mu_);
+    failed_ = true;
+  }
+  out_cv_.notify_all();
 }
 
 void Engine::device_release_slots(int g, cw_action* a) {
@@ -488,21 +559,14 @@ void Engine::device_load(int g, cw_action* a, int64_t now) {
     gpu.free_pages.pop_back();
     fence = std::max(fence, gpu.page_fence[pages[i]]);
   }
-  // Page-reuse fence: a copy must not overwrite pages an in-flight Exec still reads.
-  if (fence >= 0 && rt.exec_record((uint64_t)fence)->seq_done == (uint64_t)fence + 1) fence = -1;
+  // Page-reuse fence: a copy must not overwrite pages an in-flight Exec still reads
+  // (Runtime::load_async waits on the device only if that Exec has not completed).
   const uint64_t tag = ++load_tag_;
   LoadRecord* rec = nullptr;
   std::string err = rt.load_async(mi.blob_id, pages.data(), n, fence, tag, &rec);
   gpu.model_pages[a->model_id] = std::move(pages);
   if (!err.empty()) {
-    set_error("load: " + err);
-    // Surface as a failed copy: free the reservation like an aborted load.
-    for (int32_t p : gpu.model_pages[a->model_id]) gpu.free_pages.push_back(p);
-    gpu.model_pages.erase(a->model_id);
-    gpu.pages.in_transit.erase(a->model_id);
-    gpu.pages.free += mi.pages_needed;
-    gpu.load_exec.busy = false;
-    finish(a, OUT_OF_PAGES, now, now, 0);
+    fail_device("load: " + err);
     return;
   }
   gpu.loads.push_back({a, rec, tag, now});
@@ -534,10 +598,7 @@ void Engine::device_exec(int g, cw_action* a, int64_t now) {
                                   slots.data(), epoch_to_gt(g, a->earliest),
                                   epoch_to_gt(g, a->latest), in_seq, &seq);
   if (!err.empty()) {
-    set_error("exec: " + err);
-    gpu.infer_exec.busy = false;
-    release_io(g, a);
-    finish(a, REJECTED_TOO_LATE, now, now, 0);
+    fail_device("exec: " + err);
     return;
   }
   gpu.model_last_exec[a->model_id] = (int64_t)seq;
@@ -581,7 +642,10 @@ bool Engine::poll_device() {
         const int arch = models_[a->model_id].arch_id;
         std::string err = rt.output_async(arch, e.seq, gpu.action_slots[a->action_id].data(),
                                           a->batch_size);
-        if (!err.empty()) set_error("output: " + err);
+        if (!err.empty()) {
+          fail_device("output: " + err);
+          return progressed;
+        }
         const int64_t started = e.started, dur = e.dur;
         exec_done(g, a, started, dur);  // may append to execs
         progressed = true;
@@ -611,7 +675,7 @@ bool Engine::poll_device() {
 void Engine::run_loop() {
   std::vector<cw_action> batch;
   int idle = 0;
-  while (!stop_) {
+  while (!stop_ && !failed_) {
     bool progressed = false;
     {
       std::lock_guard<std::mutex> lk(in_mu_);

@@ -150,6 +150,22 @@ class Engine {
   int64_t next_event_time() const { return timers_.empty() ? -1 : timers_.top().t; }
   int pages(int g, int64_t* free, int32_t* models, int32_t* counts, int max, int32_t* n);
   int64_t io_in_use(int g);
+  // A CUDA failure is fatal to the engine (never turned into a protocol status): the engine
+  // stops executing, poll() returns -1 once the results issued before it are drained.
+  bool failed() const { return failed_; }
+  void executor_info(int32_t* cpu, int32_t* rt) const {
+    *cpu = exec_cpu_;
+    *rt = exec_rt_;
+  }
+  // sim: deliver an action now (at virtual time `now` >= every processed event), ahead of
+  // engine events at the same time that the caller's loop has not run yet.
+  int sim_deliver(const cw_action& a, int64_t now);
+  // sim, driven by an external event loop: process events up to (t, seq) in (time, seq)
+  // order, and hand out the (t, seq) of every event scheduled since the last call so the
+  // caller schedules one loop callback per engine event, in the same order as the
+  // reference's loop.call_at calls (worker.py:246, 265, 276, 296).
+  int sim_run_to(int64_t t, uint64_t seq);
+  int sim_take_new(int64_t* times, uint64_t* seqs, int max);
   int output(int g, int64_t ref, float* dst, int batch, int classes);
 
  private:
@@ -167,6 +183,7 @@ class Engine {
               int64_t output_ref = -1);
   void input_started(int g, cw_action* a, int64_t now);
   // --- device hooks (cuda)
+  void fail_device(const std::string& what);
   bool device_input(int g, cw_action* a);
   void device_release_slots(int g, cw_action* a);
   void device_load(int g, cw_action* a, int64_t now);
@@ -190,6 +207,7 @@ class Engine {
   std::priority_queue<Event, std::vector<Event>, std::greater<Event>> timers_;
   uint64_t ev_seq_ = 0;
   int64_t sim_now_ = 0;
+  std::deque<std::pair<int64_t, uint64_t>> sim_new_;  // scheduled, not yet handed out
   uint64_t load_tag_ = 0;
   std::unordered_set<cw_action*> owned_;  // live actions (freed at finish)
 
@@ -202,6 +220,8 @@ class Engine {
   std::mutex state_mu_;
   std::thread thread_;
   volatile bool stop_ = false;
+  volatile bool failed_ = false;
+  int32_t exec_cpu_ = -1, exec_rt_ = 0;
   bool started_ = false;
 };
 

@@ -14,7 +14,7 @@ int mk_blocks_per_sm(uint32_t smem);
 cudaError_t copy_plan(const MkLayer* d_layers, int n, cudaStream_t st);  // -> constant bank
 cudaError_t launch_mk(const MkArgs& a, int grid, uint32_t smem, cudaStream_t st);
 void launch_mk_done(const ActionBlock* ab, uint32_t mask, ExecRecord* recs, uint32_t* gen,
-                    cudaStream_t st);
+                    volatile uint64_t* done, cudaStream_t st);
 
 void launch_gate(ActionBlock* ab, const ActionDesc* ring, uint32_t mask, uint64_t* ctr,
                  ExecRecord* recs, cudaStream_t st);

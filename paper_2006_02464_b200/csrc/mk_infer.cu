@@ -2,30 +2,41 @@
 // persistent launch (replaces the emulated Exec wait of the reference worker,
 // pkg/src/sloserve/worker.py:273-277 `dur = exec_duration[b]; call_at(now+dur)`).
 //
-// Grid = one CTA per SM (148 on B200), 192 threads, ~200 KB of shared memory.
-// Every CTA walks the plan (mk.h) layer by layer; the tasks of a layer are
-// dealt round-robin (rotated per layer) over the CTAs. Warp roles:
+// Grid = one CTA per SM (148 on B200), 384 threads (3 warpgroups), ~227 KB of
+// shared memory. Every CTA walks the plan (mk.h) layer by layer; the tasks of a
+// layer are dealt round-robin (rotated per layer) over the CTAs. Warp roles:
 //
-//   warp 0     TMA producer. For each of the CTA's conv tasks, per k-block: the
+//   warpgroup 0 (setmaxnreg 120)
+//     warp 0   TMA producer. For each of the CTA's conv tasks, per k-block: the
 //              weight tile (B, K-major, from the model's paged weights through
 //              the per-model tensor map in the model header) and the activation
 //              tile (A): mode 0 a [M][K] matrix box, mode 1 a tap-shifted NHWC
 //              box (implicit GEMM; padding = TMA out-of-bounds zero fill,
 //              stride = TMA element stride), mode 2 the stem's overlapping
-//              8-pixel row windows (K = 7 rows x 32). Weight tiles of a layer's
-//              first task are issued BEFORE waiting for the layer's inputs.
-//   warp 1     tcgen05.mma issuer (one thread): M=128, N=bn, K=16 steps, fp32
-//              accumulators in TMEM, two accumulator buffers so the epilogue of
-//              task i overlaps the MMAs of task i+1.
-//   warps 2-5  epilogue: tcgen05.ld 32 lanes x 32 columns, + bias (folded
-//              BatchNorm), + residual, ReLU, bf16 NHWC stores (or fp32 split-K
-//              partials, or the fused global average pool); and the SIMT
-//              layers (input conversion, max pool, avg pool, FC + logits).
+//              8-pixel row windows (one 5D box per task), mode 3 the 3x3/s1
+//              row box shared by the three horizontal taps. Weight tiles of a
+//              layer's first task are issued BEFORE waiting for the layer's inputs.
+//     warp 1   tcgen05.mma issuer (one elected thread): M=128, N=bn, K=16 steps,
+//              fp32 accumulators in TMEM, two 256-column accumulators so the
+//              epilogue of task i overlaps the MMAs of task i+1.
+//     warps 2-3 idle (their registers go to the epilogue).
+//   warpgroups 1-2 (setmaxnreg 192): eight epilogue warps, two per TMEM lane
+//              quarter (group g = columns [32g, 32g+32) of every 64-column
+//              chunk): tcgen05.ld -> + bias (folded BatchNorm), + residual,
+//              ReLU -> bf16 into a 128-byte-swizzled staging buffer -> TMA
+//              store; or fp32 split-K partials, or the fused global average
+//              pool. The same warps run the SIMT layers (input conversion, max
+//              pool, avg pool, split-K reduce, FC + logits).
 //
-// Layer completion: after a task's stores, one epilogue thread publishes
-// counter[L] += 1 with release semantics; consumers spin with acquire loads
-// (plus an async-proxy fence before TMA reads). Waits time out (trap) rather
+// Layer completion: after a layer's stores, one epilogue thread per CTA adds its
+// task count to counter[L]; consumers spin with relaxed loads, then one acquire
+// load (plus an async-proxy fence before TMA reads). Waits time out (trap) rather
 // than hang the GPU if the plan were ever inconsistent.
+//
+// Memory-model note (hardware assumption, see red_after_bulk_add): layers whose every
+// global write is a TMA / bulk store publish with a RELAXED add after
+// cp.async.bulk.wait_group 0 + fence.proxy.async; build with -DCW_STRICT_RELEASE to
+// publish every layer with red.release instead (tests/test_gpu_strict_release.py).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -65,8 +76,19 @@ __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
 // operation in flight on the SM (the producer's prefetch of the next layer): ~0.65 us
 // per layer boundary (b=1 324 -> 280 us, b=16 568 -> 533 us). Layers with generic
 // stores (SIMT layers, the fused average pool) keep red_release_add.
+//
+// HARDWARE ASSUMPTION (outside the PTX memory model): a relaxed RMW gives no
+// happens-before edge, so this relies on bulk-async writes that wait_group 0 reported
+// complete being visible at L2 to any later reader of the count, which holds on sm_100
+// (every consumer reads through TMA / L2 or behind its own acquire load; thousands of
+// alternating-input INFERs reproduce bit for bit, tools/handoff_stress.py). Builds with
+// -DCW_STRICT_RELEASE use red.release.gpu here (one MEMBAR per layer boundary, slower).
 __device__ __forceinline__ void red_after_bulk_add(uint32_t* p, uint32_t v) {
+#ifdef CW_STRICT_RELEASE
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#else
   asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#endif
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -941,7 +963,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           continue;
         }
         const uint32_t a_bytes = a_rows(d) * (uint32_t)d.kblk * 2u;
-#ifdef CW_MK_EXPERIMENTS
+#ifdef CW_EXPERIMENTS
         const bool no_a = args.flags & 2, no_b = args.flags & 4;
 #else
         constexpr bool no_a = false, no_b = false;
@@ -1188,7 +1210,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
             const uint64_t ad = adesc0 + slot * sdesc, bd = bdesc0 + slot * sdesc;
             const int m = min(kpack, n - i);
             if (elect_one()) {
-#ifdef CW_MK_EXPERIMENTS
+#ifdef CW_EXPERIMENTS
               if (!(args.flags & 1))
 #endif
               {
@@ -1549,7 +1571,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
 
 // Bumps the plan generation after a completed (non-skipped) INFER and stamps Exec end.
 __global__ void mk_done_kernel(const ActionBlock* ab, uint32_t ring_mask, ExecRecord* recs,
-                               uint32_t* gen) {
+                               uint32_t* gen, volatile uint64_t* done) {
   griddep_wait();  // the megakernel has completed
   const uint64_t i = ab->seq;
   if (!ab->skip) *gen += 1u;
@@ -1563,6 +1585,7 @@ __global__ void mk_done_kernel(const ActionBlock* ab, uint32_t ring_mask, ExecRe
   r->seq_started = i + 1;
   __threadfence_system();
   r->seq_done = i + 1;
+  *done = i + 1;  // monotonic: INFERs of a device run in order on one Exec stream
 }
 
 // ------------------------------------------------------------------ host side
@@ -1612,17 +1635,12 @@ static cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, uint32
 }
 
 cudaError_t launch_mk(const MkArgs& a, int grid, uint32_t smem, cudaStream_t st) {
-  if (getenv("CW_NO_PDL")) {
-    mk_infer_kernel<<<grid, kMkThreads, smem, st>>>(a);
-    return cudaGetLastError();
-  }
   return launch_pdl(mk_infer_kernel, dim3(grid), dim3(kMkThreads), smem, st, a);
 }
 
 void launch_mk_done(const ActionBlock* ab, uint32_t mask, ExecRecord* recs, uint32_t* gen,
-                    cudaStream_t st) {
-  if (getenv("CW_NO_PDL")) mk_done_kernel<<<1, 1, 0, st>>>(ab, mask, recs, gen);
-  else launch_pdl(mk_done_kernel, dim3(1), dim3(1), 0, st, ab, mask, recs, gen);
+                    volatile uint64_t* done, cudaStream_t st) {
+  launch_pdl(mk_done_kernel, dim3(1), dim3(1), 0, st, ab, mask, recs, gen, done);
 }
 
 }  // namespace cw

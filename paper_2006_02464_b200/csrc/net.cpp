@@ -164,7 +164,7 @@ int cw_net_serve(cw_engine* e, int fd, const uint8_t* handshake, int64_t hs_len,
   std::condition_variable cv;
   std::unordered_map<uint64_t, Info> inflight;  // action id -> telemetry fields
   int64_t pending = 0, actions = 0, nrec = 0;
-  std::atomic<bool> reading{true}, sock_ok{true};
+  std::atomic<bool> reading{true}, sock_ok{true}, engine_failed{false};
 
   // writer: engine results -> ActionResult frames (one send per poll batch)
   std::thread writer([&] {
@@ -181,6 +181,11 @@ int cw_net_serve(cw_engine* e, int fd, const uint8_t* handshake, int64_t hs_len,
         k = cw_engine_poll(e, res.data(), (int)res.size(), 50);
       } else {
         k = cw_engine_poll(e, res.data(), (int)res.size(), 20000);
+      }
+      if (k < 0) {  // a device error stopped the engine: drop the controller connection
+        engine_failed = true;
+        shutdown(fd, SHUT_RDWR);
+        break;
       }
       if (k > 0) {
         buf.clear();
@@ -241,8 +246,8 @@ int cw_net_serve(cw_engine* e, int fd, const uint8_t* handshake, int64_t hs_len,
     if (sim) {
       std::lock_guard<std::mutex> g(sim_mu);
       const int64_t t = wall();
-      src = cw_engine_submit(e, &a, t);
-      cw_engine_sim_run(e, t);  // deliver now (the Python path runs on_action at once too)
+      src = cw_engine_sim_deliver(e, &a, t);  // on_action at once, as the Python path does
+      cw_engine_sim_run(e, t);
     } else {
       src = cw_engine_submit(e, &a, 0);
     }
@@ -261,6 +266,7 @@ int cw_net_serve(cw_engine* e, int fd, const uint8_t* handshake, int64_t hs_len,
   writer.join();
   if (n_recs) *n_recs = nrec;
   if (n_actions) *n_actions = actions;
+  if (engine_failed) return -1;  // cw_last_error() holds the engine's device error
   return rc == 0 ? 0 : cw::fail("cw_net_serve: engine submit failed");
 }
 

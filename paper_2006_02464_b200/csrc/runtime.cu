@@ -5,9 +5,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <ctime>
+#include <mutex>
 #include <thread>
 #include <vector>
 
+#include "experiments.h"
 #include "kernels.h"
 #include "tmap.h"
 
@@ -19,6 +21,38 @@ namespace cw {
     if (_e != cudaSuccess)                                                            \
       return std::string(#expr) + ": " + cudaGetErrorString(_e);                      \
   } while (0)
+
+// One Exec stream per device for every Runtime of the process: the megakernel's plan
+// lives in a process-wide __constant__ bank (copied by the head node of each INFER
+// graph) and its persistent grid assumes it owns the SMs, so INFERs of two runtimes on
+// one device must never overlap. Sharing the stream serialises them.
+namespace {
+std::mutex g_exec_mu;
+std::map<int, std::pair<cudaStream_t, int>> g_exec_streams;  // device -> (stream, users)
+
+cudaError_t acquire_exec_stream(int device, cudaStream_t* out) {
+  std::lock_guard<std::mutex> lk(g_exec_mu);
+  auto it = g_exec_streams.find(device);
+  if (it != g_exec_streams.end()) {
+    ++it->second.second;
+    *out = it->second.first;
+    return cudaSuccess;
+  }
+  cudaError_t e = cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
+  if (e == cudaSuccess) g_exec_streams[device] = {*out, 1};
+  return e;
+}
+
+void release_exec_stream(int device) {
+  std::lock_guard<std::mutex> lk(g_exec_mu);
+  auto it = g_exec_streams.find(device);
+  if (it == g_exec_streams.end()) return;
+  if (--it->second.second == 0) {
+    cudaStreamDestroy(it->second.first);
+    g_exec_streams.erase(it);
+  }
+}
+}  // namespace
 
 static int64_t realtime_ns() {
   timespec ts;
@@ -52,13 +86,15 @@ Runtime::~Runtime() {
   cudaFree(ctr_);
   cudaFreeHost(ring_);
   cudaFreeHost(exec_recs_);
+  cudaFreeHost((void*)exec_done_);
   cudaFreeHost(load_recs_);
   cudaFreeHost(in_recs_);
   cudaFreeHost(out_host_);
   cudaFreeHost(hdr_stage_);
   cudaFreeHost(in_pool_);
-  for (auto s : {s_exec_, s_load_, s_io_, s_cap_, s_out_})
+  for (auto s : {s_load_, s_io_, s_cap_, s_out_})
     if (s) cudaStreamDestroy(s);
+  if (s_exec_) release_exec_stream(device_);
 }
 
 std::string Runtime::open(int device, int64_t pages_total, int64_t page_bytes, int64_t io_slots,
@@ -83,14 +119,21 @@ std::string Runtime::open(int device, int64_t pages_total, int64_t page_bytes, i
   slot_bytes_ = in_bytes_max_ + out_bytes_max_;
   io_slots_ = io_slots;
   CW_TRY(cudaMalloc(&io_, (size_t)(io_slots * slot_bytes_)));
-  for (cudaStream_t* s : {&s_exec_, &s_load_, &s_io_, &s_cap_, &s_out_})
+  for (cudaStream_t* s : {&s_load_, &s_io_, &s_cap_, &s_out_})
     CW_TRY(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+  CW_TRY(acquire_exec_stream(device, &s_exec_));
   CW_TRY(cudaMalloc(&ab_, sizeof(ActionBlock)));
   CW_TRY(cudaMemset(ab_, 0, sizeof(ActionBlock)));
   CW_TRY(cudaMalloc(&ctr_, sizeof(uint64_t)));
   CW_TRY(cudaMemset(ctr_, 0, sizeof(uint64_t)));
   CW_TRY(cudaHostAlloc(&ring_, sizeof(ActionDesc) * kRing, cudaHostAllocMapped));
   CW_TRY(cudaHostAlloc(&exec_recs_, sizeof(ExecRecord) * kRing, cudaHostAllocMapped));
+  {
+    void* p = nullptr;
+    CW_TRY(cudaHostAlloc(&p, 64, cudaHostAllocMapped));
+    exec_done_ = static_cast<volatile uint64_t*>(p);
+    *exec_done_ = 0;
+  }
   CW_TRY(cudaHostAlloc(&load_recs_, sizeof(LoadRecord) * kRing, cudaHostAllocMapped));
   CW_TRY(cudaHostAlloc(&in_recs_, sizeof(StampRecord) * kRing, cudaHostAllocMapped));
   memset((void*)ring_, 0, sizeof(ActionDesc) * kRing);
@@ -268,7 +311,7 @@ static void box_dims(int nimg, int oh, int ow, int* bw, int* bh, int* bn) {
 static void plan_conv(MkLayer& d, int cout, int G, bool allow_split) {
   // a split layer adds a reduce layer and one more whole-GPU dependency (~6 us in the
   // network, measured with tools/sweep_bn.sh + op_profile; CW_SPLIT_US overrides)
-  static const double split_us = getenv("CW_SPLIT_US") ? atof(getenv("CW_SPLIT_US")) : 6.0;
+  static const double split_us = exp_env("CW_SPLIT_US") ? atof(exp_env("CW_SPLIT_US")) : 6.0;
   static const int kBn[3] = {256, 128, 64};
   const double rows = d.mode == 0 ? 128.0 : (double)(d.box_w * d.box_h * d.box_n);
   const double a_bytes = rows * d.kblk * 2;
@@ -301,11 +344,11 @@ static void plan_conv(MkLayer& d, int cout, int G, bool allow_split) {
     }
   }
   // experiment overrides (profiling only): CW_FORCE_BN, CW_FORCE_SPLIT
-  if (const char* e = getenv("CW_FORCE_BN")) {
+  if (const char* e = exp_env("CW_FORCE_BN")) {
     const int bn = atoi(e);
     if (bn > 0 && cout % bn == 0 && (d.mode != 2 || bn == 64)) best_bn = bn;
   }
-  if (const char* e = getenv("CW_FORCE_SPLIT")) {
+  if (const char* e = exp_env("CW_FORCE_SPLIT")) {
     const int sp = atoi(e);
     if (sp > 0 && allow_split && d.num_kb / sp >= 1) best_s = sp;
   }
@@ -460,7 +503,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
           if (!make_tmap_2d(&tm, in, (uint64_t)op.kpad, (uint64_t)d.m_total, 128))
             return "tensor map (2d) failed";
         } else if (!fuse_pool && op.kh == 3 && op.kw == 3 && op.stride == 1 && op.pad == 1 &&
-                   op.cin % 64 == 0 && op.out_w + 2 <= 128 && getenv("CW_NO_MODE3") == nullptr) {
+                   op.cin % 64 == 0 && op.out_w + 2 <= 128 && exp_env("CW_NO_MODE3") == nullptr) {
           // 3x3 / stride 1: tiles of full rows widened by the 2 padding columns, so the three
           // horizontal taps of a kernel row are ONE TMA box read at row shifts 0, 1, 2 (the
           // two extra columns per row are junk outputs, clipped by the store map)
@@ -627,8 +670,8 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
   p.ring_bytes = (cap - fixed) / 1024 * 1024;
   p.smem = mk_smem_bytes(p.ring_bytes, nl);
   int kpack_env = 0, min_slots = 2 * kMkProducers;  // experiment overrides (profiling only)
-  if (const char* e = getenv("CW_KPACK")) kpack_env = atoi(e);
-  if (const char* e = getenv("CW_KPACK_MINSLOTS")) min_slots = atoi(e);
+  if (const char* e = exp_env("CW_KPACK")) kpack_env = atoi(e);
+  if (const char* e = exp_env("CW_KPACK_MINSLOTS")) min_slots = atoi(e);
   for (auto& d : p.layers) {
     if (d.kind != MK_CONV) continue;
     if (d.mode == 2) {  // stem: one slot = the 7 kernel-row A sub-tiles (weights resident)
@@ -720,7 +763,7 @@ std::string Runtime::capture(Arch& a, Plan& p) {
   args.counters = p.d_counters;
   args.gen = p.d_gen;
   args.trace = p.d_trace;
-  if (const char* e = getenv("CW_MK_FLAGS")) args.flags = (uint32_t)atoi(e);  // experiments only
+  if (const char* e = exp_env("CW_MK_FLAGS")) args.flags = (uint32_t)atoi(e);  // experiments only
   // two weight layers ahead at b=1 (short layers: 277 -> 272 us), one at larger batches
   // (two: b=2 +2.5 us, b=16 +3 us)
   args.pf_depth = p.batch == 1 ? 2 : 1;
@@ -728,7 +771,7 @@ std::string Runtime::capture(Arch& a, Plan& p) {
   cudaError_t ce = copy_plan(p.d_layers, (int)p.layers.size(), s_cap_);
   launch_gate(ab_, ring_, kRing - 1, ctr_, exec_recs_, s_cap_);
   cudaError_t le = launch_mk(args, p.grid, p.smem, s_cap_);
-  launch_mk_done(ab_, kRing - 1, exec_recs_, p.d_gen, s_cap_);
+  launch_mk_done(ab_, kRing - 1, exec_recs_, p.d_gen, exec_done_, s_cap_);
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(s_cap_, &g);
   CW_TRY(ce);
@@ -805,7 +848,12 @@ std::string Runtime::load_async(int blob, const int32_t* pages, int npages, int6
     bias_tab[l] = reinterpret_cast<const float*>(addr(t.b_off));
     w_tab[l] = w;
   }
-  if (fence_seq >= 0) CW_TRY(cudaStreamWaitEvent(s_load_, exec_events_[fence_seq & (kRing - 1)], 0));
+  if (fence_seq >= 0 && exec_completed() <= (uint64_t)fence_seq) {
+    // Still in flight. INFERs complete in order on the Exec stream, so when the fence's
+    // event slot was re-recorded by a newer INFER (> kRing later) the newest event covers it.
+    const uint64_t s = exec_seq_ - (uint64_t)fence_seq <= kRing ? (uint64_t)fence_seq : exec_seq_ - 1;
+    CW_TRY(cudaStreamWaitEvent(s_load_, exec_events_[s & (kRing - 1)], 0));
+  }
   launch_stamp(&rec->t_start, tag, s_load_);
   for (int i = 0; i < b.npages; ++i) {
     const size_t off = (size_t)i * page_bytes_;
@@ -876,8 +924,8 @@ std::string Runtime::exec_async(int arch, int batch, int32_t hdr_page, const int
   std::atomic_thread_fence(std::memory_order_seq_cst);
   if (input_seq >= 0) CW_TRY(cudaStreamWaitEvent(s_exec_, in_events_[input_seq & (kRing - 1)], 0));
   CW_TRY(cudaGraphLaunch(pit->second.exec, s_exec_));
+  exec_seq_ = seq + 1;  // the gate consumed ring entry seq: host and device stay aligned
   CW_TRY(cudaEventRecord(exec_events_[seq & (kRing - 1)], s_exec_));
-  exec_seq_ = seq + 1;
   *seq_out = seq;
   return "";
 }

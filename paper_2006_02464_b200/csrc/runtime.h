@@ -118,7 +118,8 @@ class Runtime {
   int arch_of_blob(int blob) const;
 
   // ---- LOAD: copy blob `blob` into physical pages (async on the Load stream).
-  // Waits on infer event `fence_seq` first when >= 0 (page reuse fence).
+  // Page-reuse fence: when fence_seq >= 0 (the last INFER that read one of these pages)
+  // and that INFER has not completed, the copy first waits for it on the device.
   // The record slot is returned; completion when rec->tag_end == tag.
   std::string load_async(int blob, const int32_t* pages, int npages, int64_t fence_seq,
                          uint64_t tag, LoadRecord** rec);
@@ -140,6 +141,9 @@ class Runtime {
   int64_t last_input_seq() const { return last_input_seq_; }
   ExecRecord* exec_record(uint64_t seq) { return &exec_recs_[seq & (kRing - 1)]; }
   uint64_t exec_issued() const { return exec_seq_; }
+  // INFERs completed on the device (monotonic, written by mk_done): exec seq s is done
+  // iff exec_completed() > s, whatever the ring slot of s holds by now
+  uint64_t exec_completed() const { return *exec_done_; }
 
   // ---- Output stage: after exec `seq`, copy logits of the slots to pinned host
   // memory (out_ring entry seq) and stamp completion into the ExecRecord.
@@ -192,6 +196,7 @@ class Runtime {
   uint64_t* ctr_ = nullptr;     // device
   ActionDesc* ring_ = nullptr;  // mapped host
   ExecRecord* exec_recs_ = nullptr;  // mapped host
+  volatile uint64_t* exec_done_ = nullptr;  // mapped host: INFERs completed (mk_done)
   LoadRecord* load_recs_ = nullptr;  // mapped host
   StampRecord* in_recs_ = nullptr;   // mapped host
   float* out_host_ = nullptr;        // pinned host, kRing x kMaxBatch x out_floats

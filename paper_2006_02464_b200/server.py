@@ -17,7 +17,7 @@ import threading
 import time
 
 from . import wire
-from .timebase import WallClock, WallLoop
+from .timebase import WallClock
 from .worker import DEFAULT_IO_CAPACITY, B200Worker, WorkerActionRecord
 
 TELEMETRY_HEADER = ["action_id", "kind", "model_id", "gpu", "batch_size", "status", "start_ns",
@@ -25,7 +25,8 @@ TELEMETRY_HEADER = ["action_id", "kind", "model_id", "gpu", "batch_size", "statu
 
 
 class _EpochOnly:
-    """Loop stand-in for the cuda worker: it only needs the shared epoch."""
+    """Loop stand-in: the worker only needs the shared epoch (a cuda worker's executor runs
+    on the engine thread; a sim worker is driven in wall time from its engine's queue)."""
 
     def __init__(self, clock: WallClock):
         self.clock = clock
@@ -49,7 +50,7 @@ def serve(listen: str, catalog, gpu_count: int = 1, pages_per_gpu: int = 500, ji
     lsock.listen(1)
     bound = lsock.getsockname()[1]
     clock = WallClock(epoch_ns)
-    loop = _EpochOnly(clock) if mode == "cuda" else WallLoop(clock, name="worker").start()
+    loop = _EpochOnly(clock)
     wlock = threading.Lock()
     conn_box: dict = {}
     pending = {"n": 0}
@@ -96,10 +97,7 @@ def serve(listen: str, catalog, gpu_count: int = 1, pages_per_gpu: int = 500, ji
                 break
             with done:
                 pending["n"] += 1
-            if mode == "cuda":
-                worker.on_action(msg)
-            else:
-                loop.call_soon(worker.on_action, msg)
+            worker.on_action(msg)
     finally:
         deadline = time.monotonic() + 2.0
         with done:
@@ -109,8 +107,6 @@ def serve(listen: str, catalog, gpu_count: int = 1, pages_per_gpu: int = 500, ji
             conn_box["conn"] = None
         conn.close()
         lsock.close()
-        if mode != "cuda":
-            loop.stop(join=False)
         try:
             worker.close()
         finally:
@@ -130,7 +126,7 @@ def _serve_native(worker, conn, lsock, clock, loop, mode, telemetry_path) -> Non
     n_recs, n_act = C.c_int64(0), C.c_int64(0)
     try:
         if mode != "cuda":
-            loop.stop(join=True)  # the native loop drives the sim engine from here on
+            worker.detach_driver()  # the native loop drives the sim engine from here on
         check(lib.cw_net_serve(worker.engine.h, conn.fileno(), hs, len(hs), clock.epoch_ns, recs,
                                cap, C.byref(n_recs), C.byref(n_act)), "net_serve")
     finally:

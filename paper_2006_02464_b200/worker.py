@@ -109,10 +109,23 @@ class Engine:
         cfg.io_slots = io_slots
         cfg.in_bytes_max = in_bytes_max
         cfg.out_bytes_max = out_bytes_max
+        cfg.executor_cpu, cfg.executor_rt_prio = -1, 0
+        if mode == "cuda":  # one pinned (real-time if allowed) executor thread
+            cpus = sorted(os.sched_getaffinity(0))
+            first = (devices or [0])[0]
+            cfg.executor_cpu = cpus[(2 * first + 1) % len(cpus)] if len(cpus) > 1 else -1
+            cfg.executor_rt_prio = 10
         self.h = lib.cw_engine_open(C.byref(cfg))
         if not self.h:
             raise CwError(f"cw_engine_open: {lib.cw_last_error().decode()}")
         self._res = (cw_result * 256)()
+        self._new_t = (C.c_int64 * 64)()
+        self._new_s = (C.c_uint64 * 64)()
+
+    def executor_info(self) -> dict:
+        cpu, rt = C.c_int32(), C.c_int32()
+        lib.cw_engine_executor_info(self.h, C.byref(cpu), C.byref(rt))
+        return {"cpu": cpu.value, "sched_fifo": bool(rt.value)}
 
     def runtime(self, gpu: int) -> DeviceRuntime:
         h = lib.cw_engine_runtime(self.h, gpu)
@@ -128,7 +141,8 @@ class Engine:
             lib.cw_engine_close(self.h)
             self.h = None
 
-    def submit(self, action, at: int = 0):
+    @staticmethod
+    def _action(action) -> cw_action:
         a = cw_action()
         a.action_id = action.action_id
         a.kind = int(action.kind)
@@ -141,10 +155,32 @@ class Engine:
         a.earliest = action.earliest
         a.latest = action.latest
         a.expected_duration = getattr(action, "expected_duration", 0)
-        check(lib.cw_engine_submit(self.h, C.byref(a), at), "submit")
+        return a
+
+    def submit(self, action, at: int = 0):
+        check(lib.cw_engine_submit(self.h, C.byref(self._action(action)), at), "submit")
+
+    def sim_deliver(self, action, now: int):
+        check(lib.cw_engine_sim_deliver(self.h, C.byref(self._action(action)), now), "sim_deliver")
+
+    def sim_take_new(self) -> list[tuple[int, int]]:
+        out = []
+        while True:
+            n = lib.cw_engine_sim_take_new(self.h, self._new_t, self._new_s, len(self._new_t))
+            out += [(self._new_t[i], self._new_s[i]) for i in range(n)]
+            if n < len(self._new_t):
+                return out
+
+    def sim_run_to(self, t: int, seq: int) -> int:
+        return lib.cw_engine_sim_run_to(self.h, t, seq)
+
+    def failed(self) -> bool:
+        return bool(self.h) and lib.cw_engine_failed(self.h) == 1
 
     def poll(self, timeout_us: int = 0) -> list[tuple]:
         n = lib.cw_engine_poll(self.h, self._res, len(self._res), timeout_us)
+        if n < 0:
+            raise CwError(f"engine failed: {lib.cw_last_error().decode()}")
         return [(r.action_id, r.status, r.start, r.end, r.device_duration, r.output_ref,
                  r.pages_free, r.kind) for r in self._res[:n]]
 
@@ -170,6 +206,54 @@ class Engine:
         out = np.empty((batch, classes), np.float32)
         check(lib.cw_engine_output(self.h, gpu, ref, out.ctypes.data, batch, classes), "output")
         return out
+
+
+class _WallDriver:
+    """Runs a sim-mode engine in wall time when the caller supplies no event loop (the TCP
+    server): the engine's own timer queue is the schedule; one thread sleeps until the next
+    engine event is close, spins to it, runs the engine up to now and hands the results out
+    (outside the lock: send_result may block on a socket)."""
+
+    SPIN_NS = 150_000
+
+    def __init__(self, engine: Engine, now, deliver):
+        self.engine, self.now, self.deliver = engine, now, deliver
+        self.cv = threading.Condition()
+        self.stopped = False
+        self.thread = threading.Thread(target=self._run, name="b200-sim-wall", daemon=True)
+        self.thread.start()
+
+    def on_action(self, action):
+        with self.cv:
+            self.engine.sim_deliver(action, self.now())
+            self.engine.sim_take_new()
+            res = self.engine.poll(0)
+            self.cv.notify()
+        self.deliver(res)
+
+    def _run(self):
+        while True:
+            with self.cv:
+                if self.stopped:
+                    return
+                nt, now = self.engine.next_time(), self.now()
+                if nt < 0 or nt - now > self.SPIN_NS:
+                    self.cv.wait(0.05 if nt < 0 else (nt - now - self.SPIN_NS) / 1e9)
+                    continue
+            while self.now() < nt:
+                pass
+            with self.cv:
+                self.engine.sim_run(self.now())
+                self.engine.sim_take_new()
+                res = self.engine.poll(0)
+            self.deliver(res)
+
+    def stop(self):
+        with self.cv:
+            self.stopped = True
+            self.cv.notify()
+        if self.thread is not threading.current_thread():
+            self.thread.join(timeout=2.0)
 
 
 class B200Worker:
@@ -203,6 +287,8 @@ class B200Worker:
         self._actions: dict[int, tuple] = {}
         self._lock = threading.Lock()
         self._closed = False
+        self.failure: str | None = None
+        self._driver: _WallDriver | None = None
         cat = self.catalog
         specs = {}
         if mode == "cuda":
@@ -263,8 +349,9 @@ class B200Worker:
                                             daemon=True)
             if poll_results:
                 self._poller.start()
-        else:
-            self._scheduled = -1
+        elif not hasattr(loop, "call_at"):
+            # no event loop to schedule engine events on (server.py): run them in wall time
+            self._driver = _WallDriver(self.engine, loop.now, self._deliver)
 
     # -- protocol surface (worker.py:193-219)
     def handshake(self) -> WorkerHandshake:
@@ -276,30 +363,40 @@ class B200Worker:
             self._actions[action.action_id] = (int(action.kind), action.model_id,
                                                action.gpu_index, len(action.batch))
         if self.mode == "cuda":
+            if self.failure is not None:
+                raise CwError(f"worker stopped after a device error: {self.failure}")
             self.engine.submit(action)
             return
-        now = self.loop.now()
-        self.engine.submit(action, at=now)
-        self._advance()
+        if self._driver is not None:
+            self._driver.on_action(action)
+            return
+        self.engine.sim_deliver(action, self.loop.now())
+        self._after_engine()
 
-    # -- sim mode: engine events interleaved with the caller's SimLoop
-    def _advance(self):
-        self.engine.sim_run(self.loop.now())
+    def detach_driver(self):
+        """Stop the wall-time driver: a native loop (csrc/net.cpp) drives the engine now."""
+        if self._driver is not None:
+            self._driver.stop()
+
+    # -- sim mode: every engine event gets its own callback on the caller's loop, scheduled
+    # when the engine schedules it (the reference's loop.call_at order, worker.py:246-296)
+    def _after_engine(self):
         self._deliver(self.engine.poll(0))
-        nt = self.engine.next_time()
-        if nt >= 0 and nt != self._scheduled:
-            self._scheduled = nt
-            self.loop.call_at(nt, self._advance_at, nt)
+        for t, seq in self.engine.sim_take_new():
+            self.loop.call_at(t, self._run_event, t, seq)
 
-    def _advance_at(self, t):
-        if self._scheduled == t:
-            self._scheduled = -1
-        self._advance()
+    def _run_event(self, t, seq):
+        self.engine.sim_run_to(t, seq)
+        self._after_engine()
 
     # -- cuda mode: results arrive on the engine thread
     def _poll_loop(self):
         while not self._closed:
-            res = self.engine.poll(20_000)
+            try:
+                res = self.engine.poll(20_000)
+            except CwError as exc:     # a device error stopped the engine: no more results
+                self.failure = str(exc)
+                return
             if res:
                 self._deliver(res)
 
@@ -319,6 +416,8 @@ class B200Worker:
 
     def close(self):
         self._closed = True
+        if self._driver is not None:
+            self._driver.stop()
         if self.mode == "cuda" and self._poller.is_alive():
             self._poller.join(timeout=1.0)
         self.engine.close()
