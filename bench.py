@@ -1,30 +1,40 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 Clockwork worker (BASELINE.json configs[1]):
+"""Benchmark of the B200 Clockwork worker (BASELINE.json: goodput req/s within a 100 ms SLO;
+INFER images/s and p99.99/p50 per batch size).
 
-  single B200 worker, LOAD / INFER / UNLOAD over 1000 ResNet-50 copies in the
-  16 MiB-paged weight cache (cold-start heavy), 100 ms SLO.
+One line of JSON from rank 0. Its legs:
 
-One step = one INFER action of batch 16 (16 requests) on the copy the step's
-seeded schedule picks (uniform over the 1000 copies).
+  value      configs[0] at b = --batch (16): INFER throughput of the device path with the
+             request inputs already in the IOCache and the weights of all --copies (1000)
+             ResNet-50 copies resident in distinct HBM pages, one copy per step from a seeded
+             uniform schedule (so every step streams its copy's 51 MB from HBM: far larger
+             than L2). K timed steps = K INFER graphs (gate -> megakernel -> done) back to
+             back on the Exec stream, CUDA-event time, max over ranks. A request counts if its
+             Exec time is within the SLO (all are). No LOAD in this leg.
+  infer      configs[0] sweep, b = 1..16: img/s (pipelined launches) and the Exec-time spread
+             (device %globaltimer) over --sweep-samples INFERs per batch, plus the
+             host-observed span of --host-samples closed-loop INFERs.
+  e2e        configs[2] at N GPUs, the headline: the UNMODIFIED reference controller
+             (sloserve from baseline/_ref: Scheduler, ClientManager, summarize) replays a
+             synthetic MAF-style trace (workload.gen_synthetic_trace) over the 1000 copies at
+             --e2e-rate req/s per GPU for --e2e-seconds of wall clock against one B200 worker
+             process per GPU over TCP (the public API: `python -m paper_2006_02464_b200
+             worker --native-net`). Every INFER copies its requests' inputs H2D (pinned) and
+             their logits D2H; cold models are LOADed (paged pinned H2D). Goodput as the
+             reference's summarize computes it.
+  cold_start configs[1]: the same controller and worker with only --cold-pages pages (71
+             copies of 7 pages fit) and open-loop arrivals spread uniformly over all 1000
+             copies: LOAD / UNLOAD on almost every request.
+  roofline   the INFER megakernel at --batch: algorithmic FLOPs per launch / the measured
+             launch time vs the measured bf16 peak; DRAM traffic from the committed ncu capture.
+  cpu_baseline  the fp32 CPU oracle (oracle/resnet_oracle.py, torchvision ResNet-50) on all
+             host cores, ~15 s sample, rank 0 only.
 
-  value  device-resident leg: the per-(arch, batch) CUDA graph replayed back to
-         back on the Exec stream, weights of all 1000 copies resident in
-         distinct HBM pages (so every step streams its copy's weights from HBM),
-         request inputs already in the IOCache; CUDA-event time on the Exec
-         stream; closed loop (one batch in flight), every step's requests are
-         within the SLO if its Exec time is <= 100 ms.
-  e2e    the same workload through the worker's public API
-         (B200Worker.on_action, the drop-in for the reference EmulatedWorker):
-         pages_per_gpu=500 so only 125 copies fit; a cold copy costs an UNLOAD
-         of the LRU victim and a LOAD (pinned H2D of the 54 MB paged blob);
-         every INFER copies its 16 inputs H2D (pinned) and its logits D2H.
-         Goodput = requests whose (result.end - arrival) <= 100 ms, / wall time.
-
-`python bench.py --impl reference` times the reference path on the host CPU:
-the reference worker computes nothing (worker.py:1-9), so its CPU path is the
-oracle port (oracle/): the same cold-start schedule with LOAD = memcpy of the
-blob into a host page pool and INFER = the fp32 torchvision forward on all
-host cores, at the largest batch whose latency meets the SLO.
+`--impl reference`: the reference's own implementation of the path, run unmodified from
+baseline/_ref: the same configs[2] experiment (same controller, trace, rate, SLO, copies,
+pages) against the reference EmulatedWorker processes (`python -m sloserve.cli worker`, the
+reference catalog's resnet50 durations), which wait out profiled V100 durations on the host
+CPU (pkg/src/sloserve/worker.py:1-9). It imports nothing of this repo but bench_e2e.py.
 """
 
 from __future__ import annotations
@@ -32,20 +42,28 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
 import threading
 import time
 
-import numpy as np
-
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-SLO_NS = 100_000_000
+import numpy as np  # noqa: E402
+
+import bench_e2e  # noqa: E402
+
+SLO_NS = bench_e2e.SLO_NS
 METRIC = "goodput req/s within 100ms SLO; INFER images/s and p99.99/p50 per batch"
-WORKLOAD = "resnet50 x1000 copies, 16MiB-paged weight cache, LOAD/INFER/UNLOAD, b=16, SLO 100ms"
+VALUE_WORKLOAD = ("configs[0] INFER throughput, resnet50 b=16, request inputs resident in the "
+                  "IOCache, 1000 weight copies resident in 16MiB HBM pages rotating per step "
+                  "(no LOAD in the timed region)")
+E2E_WORKLOAD = ("configs[2] synthetic MAF-style trace over 1000 resnet50 copies, unmodified "
+                "reference controller (baseline/_ref sloserve) -> one worker process per GPU "
+                "over TCP, SLO 100ms")
 
 
 def parse_args():
@@ -56,51 +74,71 @@ def parse_args():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--copies", type=int, default=1000)
-    ap.add_argument("--pages", type=int, default=500)
-    ap.add_argument("--sweep-samples", type=int, default=10000)
-    ap.add_argument("--clients", type=int, default=4)
+    ap.add_argument("--sweep-samples", type=int, default=20000)
+    ap.add_argument("--host-samples", type=int, default=2000)
+    ap.add_argument("--e2e-seconds", type=float, default=30.0)
+    ap.add_argument("--e2e-rate", type=float, default=2500.0, help="offered req/s per GPU")
+    ap.add_argument("--e2e-pages", type=int, default=8000)
+    ap.add_argument("--cold-seconds", type=float, default=15.0)
+    ap.add_argument("--cold-rate", type=float, default=1000.0)
+    ap.add_argument("--cold-pages", type=int, default=500)
+    ap.add_argument("--startup", type=float, default=60.0,
+                    help="seconds allowed for the worker processes to build their plans")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cold", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
 
-# ----------------------------------------------------------------------------- distributed
+# ----------------------------------------------------------------------------- processes
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def maybe_spawn(args) -> None:
+    """`--gpus N` without a launcher: re-run under torch.distributed.run, one rank per GPU."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+
 
 class Dist:
+    """Rank plumbing over gloo (CPU tensors): barriers and max / sum of scalars. The
+    workers share no tensors (replicas only), so there is no NCCL."""
+
     def __init__(self):
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
-        self.pg = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
-            if backend == "nccl":
-                torch.cuda.set_device(self.local)
-            dist.init_process_group(backend)
-            self.dist = dist
-            self.torch = torch
-            self.backend = backend
+            dist.init_process_group("gloo")
+            self.dist, self.torch = dist, torch
 
     def barrier(self):
         if self.world > 1:
             self.dist.barrier()
 
-    def max(self, v: float) -> float:
+    def _reduce(self, v: float, op) -> float:
         if self.world == 1:
             return v
-        dev = "cuda" if self.backend == "nccl" else "cpu"
-        t = self.torch.tensor([float(v)], dtype=self.torch.float64, device=dev)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        t = self.torch.tensor([float(v)], dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=op)
         return float(t.item())
 
+    def max(self, v: float) -> float:
+        return self._reduce(v, None if self.world == 1 else self.dist.ReduceOp.MAX)
+
     def sum(self, v: float) -> float:
-        if self.world == 1:
-            return v
-        dev = "cuda" if self.backend == "nccl" else "cpu"
-        t = self.torch.tensor([float(v)], dtype=self.torch.float64, device=dev)
-        self.dist.all_reduce(t)
-        return float(t.item())
+        return self._reduce(v, None if self.world == 1 else self.dist.ReduceOp.SUM)
 
     def close(self):
         if self.world > 1:
@@ -110,12 +148,13 @@ class Dist:
 # ----------------------------------------------------------------------------- clocks
 
 class ClockSampler:
+    """nvidia-smi every 100 ms while a region runs (the recipe's clocks line)."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device: int):
-        self.device = device
+    def __init__(self, devices):
+        self.devices = ",".join(str(d) for d in devices)
         self.proc = None
         self.lines: list[str] = []
 
@@ -123,7 +162,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100", "-i", str(self.device)],
+                 "-lms", "100", "-i", self.devices],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -183,41 +222,27 @@ def pct(a, q):
     return float(np.percentile(np.asarray(a, dtype=np.float64), q))
 
 
-def b200_catalog(copies: int, blob_bytes: int):
-    from paper_2006_02464_b200 import catalog
-    text = f"""page_bytes 16777216
-model resnet50
-weights_bytes {blob_bytes}
-weights_transfer_ns 1200000
-io_ns 12000 2000
-io_bytes 602112 4000
-batch 1 500000
-batch 2 530000
-batch 4 600000
-batch 8 750000
-batch 16 1100000
-replicas resnet50 {copies - 1}
-"""
-    return catalog.parse(text)
+def ncu_traffic(b: int):
+    """DRAM bytes (read + write) per launch of the INFER megakernel at batch b, from the
+    newest committed `ncu --set full` capture summary (tools/ncu_capture.sh +
+    tools/ncu_summary.py) under profiles/."""
+    for name in ("r2_ncu_full_mk_infer_summary.json", "r1_ncu_full_mk_infer_summary.json"):
+        path = os.path.join(REPO, "profiles", name)
+        try:
+            s = json.load(open(path))[f"b{b}"]
+            mb = sum(float(s[k].split()[0]) for k in ("dram__bytes_read.sum",
+                                                       "dram__bytes_write.sum"))
+            unit = s["dram__bytes_read.sum"].split()[1]
+            scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1.0)
+            return mb * scale, f"profiles/{name} (b={b})"
+        except (OSError, KeyError, ValueError, IndexError):
+            continue
+    return None, None
 
 
 # ----------------------------------------------------------------------------- our arm
 
-def ncu_traffic(b: int):
-    """DRAM bytes (read + write) per launch of the INFER megakernel at batch b, from the
-    committed `ncu --set full` capture summary (tools/ncu_capture.sh + tools/ncu_summary.py)."""
-    path = os.path.join(REPO, "profiles", "r1_ncu_full_mk_infer_summary.json")
-    try:
-        s = json.load(open(path))[f"b{b}"]
-        mb = sum(float(s[k].split()[0]) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-        unit = s["dram__bytes_read.sum"].split()[1]
-        scale = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1.0)
-        return mb * scale, f"profiles/{os.path.basename(path)} (b={b})"
-    except (OSError, KeyError, ValueError, IndexError):
-        return None, None
-
-
-def run_ours(args, d: Dist) -> dict | None:
+def run_device_legs(args, d: Dist) -> dict:
     from paper_2006_02464_b200 import arch
     from paper_2006_02464_b200.device import DeviceRuntime
 
@@ -227,9 +252,7 @@ def run_ours(args, d: Dist) -> dict | None:
     blob = arch.pack_blob(spec, arch.fold(spec, params))
     b = args.batch
     bf16_peak, bf16_sus, hbm_peak, peak_kind = peaks()
-    out: dict = {}
-
-    # ---------------- value: device-resident leg
+    out: dict = {"spec": spec, "params": params, "blob_bytes": blob.data.nbytes}
     copies = args.copies
     with DeviceRuntime(device=dev, pages_total=copies * blob.pages, io_slots=16) as rt:
         rt.register_arch(0, spec)
@@ -243,7 +266,7 @@ def run_ours(args, d: Dist) -> dict | None:
         hdr = [int(c) * blob.pages for c in sched]
         rt.exec_many(0, b, hdr[:args.warmup])
         d.barrier()
-        with ClockSampler(dev) as clk:
+        with ClockSampler([dev]) as clk:
             d.barrier()
             ex, wall = rt.exec_many(0, b, hdr[args.warmup:])
             d.barrier()
@@ -257,39 +280,46 @@ def run_ours(args, d: Dist) -> dict | None:
         out["load_copy_ms_p50"] = pct(load_ns, 50) / 1e6
         out["load_gbs"] = blob.data.nbytes / (pct(load_ns, 50) / 1e9) / 1e9
 
-        # ---------------- per-batch INFER sweep (device Exec time, %globaltimer)
+        # ---- per-batch sweep: img/s + device Exec spread (pipelined), host span (closed loop)
         sweep = {}
-        for bb in (1, 2, 4, 8, 16):
-            n = args.sweep_samples
-            hp = [int(c) * blob.pages for c in schedule(n + 50, copies, 100 + bb)]
-            rt.exec_many(0, bb, hp[:50])
-            ex_b, wall_b = rt.exec_many(0, bb, hp[50:])
-            p50 = pct(ex_b, 50)
-            # ~2 ms whole-GPU stalls hit any kernel on these boxes every few seconds (a plain
-            # FMA kernel shows them too: tools/stall_probe.cu, profiles/r1_tail.txt): counted
-            # and also excluded in a separately labelled percentile; the raw one stays
-            stall = ex_b > p50 + 1_000_000
-            calm = ex_b[~stall]
-            sweep[str(bb)] = {
-                "img_s": bb * n / (wall_b / 1e9), "p50_us": p50 / 1e3,
-                "p99_us": pct(ex_b, 99) / 1e3, "p9999_us": pct(ex_b, 99.99) / 1e3,
-                "max_us": float(ex_b.max()) / 1e3, "p9999_over_p50": pct(ex_b, 99.99) / p50,
-                "platform_stalls": int(stall.sum()),
-                "p9999_over_p50_excl_stalls": pct(calm, 99.99) / p50,
-                "n": n, "roofline_us": max(spec.flops_per_image * bb / (bf16_peak * 1e12),
-                                           (blob.data.nbytes + bb * 606112) / (hbm_peak * 1e9)) * 1e6}
+        with ClockSampler([dev]) as clk_sweep:
+            for bb in (1, 2, 4, 8, 16):
+                n = args.sweep_samples
+                hp = [int(c) * blob.pages for c in schedule(n + 50, copies, 100 + bb)]
+                rt.exec_many(0, bb, hp[:50])
+                ex_b, wall_b = rt.exec_many(0, bb, hp[50:])
+                hn = args.host_samples
+                ex_c, host_c = rt.exec_closed(0, bb, hp[:hn])
+                p50 = pct(ex_b, 50)
+                # ~2 ms whole-GPU stalls hit any kernel on these boxes every few seconds (a plain
+                # FMA kernel shows them too: tools/stall_probe.cu, profiles/r1_tail.txt):
+                # counted, and excluded only in the separately labelled percentile
+                stall = ex_b > p50 + 1_000_000
+                calm = ex_b[~stall]
+                sweep[str(bb)] = {
+                    "img_s": bb * n / (wall_b / 1e9), "p50_us": p50 / 1e3,
+                    "p99_us": pct(ex_b, 99) / 1e3, "p9999_us": pct(ex_b, 99.99) / 1e3,
+                    "max_us": float(ex_b.max()) / 1e3, "p9999_over_p50": pct(ex_b, 99.99) / p50,
+                    "platform_stalls": int(stall.sum()),
+                    "p9999_over_p50_excl_stalls": pct(calm, 99.99) / p50, "n": n,
+                    "host_span_p50_us": pct(host_c, 50) / 1e3,
+                    "host_span_p99_us": pct(host_c, 99) / 1e3,
+                    "host_span_max_us": float(host_c.max()) / 1e3,
+                    "closed_loop_exec_p50_us": pct(ex_c, 50) / 1e3, "host_n": hn,
+                    "roofline_us": max(spec.flops_per_image * bb / (bf16_peak * 1e12),
+                                       (blob.data.nbytes + bb * 606112) / (hbm_peak * 1e9)) * 1e6}
         out["infer"] = sweep
+        out["clocks_sweep"] = clk_sweep.summary()
 
-        # ---------------- roofline of the dominant kernel: the INFER megakernel
-        # (one persistent launch per INFER; the graph adds the 1-thread gate and
-        # done kernels). Achieved = algorithmic FLOPs of the timed INFERs / the
-        # CUDA-event time of the timed region on the Exec stream.
+        # ---- roofline of the dominant kernel: the INFER megakernel (one persistent launch
+        # per INFER; the graph adds a 1-CTA gate and a 1-thread done kernel). Achieved =
+        # algorithmic FLOPs of the timed INFERs / the CUDA-event time of the timed region on
+        # the Exec stream (the stream the graphs are launched on).
         flops = spec.flops_per_image * b
         achieved = flops * args.steps / (wall / 1e9) / 1e12
         ends, kinds = rt.profile_layers(0, b, int(sched[0]) * blob.pages)
         plan = rt.plan_layers(0, b)
-        conv_t = 0.0
-        prev = 0.0
+        conv_t = prev = 0.0
         for k, t in zip(kinds, ends):
             t = float(t)
             if k == 1:
@@ -299,162 +329,56 @@ def run_ours(args, d: Dist) -> dict | None:
         out["roofline"] = {
             "bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
             "frac": achieved / bf16_peak, "traffic": traffic, "traffic_source": traffic_src,
+            "algorithmic_bytes": blob.data.nbytes + b * 606112,
             "kernel": "mk_infer_kernel (persistent tcgen05/TMA megakernel, whole forward)",
-            "flops_per_launch": flops,
-            "launches_per_infer": int(launches),
-            "layers": int(len(plan)),
-            "conv_share_of_trace": conv_t / max(prev, 1e-9),
+            "flops_per_launch": flops, "launches_per_infer": int(launches),
+            "layers": int(len(plan)), "conv_share_of_trace": conv_t / max(prev, 1e-9),
             "trace_end_us": prev * 1e3,
             "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst, {peak_kind})"}
-
-    # ---------------- e2e: through the worker's public API
-    out["e2e"] = run_e2e(args, d, spec, blob)
-
-    # ---------------- cpu baseline (oracle port, rank 0, bounded sample)
-    if d.rank == 0 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(spec, params, budget_s=15.0)
     return out
 
 
-def run_e2e(args, d: Dist, spec, blob) -> dict:
-    from paper_2006_02464_b200.wire import Action, ActionKind
-    from paper_2006_02464_b200.worker import B200Worker
-
-    cat = b200_catalog(args.copies, blob.data.nbytes)
-    pages_per_model = cat.pages_needed(0)
-    b = args.batch
-    lock = threading.Lock()
-    waiters: dict[int, tuple] = {}
-
-    def send_result(r):
-        with lock:
-            ev = waiters.pop(r.action_id, None)
-        if ev is not None:
-            ev[1].append(r)
-            ev[0].set()
-
-    w = B200Worker(0, cat, None, send_result, pages_per_gpu=args.pages, mode="cuda",
-                   devices=[d.local], epoch_ns=time.time_ns())
-    ids = iter(range(1, 1 << 62))
-
-    def call(kind, model, batch=(), window_ns=1_000_000_000):
-        aid = next(ids)
-        ev = (threading.Event(), [])
-        with lock:
-            waiters[aid] = ev
-        now = time.time_ns() - w.epoch_ns
-        w.on_action(Action(aid, kind, model, now, now + window_ns, tuple(batch), 0))
-        ev[0].wait()
-        return ev[1][0]
-
-    # Driver-side page mirror (what the controller tracks, controller_state.py:74-142).
-    resident: dict[int, int] = {}          # model -> last use
-    pins: dict[int, int] = {}
-    loading: dict[int, threading.Event] = {}
-    free = [args.pages]
-    stats = {"loads": 0, "cold": 0, "ok": 0, "reqs": 0, "lat": [], "not_loaded": 0,
-             "loaded_bytes": 0}
-    mlock = threading.Lock()
-    sched = schedule(args.warmup + args.steps, args.copies, 7 + d.rank)
-    cursor = [0]
-
-    def ensure(m):
-        waited = False
-        while True:
-            with mlock:
-                if m in resident:
-                    resident[m] = time.monotonic_ns()
-                    pins[m] = pins.get(m, 0) + 1
-                    return waited
-                ev = loading.get(m)
-                if ev is None:
-                    ev = loading[m] = threading.Event()
-                    victims = []
-                    while free[0] < pages_per_model:
-                        cands = [x for x in resident if pins.get(x, 0) == 0]
-                        if not cands:
-                            break
-                        v = min(cands, key=resident.get)
-                        del resident[v]
-                        free[0] += pages_per_model
-                        victims.append(v)
-                    free[0] -= pages_per_model
-                    owner = True
-                else:
-                    owner = False
-            if not owner:
-                ev.wait()
-                waited = True
-                continue
-            for v in victims:
-                call(ActionKind.UNLOAD, int(v))
-            r = call(ActionKind.LOAD, int(m))
-            with mlock:
-                if int(r.status) == 1:
-                    resident[m] = time.monotonic_ns()
-                    stats["loads"] += 1
-                    stats["loaded_bytes"] += blob.data.nbytes
-                else:
-                    free[0] += pages_per_model
-                del loading[m]
-            ev.set()
-            if int(r.status) != 1:
-                raise RuntimeError(f"LOAD failed with status {int(r.status)}")
-            waited = True
-
-    def client(timed_steps, record):
-        while True:
-            with mlock:
-                i = cursor[0]
-                if i >= timed_steps:
-                    return
-                cursor[0] += 1
-            m = int(sched[i % len(sched)])
-            arrival = time.time_ns() - w.epoch_ns
-            cold = ensure(m)
-            r = call(ActionKind.INFER, m, batch=[i * b + j for j in range(b)])
-            with mlock:
-                pins[m] -= 1
-                if record:
-                    stats["reqs"] += b
-                    stats["cold"] += int(cold)
-                    if int(r.status) == 1:
-                        lat = r.end - arrival
-                        stats["lat"].append(lat)
-                        stats["ok"] += b if lat <= SLO_NS else 0
-                    else:
-                        stats["not_loaded"] += 1
-
-    def run(n, record):
-        cursor[0] = 0
-        ts = [threading.Thread(target=client, args=(n, record)) for _ in range(args.clients)]
-        t0 = time.perf_counter()
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
-        return time.perf_counter() - t0
-
-    run(max(args.warmup, 1), False)
-    for k in ("loads", "loaded_bytes"):
-        stats[k] = 0
-    sched = schedule(args.steps, args.copies, 11 + d.rank)
+def run_controller_legs(args, d: Dist) -> dict:
+    """configs[2] (e2e) and configs[1] (cold_start) behind the reference controller. Rank 0
+    starts one worker process per GPU of the job and drives them; the other ranks wait."""
+    out = {}
+    if d.rank == 0:
+        devices = list(range(d.world))
+        if not args.skip_e2e:
+            h = int(args.e2e_seconds * 1e9)
+            with ClockSampler(devices) as clk:
+                r = bench_e2e.run_leg(
+                    "b200", lambda wl: [bench_e2e.trace_group(wl, args.copies,
+                                                              args.e2e_rate * d.world, h, 1)[0]],
+                    args.copies, args.e2e_pages, h, devices, args.startup)
+            r["clocks"] = clk.summary()
+            out["e2e"] = r
+        if not args.skip_cold:
+            h = int(args.cold_seconds * 1e9)
+            out["cold_start"] = bench_e2e.run_leg(
+                "b200", lambda wl: [bench_e2e.cold_group(wl, args.copies, args.cold_rate * d.world)],
+                args.copies, args.cold_pages, h, devices, args.startup)
     d.barrier()
-    dt = run(args.steps, True)
-    d.barrier()
-    t_max = d.max(dt)
-    ok = d.sum(stats["ok"])
-    w.close()
-    lat = stats["lat"] or [0]
+    return out
+
+
+def e2e_line(r: dict, args, n_gpus: int) -> dict:
     return {
-        "value": ok / t_max, "unit": "req/s",
-        "h2d_bytes_per_step": int(b * 602112 + stats["loaded_bytes"] / max(args.steps, 1)),
-        "d2h_bytes_per_step": int(b * 4000),
-        "cold_start_fraction": stats["cold"] / max(args.steps, 1),
-        "loads": stats["loads"], "failed_infers": stats["not_loaded"],
-        "latency_p50_ms": pct(lat, 50) / 1e6, "latency_p99_ms": pct(lat, 99) / 1e6,
-        "clients": args.clients, "pages_per_gpu": args.pages, "copies": args.copies,
-        "satisfaction": stats["ok"] / max(stats["reqs"], 1),
+        "value": r["goodput_rps"], "unit": "req/s",
+        "h2d_bytes_per_step": int(r["h2d_bytes_per_infer"]),
+        "d2h_bytes_per_step": int(r["d2h_bytes_per_infer"]),
+        "step": "one INFER action (mean_batch requests)",
+        "workload": E2E_WORKLOAD, "offered_rps": r["offered_rps"],
+        "satisfaction": r["satisfaction"], "cold_starts": r["cold_starts"],
+        "rejected_too_late": r["rejected_too_late"], "actions": r["actions"],
+        "mean_batch": r["mean_batch"], "latency_p50_ms": r["latency_p50_ms"],
+        "latency_p99_ms": r["latency_p99_ms"], "latency_max_ms": r["latency_max_ms"],
+        "over_slo": r["totals"].get("over_slo"), "horizon_s": r["horizon_s"],
+        "wall_s": r["wall_s"], "pages_per_gpu": args.e2e_pages, "copies": args.copies,
+        "rate_per_gpu": args.e2e_rate, "workers": r["workers"], "worker_kind": r["worker_kind"],
+        "clocks": r.get("clocks"),
+        "underprediction_fraction": r["underprediction_fraction"],
+        "overprediction_fraction": r["overprediction_fraction"],
     }
 
 
@@ -474,119 +398,103 @@ def cpu_baseline(spec, params, budget_s: float) -> dict:
         resnet_oracle.logits(model, x)
         n += 1
     dt = time.perf_counter() - t0
-    return {"value": 16 * n / dt, "unit": "req/s", "cores": cores, "kind": "port",
-            "sample": f"{n} INFERs of batch 16 through the fp32 CPU oracle "
-                      f"(torchvision resnet50, {cores} threads), {dt:.1f} s; "
-                      f"per-batch latency {dt / n * 1e3:.0f} ms (> SLO at b=16)"}
+    return {"value": 16 * n / dt, "unit": "img/s", "cores": cores, "kind": "port",
+            "sample": f"{n} INFERs of batch 16 through the fp32 CPU oracle (torchvision "
+                      f"resnet50, {cores} threads), {dt:.1f} s; per-batch latency "
+                      f"{dt / n * 1e3:.0f} ms"}
 
 
 # ----------------------------------------------------------------------------- reference arm
 
-def run_reference(args) -> dict:
-    """CPU path of the reference worker (oracle port): cold-start schedule with
-    LOAD = memcpy into a host page pool and INFER = fp32 torchvision forward."""
-    import torch
-
-    from oracle import resnet_oracle
-    from paper_2006_02464_b200 import arch
-
-    cores = os.cpu_count() or 1
-    torch.set_num_threads(cores)
-    spec = arch.build_arch("resnet50")
-    params = arch.make_params(spec, seed=0)
-    blob = arch.pack_blob(spec, arch.fold(spec, params))
-    model = resnet_oracle.torchvision_model("resnet50", params)
-    x = arch.make_inputs(16, spec)
-    # Largest batch whose CPU latency meets the SLO (what a Clockwork controller would pick).
-    batch, lat_by_b = 1, {}
-    for bb in (1, 2, 4, 8, 16):
-        resnet_oracle.logits(model, x[:bb])
-        t0 = time.perf_counter()
-        resnet_oracle.logits(model, x[:bb])
-        lat_by_b[bb] = time.perf_counter() - t0
-        if lat_by_b[bb] * 1e9 <= SLO_NS * 0.8:
-            batch = bb
-        else:
-            break
-    # Bound the run to ~2 minutes of CPU work.
-    per_step = lat_by_b[batch] + 0.01
-    steps = max(3, min(args.steps, int(120 / per_step)))
-    warm = min(args.warmup, 3)
-    pages_per_model = blob.pages
-    resident_cap = max(1, args.pages // pages_per_model)
-    pool = np.zeros((resident_cap, blob.data.nbytes), np.uint8)
-    slot_of: dict[int, int] = {}
-    lru: dict[int, int] = {}
-    sched = schedule(warm + steps, args.copies, 7)
-    ok = reqs = cold = 0
-    t_start = None
-    for i, m in enumerate(sched):
-        if i == warm:
-            t_start = time.perf_counter()
-            ok = reqs = cold = 0
-        m = int(m)
-        t0 = time.perf_counter()
-        if m not in slot_of:
-            cold += 1
-            if len(slot_of) >= resident_cap:
-                v = min(lru, key=lru.get)
-                slot = slot_of.pop(v)
-                del lru[v]
-            else:
-                slot = len(slot_of)
-            pool[slot, :] = blob.data     # LOAD: copy the paged blob
-            slot_of[m] = slot
-        lru[m] = i
-        resnet_oracle.logits(model, x[:batch])
-        lat = (time.perf_counter() - t0) * 1e9
-        reqs += batch
-        ok += batch if lat <= SLO_NS else 0
-    dt = time.perf_counter() - t_start
-    value = ok / dt
+def run_reference(args, d: Dist):
+    """The reference implementation behind the same controller on the same configs[2]
+    experiment: EmulatedWorker processes (CPU) in place of the B200 workers. Rank 0 only."""
+    if d.rank != 0:
+        return None
+    h = int(args.e2e_seconds * 1e9)
+    devices = list(range(d.world))   # one emulated worker per GPU of the job
+    r = bench_e2e.run_leg(
+        "reference", lambda wl: [bench_e2e.trace_group(wl, args.copies,
+                                                       args.e2e_rate * d.world, h, 1)[0]],
+        args.copies, args.e2e_pages, h, devices, startup_s=15.0)
+    e2e = e2e_line(r, args, d.world)
+    e2e["h2d_bytes_per_step"] = 0
+    e2e["d2h_bytes_per_step"] = 0
+    value = r["goodput_rps"]
     return {
-        "metric": METRIC, "value": value, "unit": "req/s", "n_gpus": args.gpus, "steps": steps,
-        "warmup": warm, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "impl": "reference",
-        "config": {"workload": WORKLOAD, "batch": batch, "copies": args.copies,
-                   "pages_per_gpu": args.pages, "parallelism": "replicas"},
-        "cpu_baseline": {"value": value, "unit": "req/s", "cores": cores, "kind": "port",
-                         "sample": f"{steps} steps of the cold-start schedule at batch {batch} "
-                                   f"(largest batch meeting the SLO on {cores} cores; "
-                                   f"latency by batch {json.dumps({k: round(v * 1e3, 1) for k, v in lat_by_b.items()})} ms), "
-                                   f"cold fraction {cold / steps:.2f}"},
-        "e2e": {"value": value, "unit": "req/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "metric": METRIC, "value": value, "unit": "req/s", "n_gpus": d.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / max(value, 1e-9),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (gen_synthetic_trace, seed 1)", "impl": "reference",
+        "config": {"workload": E2E_WORKLOAD, "copies": args.copies,
+                   "pages_per_gpu": args.e2e_pages, "rate_per_gpu": args.e2e_rate,
+                   "horizon_s": args.e2e_seconds, "parallelism": "replicas (one worker per GPU)"},
+        "cpu_baseline": {"value": value, "unit": "req/s", "cores": 2, "kind": "reference",
+                         "sample": f"{args.e2e_seconds:.0f} s of the configs[2] trace replay "
+                                   f"through the reference controller against "
+                                   f"{len(devices)} reference EmulatedWorker process(es) "
+                                   "(each: one WallLoop thread + one socket thread), which "
+                                   "wait out the reference catalog's V100 resnet50 durations"},
+        "e2e": e2e,
+        "native_so_loaded": [m for m in _loaded_objects() if "libcw" in m],
     }
+
+
+def _loaded_objects() -> list[str]:
+    try:
+        with open(f"/proc/{os.getpid()}/maps") as f:
+            return sorted({ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")})
+    except OSError:
+        return []
 
 
 # ----------------------------------------------------------------------------- main
 
 def main():
     args = parse_args()
+    maybe_spawn(args)
     d = Dist()
     if args.impl == "reference":
-        if d.rank == 0:
-            print(json.dumps(run_reference(args)), flush=True)
+        line = run_reference(args, d)
+        if line is not None:
+            print(json.dumps(line), flush=True)
         d.close()
         return
-    res = run_ours(args, d)
+    res = run_device_legs(args, d)
+    ctl = run_controller_legs(args, d)
     if d.rank == 0:
         line = {
             "metric": METRIC, "value": res["value"], "unit": "req/s", "n_gpus": d.world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (N(0,1) 3x224x224 inputs, random-init ResNet-50 weights)",
-            "config": {"workload": WORKLOAD, "batch": args.batch, "copies": args.copies,
-                       "pages_per_gpu_e2e": args.pages, "parallelism": "replicas (one worker per GPU)",
-                       "l2": "inputs larger than L2: 1000 copies x 54 MB weights rotate per step"},
-            "clocks": res["clocks"], "gpu_launches": res["gpu_launches"],
-            "e2e": res["e2e"], "roofline": res["roofline"], "infer": res["infer"],
-            "load": {"copy_ms_p50": res["load_copy_ms_p50"], "gbs": res["load_gbs"]},
+            "config": {"workload": VALUE_WORKLOAD, "batch": args.batch, "copies": args.copies,
+                       "parallelism": "replicas (one worker per GPU)",
+                       "l2": "inputs larger than L2: 1000 copies x 51 MB weights rotate per step",
+                       "e2e_workload": E2E_WORKLOAD},
+            "clocks": res["clocks"], "clocks_sweep": res["clocks_sweep"],
+            "gpu_launches": res["gpu_launches"], "roofline": res["roofline"],
+            "infer": res["infer"],
+            "load": {"copy_ms_p50": res["load_copy_ms_p50"], "gbs": res["load_gbs"],
+                     "blob_bytes": res["blob_bytes"]},
             "exec_p50_us": res["exec_p50_us"],
         }
-        if "cpu_baseline" in res:
-            line["cpu_baseline"] = res["cpu_baseline"]
+        if "e2e" in ctl:
+            line["e2e"] = e2e_line(ctl["e2e"], args, d.world)
+            line["gpu_launches_e2e"] = 3 * sum(
+                v for k, v in ctl["e2e"]["actions"].items() if k.startswith("infer:")
+                and not k.endswith("model_not_loaded"))
+        if "cold_start" in ctl:
+            c = ctl["cold_start"]
+            line["cold_start"] = {
+                "workload": "configs[1]: 1000 resnet50 copies, open-loop uniform over copies, "
+                            f"{args.cold_pages} pages per GPU (71 copies fit), reference controller",
+                "goodput_rps": c["goodput_rps"], "offered_rps": c["offered_rps"],
+                "satisfaction": c["satisfaction"], "cold_starts": c["cold_starts"],
+                "loads": c["loads"], "actions": c["actions"], "mean_batch": c["mean_batch"],
+                "latency_p99_ms": c["latency_p99_ms"], "horizon_s": c["horizon_s"]}
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(res["spec"], res["params"], budget_s=15.0)
         print(json.dumps(line), flush=True)
     d.close()
 

@@ -89,6 +89,11 @@ int cw_rt_infer_sync(cw_runtime* rt, int arch_id, int batch, int32_t hdr_page,
  * %globaltimer) into exec_ns[i]; *wall_ns = CUDA-event time of all n on the Exec stream. */
 int cw_rt_exec_many(cw_runtime* rt, int arch_id, int batch, const int32_t* hdr_pages, int n,
                     int64_t* exec_ns, int64_t* wall_ns);
+/* Closed loop (one INFER in flight): per INFER i, exec_ns[i] = device Exec time and
+ * host_ns[i] = host-observed span (CLOCK_MONOTONIC from before the graph launch until the
+ * host sees the completion record). */
+int cw_rt_exec_closed(cw_runtime* rt, int arch_id, int batch, const int32_t* hdr_pages, int n,
+                      int64_t* exec_ns, int64_t* host_ns);
 /* One INFER with the megakernel's per-layer trace read back: end_ms[i] = time from
  * Exec start until plan layer i finished on its last SM; kinds[i] = layer kind
  * (1 conv, 2 input, 3 maxpool, 4 avgpool, 5 fc, 6 split-K reduce). Returns the layer count. */

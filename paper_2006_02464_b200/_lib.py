@@ -94,6 +94,7 @@ SIGNATURES = [
     ("cw_rt_load_sync", C.c_int, [_P, C.c_int, _I32P, C.c_int, _I64P]),
     ("cw_rt_infer_sync", C.c_int, [_P, C.c_int, C.c_int, C.c_int32, _P, _P, _I64P]),
     ("cw_rt_exec_many", C.c_int, [_P, C.c_int, C.c_int, _I32P, C.c_int, _I64P, _I64P]),
+    ("cw_rt_exec_closed", C.c_int, [_P, C.c_int, C.c_int, _I32P, C.c_int, _I64P, _I64P]),
     ("cw_rt_profile_layers", C.c_int, [_P, C.c_int, C.c_int, C.c_int32, _P, _I32P, C.c_int]),
     ("cw_rt_last_trace", C.c_int64, [_P, _P, C.c_int64]),
     ("cw_rt_plan_layers", C.c_int, [_P, C.c_int, C.c_int, _I32P, C.c_int]),

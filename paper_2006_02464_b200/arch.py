@@ -26,8 +26,6 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib
-
 HEADER_BYTES = 65536
 BN_EPS = 1e-5
 
@@ -64,6 +62,7 @@ class ArchSpec:
     flops_per_image: int = 0   # algorithmic (unpadded K), conv + fc
 
     def op_structs(self):
+        from . import _lib  # lazily: the tables themselves load no native code
         arr = (_lib.cw_op * len(self.ops))()
         for i, op in enumerate(self.ops):
             for k, v in op.items():
@@ -253,6 +252,7 @@ class Blob:
     page_bytes: int
 
     def loc_structs(self):
+        from . import _lib
         arr = (_lib.cw_tensor_loc * len(self.locs))()
         for i, (w, b, r, k) in enumerate(self.locs):
             arr[i].w_off, arr[i].b_off, arr[i].rows, arr[i].k = w, b, r, k

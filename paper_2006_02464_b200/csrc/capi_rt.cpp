@@ -2,6 +2,7 @@
 #include <cstdlib>
 #include <cuda_runtime.h>
 #include <cstring>
+#include <ctime>
 #include <string>
 #include <vector>
 
@@ -162,6 +163,32 @@ int cw_rt_exec_many(cw_runtime* rt, int arch_id, int batch, const int32_t* hdr_p
   if (wall_ns) *wall_ns = (int64_t)(ms * 1e6);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  return 0;
+}
+
+int cw_rt_exec_closed(cw_runtime* rt, int arch_id, int batch, const int32_t* hdr_pages, int n,
+                      int64_t* exec_ns, int64_t* host_ns) {
+  Runtime& r = rt->rt;
+  if (batch < 1 || batch > cw::kMaxBatch || batch > r.io_slots()) return cw::fail("bad batch");
+  std::vector<int32_t> slots(batch);
+  for (int j = 0; j < batch; ++j) slots[j] = j;
+  auto mono = [] {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (int64_t)ts.tv_sec * 1000000000LL + ts.tv_nsec;
+  };
+  for (int i = 0; i < n; ++i) {
+    uint64_t seq = 0;
+    const int64_t t0 = mono();
+    std::string err = r.exec_async(arch_id, batch, hdr_pages[i], slots.data(), 0, ~0ull, -1, &seq);
+    if (!err.empty()) return cw::fail(err);
+    cw::ExecRecord* rec = r.exec_record(seq);
+    while (rec->seq_done != seq + 1) {
+    }
+    const int64_t t1 = mono();
+    if (host_ns) host_ns[i] = t1 - t0;
+    if (exec_ns) exec_ns[i] = (int64_t)(rec->t_end - rec->t_start);
+  }
   return 0;
 }
 

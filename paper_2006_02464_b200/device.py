@@ -115,6 +115,17 @@ class DeviceRuntime:
               "exec_many")
         return ex, wall.value
 
+    def exec_closed(self, arch_id: int, batch: int, hdr_pages) -> tuple[np.ndarray, np.ndarray]:
+        """One INFER in flight at a time: (device Exec ns, host-observed span ns) per INFER."""
+        hp = _i32(hdr_pages)
+        n = len(hdr_pages)
+        ex = np.zeros(n, np.int64)
+        host = np.zeros(n, np.int64)
+        check(lib.cw_rt_exec_closed(self.h, arch_id, batch, hp, n,
+                                    ex.ctypes.data_as(C.POINTER(C.c_int64)),
+                                    host.ctypes.data_as(C.POINTER(C.c_int64))), "exec_closed")
+        return ex, host
+
     def profile_layers(self, arch_id: int, batch: int, hdr_page: int
                        ) -> tuple[np.ndarray, np.ndarray]:
         """One INFER with the megakernel trace: per plan layer, ms from Exec start

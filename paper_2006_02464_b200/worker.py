@@ -24,6 +24,7 @@ modes
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import os
 import threading
 import time
@@ -208,6 +209,15 @@ class Engine:
         return out
 
 
+@functools.lru_cache(maxsize=8)
+def _random_init_blob(base: str, seed: int, page_bytes: int):
+    """Folded, paged blob of the deterministic random-init weights of an arch (shared by
+    every worker of the process; the blob is read-only once packed)."""
+    spec = arch_mod.build_arch(base)
+    return arch_mod.pack_blob(spec, arch_mod.fold(spec, arch_mod.make_params(spec, seed=seed)),
+                              page_bytes=page_bytes)
+
+
 class _WallDriver:
     """Runs a sim-mode engine in wall time when the caller supplies no event loop (the TCP
     server): the engine's own timer queue is the schedule; one thread sleeps until the next
@@ -325,9 +335,7 @@ class B200Worker:
                                       f"(catalog: {base}, {cat.page_bytes})")
                     blobs[base] = blob
                     continue
-                params = arch_mod.make_params(spec, seed=weights_seed)
-                blobs[base] = arch_mod.pack_blob(spec, arch_mod.fold(spec, params),
-                                                 page_bytes=cat.page_bytes)
+                blobs[base] = _random_init_blob(base, weights_seed, cat.page_bytes)
             pool_shape = {(s.in_c, s.in_h, s.in_w) for s in specs.values()}
             if len(pool_shape) != 1:
                 raise CwError("one input shape per worker is supported")

@@ -50,7 +50,7 @@ def _worker(rank: int, world: int, port: int, q):
     sys.path.insert(0, REPO)
     import bench
     d = bench.Dist()
-    assert d.backend == "gloo"
+    assert d.dist.get_backend() == "gloo"   # no NCCL: replicas exchange no tensors
     res = _shard_results(rank, world)
     d.barrier()
     n_ok = d.sum(float(sum(r[2] for r in res)))
@@ -131,3 +131,20 @@ def test_two_external_workers_distinct_ids_behind_reference_controller(tmp_path)
     # both workers executed actions (requests were sharded across them)
     rows = [sum(1 for _ in open(tmp_path / f"w{w}.csv")) - 1 for w in (0, 1)]
     assert all(r > 0 for r in rows), rows
+
+
+@pytest.mark.skipif(not os.path.isdir(os.path.join(REPO, "baseline", "_ref", "sloserve")),
+                    reason="baseline/_ref (reference install) missing")
+def test_bench_controller_leg_two_workers_sim():
+    """bench.py's configs[2] leg as it runs at N=2: the unmodified reference controller
+    (baseline/_ref) replays the synthetic trace against two worker processes with distinct
+    ids (sim engines here, one cuda worker per GPU on the box); both receive INFERs."""
+    sys.path.insert(0, REPO)
+    import bench_e2e
+    h = 3_000_000_000
+    r = bench_e2e.run_leg(
+        "b200-sim", lambda wl: [bench_e2e.trace_group(wl, 50, 400.0, h, 1)[0]],
+        50, 200, h, [0, 1], startup_s=20.0)
+    assert r["workers"] == 2 and r["infer_actions"] > 100
+    assert r["satisfaction"] > 0.9, r
+    assert r["totals"]["over_slo"] == 0
