@@ -188,6 +188,11 @@ int cw_engine_submit(cw_engine* e, const cw_action* a, int64_t at);
 int cw_engine_poll(cw_engine* e, cw_result* out, int max, int64_t timeout_us);
 /* 1 if a device error stopped the engine (cw_last_error() holds the first error). */
 int cw_engine_failed(cw_engine* e);
+/* cuda: INFER executor counters of one GPU (19 int64, see ExecStats in csrc/engine.h and
+ * Engine.STAT_NAMES in worker.py); returns the count written. */
+int cw_engine_stats(cw_engine* e, int gpu_index, int64_t* out, int max);
+/* cuda: globaltimer-vs-CLOCK_REALTIME offset measured now minus the one calibrated at open. */
+int cw_engine_clock_drift(cw_engine* e, int gpu_index, int64_t* drift_ns);
 /* cuda: how the executor thread runs: *cpu = pinned CPU or -1, *rt = 1 if SCHED_FIFO. */
 int cw_engine_executor_info(cw_engine* e, int32_t* cpu, int32_t* rt);
 /* sim: run the virtual-time event loop until no event is left at or before `until`. */

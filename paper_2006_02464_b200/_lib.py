@@ -112,6 +112,8 @@ SIGNATURES = [
     ("cw_engine_next_time", C.c_int64, [_P]),
     ("cw_engine_failed", C.c_int, [_P]),
     ("cw_engine_executor_info", C.c_int, [_P, _I32P, _I32P]),
+    ("cw_engine_stats", C.c_int, [_P, C.c_int, _I64P, C.c_int]),
+    ("cw_engine_clock_drift", C.c_int, [_P, C.c_int, _I64P]),
     ("cw_engine_sim_deliver", C.c_int, [_P, C.POINTER(cw_action), C.c_int64]),
     ("cw_engine_sim_take_new", C.c_int, [_P, _I64P, C.POINTER(C.c_uint64), C.c_int]),
     ("cw_engine_sim_run_to", C.c_int, [_P, C.c_int64, C.c_uint64]),

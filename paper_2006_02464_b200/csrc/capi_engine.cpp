@@ -50,6 +50,21 @@ int cw_engine_sim_take_new(cw_engine* e, int64_t* times, uint64_t* seqs, int max
 
 int cw_engine_failed(cw_engine* e) { return e->e.failed() ? 1 : 0; }
 
+int cw_engine_stats(cw_engine* e, int gpu_index, int64_t* out, int max) {
+  const int n = e->e.stats(gpu_index, out, max);
+  return n < 0 ? cw::fail("bad gpu index") : n;
+}
+
+int cw_engine_clock_drift(cw_engine* e, int gpu_index, int64_t* drift_ns) {
+  cw_runtime* rt = e->e.runtime(gpu_index);
+  if (!rt) return cw::fail("no device runtime");
+  int64_t off = 0;
+  std::string err = rt->rt.measure_clock_offset(&off);
+  if (!err.empty()) return cw::fail(err);
+  *drift_ns = off - rt->rt.clock_offset();
+  return 0;
+}
+
 int cw_engine_executor_info(cw_engine* e, int32_t* cpu, int32_t* rt) {
   e->e.executor_info(cpu, rt);
   return 0;

@@ -1,6 +1,7 @@
 #include "engine.h"
 
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cstring>
 #include <ctime>
@@ -166,6 +167,20 @@ int Engine::sim_deliver(const cw_action& a, int64_t now) {
   return 0;
 }
 
+int Engine::stats(int g, int64_t* out, int max) {
+  if (g < 0 || g >= (int)gpus_.size()) return -1;
+  std::lock_guard<std::mutex> lk(state_mu_);
+  const ExecStats& s = gpus_[g].stats;
+  const int64_t v[] = {s.dispatched, s.host_late, s.host_eff_late, s.gate_late, s.done,
+                       s.dispatch_delay_sum, s.dispatch_delay_max, s.gate_late_sum,
+                       s.gate_late_max, s.start_slack_min, s.busy_gap_sum, s.busy_gap_max,
+                       s.busy_gaps, s.launch_lat_sum, s.launch_lat_max, s.observe_lat_sum,
+                       s.observe_lat_max, s.clock_resyncs, s.clock_step_max};
+  const int n = (int)(sizeof(v) / sizeof(v[0]));
+  for (int i = 0; i < n && i < max; ++i) out[i] = v[i];
+  return n;
+}
+
 int Engine::sim_run_to(int64_t t, uint64_t seq) {
   if (cfg_.mode != 0) return -1;
   int n = 0;
@@ -310,6 +325,7 @@ void Engine::try_start(int g, bool infer) {
     cw_action* a = top.a;
     if (now > a->latest) {
       ex.pending.pop();
+      if (a->kind == INFER) ++gpu.stats.host_late;
       reject(g, a, now);
       continue;
     }
@@ -322,6 +338,7 @@ void Engine::try_start(int g, bool infer) {
       // Window will certainly be missed (e.g. IOCache-blocked input).
       if (eff < kNever) {
         ex.pending.pop();
+        if (a->kind == INFER) ++gpu.stats.host_eff_late;
         reject(g, a, now);
         continue;
       }
@@ -602,7 +619,21 @@ void Engine::device_exec(int g, cw_action* a, int64_t now) {
     return;
   }
   gpu.model_last_exec[a->model_id] = (int64_t)seq;
-  gpu.execs.push_back({a, seq, now, 0, false});
+  ExecStats& st = gpu.stats;
+  ++st.dispatched;
+  int64_t ready = a->earliest;
+  auto it = input_done_.find(a->action_id);
+  if (it != input_done_.end()) ready = std::max(ready, it->second);
+  InflightExec ie{a, seq, now, 0, false};
+  ie.ready = ready;
+  ie.dispatched = this->now();
+  gpu.execs.push_back(ie);
+  if (gpu.last_done_seen > ready) ready = gpu.last_done_seen;
+  const int64_t delay = now - ready;
+  if (delay > 0) {
+    st.dispatch_delay_sum += delay;
+    st.dispatch_delay_max = std::max(st.dispatch_delay_max, delay);
+  }
 }
 
 bool Engine::poll_device() {
@@ -628,6 +659,30 @@ bool Engine::poll_device() {
       if (!e.output && rec->seq_done == e.seq + 1) {
         cw_action* a = e.a;
         const int64_t t0 = gt_to_epoch(g, rec->t_start);
+        ExecStats& st = gpu.stats;
+        gpu.last_done_seen = now();
+        if (gpu.last_exec_end >= 0 && e.ready <= gpu.last_exec_end) {
+          const int64_t gap = t0 - gpu.last_exec_end;
+          st.busy_gap_sum += gap;
+          st.busy_gap_max = std::max(st.busy_gap_max, gap);
+          ++st.busy_gaps;
+        }
+        const int64_t t_end = gt_to_epoch(g, rec->t_end);
+        const int64_t ll = t0 - e.dispatched, ol = gpu.last_done_seen - t_end;
+        st.launch_lat_sum += ll;
+        st.launch_lat_max = std::max(st.launch_lat_max, ll);
+        st.observe_lat_sum += ol;
+        st.observe_lat_max = std::max(st.observe_lat_max, ol);
+        gpu.last_exec_end = t_end;
+        if (rec->rejected) {
+          ++st.gate_late;
+          const int64_t late = t0 - a->latest;
+          st.gate_late_sum += late;
+          st.gate_late_max = std::max(st.gate_late_max, late);
+        } else {
+          ++st.done;
+          st.start_slack_min = std::min(st.start_slack_min, a->latest - t0);
+        }
         if (rec->rejected) {
           gpu.execs.erase(gpu.execs.begin() + i);
           gpu.infer_exec.busy = false;
@@ -688,6 +743,22 @@ void Engine::run_loop() {
     }
     batch.clear();
     progressed |= poll_device();
+    // keep the globaltimer <-> CLOCK_REALTIME offset current (drift: tens of ppm), between
+    // INFERs so the stamp kernel finds an SM
+    for (int g = 0; g < (int)gpus_.size(); ++g) {
+      GpuState& gpu = gpus_[g];
+      if (!gpu.execs.empty() && !gpu.execs.back().output) continue;
+      const int64_t t = now();
+      if (t < gpu.next_clock_sync) continue;
+      int64_t step = 0;
+      if (gpu.rt->rt.resync_clock(&step)) {
+        ++gpu.stats.clock_resyncs;
+        gpu.stats.clock_step_max = std::max(gpu.stats.clock_step_max, step < 0 ? -step : step);
+        gpu.next_clock_sync = t + 100000000;  // 10 per second
+      } else {
+        gpu.next_clock_sync = t + 1000000;
+      }
+    }
     while (!timers_.empty() && timers_.top().t <= now()) {
       Event ev = timers_.top();
       timers_.pop();

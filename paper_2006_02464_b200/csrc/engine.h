@@ -104,6 +104,26 @@ struct InflightExec {
   int64_t started;  // epoch ns (device Exec start)
   int64_t dur;
   bool output;      // false: waiting for Exec end; true: waiting for Output end
+  int64_t ready = 0;     // max(earliest, input_done) when dispatched
+  int64_t dispatched = 0;  // host time of the graph launch
+};
+
+// Executor diagnostics (cuda): where INFER windows are met or missed.
+struct ExecStats {
+  int64_t dispatched = 0;      // INFER graphs launched
+  int64_t host_late = 0;       // rejected by try_start: now > latest (worker.py:230-233)
+  int64_t host_eff_late = 0;   // rejected by try_start: eff > latest (worker.py:237-242)
+  int64_t gate_late = 0;       // rejected by the device gate (Exec start > latest)
+  int64_t done = 0;            // Exec completed on the device
+  int64_t dispatch_delay_sum = 0, dispatch_delay_max = 0;  // host dispatch - max(eff, prev end)
+  int64_t gate_late_sum = 0, gate_late_max = 0;            // device start - latest (rejects)
+  int64_t start_slack_min = INT64_MAX;                      // latest - device start (ok)
+  // back-to-back INFERs (the next one was eligible before the previous Exec ended):
+  // device start - previous device end
+  int64_t busy_gap_sum = 0, busy_gap_max = 0, busy_gaps = 0;
+  int64_t launch_lat_sum = 0, launch_lat_max = 0;    // device start - host dispatch
+  int64_t observe_lat_sum = 0, observe_lat_max = 0;  // host sees the end - device end
+  int64_t clock_resyncs = 0, clock_step_max = 0;      // |offset change| per resync
 };
 
 struct GpuState {
@@ -122,6 +142,10 @@ struct GpuState {
   std::unordered_map<uint64_t, int64_t> action_input_seq;
   std::vector<InflightLoad> loads;
   std::vector<InflightExec> execs;
+  ExecStats stats;
+  int64_t last_exec_end = -1;  // epoch ns of the previous Exec end (device)
+  int64_t last_done_seen = -1; // host time the engine saw it
+  int64_t next_clock_sync = 0; // host time of the next globaltimer resync
 };
 
 enum EvType { EV_DELIVER, EV_WAKE, EV_LOAD_DONE, EV_EXEC_DONE, EV_OUTPUT_DONE };
@@ -165,6 +189,7 @@ class Engine {
   // caller schedules one loop callback per engine event, in the same order as the
   // reference's loop.call_at calls (worker.py:246, 265, 276, 296).
   int sim_run_to(int64_t t, uint64_t seq);
+  int stats(int g, int64_t* out, int max);
   int sim_take_new(int64_t* times, uint64_t* seqs, int max);
   int output(int g, int64_t ref, float* dst, int batch, int classes);
 

@@ -1,6 +1,7 @@
 #include "runtime.h"
 
 #include <algorithm>
+#include <climits>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -87,6 +88,7 @@ Runtime::~Runtime() {
   cudaFreeHost(ring_);
   cudaFreeHost(exec_recs_);
   cudaFreeHost((void*)exec_done_);
+  cudaFreeHost((void*)sync_slot_);
   cudaFreeHost(load_recs_);
   cudaFreeHost(in_recs_);
   cudaFreeHost(out_host_);
@@ -133,6 +135,9 @@ std::string Runtime::open(int device, int64_t pages_total, int64_t page_bytes, i
     CW_TRY(cudaHostAlloc(&p, 64, cudaHostAllocMapped));
     exec_done_ = static_cast<volatile uint64_t*>(p);
     *exec_done_ = 0;
+    CW_TRY(cudaHostAlloc(&p, 64, cudaHostAllocMapped));
+    sync_slot_ = static_cast<volatile uint64_t*>(p);
+    sync_slot_[0] = sync_slot_[1] = 0;
   }
   CW_TRY(cudaHostAlloc(&load_recs_, sizeof(LoadRecord) * kRing, cudaHostAllocMapped));
   CW_TRY(cudaHostAlloc(&in_recs_, sizeof(StampRecord) * kRing, cudaHostAllocMapped));
@@ -163,6 +168,39 @@ std::string Runtime::set_input_pool(const float* data, int n, int64_t bytes) {
 }
 
 std::string Runtime::calibrate_clock() {
+  int64_t off = 0;
+  std::string err = measure_clock_offset(&off);
+  if (err.empty()) gt_offset_ = off;
+  return err;
+}
+
+bool Runtime::resync_clock(int64_t* step) {
+  *step = 0;
+  if (cudaSetDevice(device_) != cudaSuccess) return false;
+  int64_t best_rtt = INT64_MAX, best = 0;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    const uint64_t tag = ++sync_tag_;
+    const int64_t t0 = realtime_ns();
+    launch_stamp(sync_slot_, tag, s_cap_);
+    int64_t t1 = realtime_ns();
+    while (sync_slot_[1] != tag && t1 - t0 < 2000000) t1 = realtime_ns();
+    if (sync_slot_[1] != tag) {
+      cudaStreamSynchronize(s_cap_);  // an SM was busy: give up for now
+      return false;
+    }
+    // the stamp is written ~1.5 us (one PCIe posted write + the host poll) before t1
+    if (t1 - t0 < best_rtt) {
+      best_rtt = t1 - t0;
+      best = (int64_t)sync_slot_[0] - (t1 - 1500);
+    }
+  }
+  if (best_rtt > 40000) return false;
+  *step = best - gt_offset_;
+  gt_offset_ = best;
+  return true;
+}
+
+std::string Runtime::measure_clock_offset(int64_t* offset) {
   CW_TRY(cudaSetDevice(device_));
   uint64_t* slot = nullptr;
   CW_TRY(cudaHostAlloc(&slot, 64, cudaHostAllocMapped));
@@ -193,7 +231,7 @@ std::string Runtime::calibrate_clock() {
   cudaFreeHost(slot);
   if (est.empty()) return "clock calibration failed";
   std::nth_element(est.begin(), est.begin() + est.size() / 2, est.end());
-  gt_offset_ = est[est.size() / 2];
+  *offset = est[est.size() / 2];
   return "";
 }
 

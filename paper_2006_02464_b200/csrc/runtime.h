@@ -166,6 +166,13 @@ class Runtime {
   std::string sync_all();
   int64_t clock_offset() const { return gt_offset_; }  // globaltimer - CLOCK_REALTIME
   std::string calibrate_clock();
+  // A fresh globaltimer - CLOCK_REALTIME measurement (diagnostics: drift since open).
+  std::string measure_clock_offset(int64_t* offset);
+  // Quick re-calibration (call while no INFER runs, so the stamp kernel finds an SM): the
+  // globaltimer drifts against CLOCK_REALTIME by tens of ppm (measured ~1.7 ms / min), far
+  // too much for the controller's 1 ms window slack. One stamp kernel per attempt, accepted
+  // if its host round trip is short; *step = the offset change applied (0 if none).
+  bool resync_clock(int64_t* step);
   const Arch* arch(int id) const;
   cudaStream_t exec_stream() const { return s_exec_; }
   float* slot_in(int32_t s) const { return reinterpret_cast<float*>(io_ + (int64_t)s * slot_bytes_); }
@@ -197,6 +204,8 @@ class Runtime {
   ActionDesc* ring_ = nullptr;  // mapped host
   ExecRecord* exec_recs_ = nullptr;  // mapped host
   volatile uint64_t* exec_done_ = nullptr;  // mapped host: INFERs completed (mk_done)
+  volatile uint64_t* sync_slot_ = nullptr;  // mapped host: resync stamp (time, tag)
+  uint64_t sync_tag_ = 0;
   LoadRecord* load_recs_ = nullptr;  // mapped host
   StampRecord* in_recs_ = nullptr;   // mapped host
   float* out_host_ = nullptr;        // pinned host, kRing x kMaxBatch x out_floats

@@ -123,6 +123,23 @@ class Engine:
         self._new_t = (C.c_int64 * 64)()
         self._new_s = (C.c_uint64 * 64)()
 
+    STAT_NAMES = ("dispatched", "host_late", "host_eff_late", "gate_late", "done",
+                  "dispatch_delay_sum_ns", "dispatch_delay_max_ns", "gate_late_sum_ns",
+                  "gate_late_max_ns", "start_slack_min_ns", "busy_gap_sum_ns",
+                  "busy_gap_max_ns", "busy_gaps", "launch_lat_sum_ns", "launch_lat_max_ns",
+                  "observe_lat_sum_ns", "observe_lat_max_ns", "clock_resyncs",
+                  "clock_step_max_ns")
+
+    def stats(self, gpu: int = 0) -> dict:
+        out = (C.c_int64 * 32)()
+        n = check(lib.cw_engine_stats(self.h, gpu, out, 32), "stats")
+        return dict(zip(self.STAT_NAMES, out[:n]))
+
+    def clock_drift(self, gpu: int = 0) -> int:
+        d = C.c_int64()
+        check(lib.cw_engine_clock_drift(self.h, gpu, C.byref(d)), "clock_drift")
+        return d.value
+
     def executor_info(self) -> dict:
         cpu, rt = C.c_int32(), C.c_int32()
         lib.cw_engine_executor_info(self.h, C.byref(cpu), C.byref(rt))

@@ -80,7 +80,7 @@ def _oracle_sequential(sc):
         assert r[0] == d["action_id"]
         g = d["gpu"] if d["gpu"] < sc["gpu_count"] else 0
         out.append((r[1], w.pages_state(g)))
-        t = max(t, r[3]) + 1
+        t = w.now + 1     # run_until advanced the oracle's clock to the horizon
     return out
 
 
