@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define CW_ABI_VERSION 1
+#define CW_ABI_VERSION 2
 #define CW_MAX_BATCH 16
 
 /* ------------------------------------------------------------------ common */
@@ -41,23 +41,36 @@ int cw_device_count(void);
 
 /* ------------------------------------------------------------------ model artifacts */
 
-/* One op of an architecture's forward pass (built by the Python arch tables). */
+/* One op of an architecture's forward pass (built by the Python arch tables, arch.py).
+ * Activations are NHWC bf16 workspace buffers; a conv reads channels [0, cin) of a buffer
+ * whose channel stride is in_ctot and writes cout channels at channel offset out_coff of
+ * a buffer of stride out_ctot (concats are convs writing disjoint slices of one buffer). */
 typedef struct cw_op {
-  int32_t kind; /* 0 stem im2col, 1 conv (tensor core), 2 maxpool3x3s2, 3 global avgpool, 4 fc */
+  int32_t kind; /* 0 input (NHWC4 rows), 1 conv (tensor core), 2 maxpool, 3 global avgpool,
+                   4 fc, 5 im2col (fp32 images -> [M][64]), 6 BN+ReLU+2x2 avgpool */
   int32_t layer; /* index into the model header (conv / fc weights) */
   int32_t in_buf, out_buf, res_buf; /* workspace buffer ids, -1 = none */
-  int32_t cin, cout, kh, kw, stride, pad, relu;
+  int32_t cin, cout, kh, kw, stride, pad, relu; /* pad: vertical padding */
   int32_t in_h, in_w, out_h, out_w;
-  int32_t kpad; /* stored K = kh*kw*cin rounded up to 64 */
-  int32_t reserved;
+  int32_t kpad;     /* stored K: kh*kw*round_up(cin, 64) (64 per tap for grouped convs) */
+  int32_t pad_w;    /* horizontal padding */
+  int32_t in_ctot;  /* channel stride of the input buffer */
+  int32_t out_ctot; /* channel stride of the output buffer */
+  int32_t out_coff; /* first output channel in that buffer */
+  int32_t cout_pad; /* weight rows = MMA columns: cout rounded up to 64 */
+  int32_t flags;    /* 1: grouped within 64-channel blocks, 2: BN+ReLU on the input (pre_layer) */
+  int32_t pre_layer; /* header entry holding the input BatchNorm's scale/shift, -1 none */
 } cw_op;
 
-/* Where one layer's folded weights (bf16 [rows][k]) and bias (fp32 [rows]) sit in a blob. */
+/* Where one layer's folded weights (bf16 [rows][k]), bias (fp32 [rows]) and input
+ * BatchNorm scale/shift (fp32 [2][cin_pad], DenseNet pre-activation) sit in a blob;
+ * -1 = absent. */
 typedef struct cw_tensor_loc {
   int64_t w_off;
   int64_t b_off;
   int32_t rows;
   int32_t k;
+  int64_t s_off;
 } cw_tensor_loc;
 
 /* ------------------------------------------------------------------ device runtime */
@@ -72,7 +85,9 @@ int cw_rt_register_arch(cw_runtime* rt, int arch_id, const cw_op* ops, int n_ops
 int cw_rt_register_blob(cw_runtime* rt, int blob_id, int arch_id, const void* data, int64_t bytes,
                         const cw_tensor_loc* locs, int n_locs);
 int cw_rt_build(cw_runtime* rt);
-int cw_rt_set_input_pool(cw_runtime* rt, const float* images, int n, int64_t bytes_per_image);
+/* The synthetic request inputs of one arch (request id r -> image r % n). */
+int cw_rt_set_input_pool(cw_runtime* rt, int arch_id, const float* images, int n,
+                         int64_t bytes_per_image);
 int64_t cw_rt_clock_offset(cw_runtime* rt); /* %globaltimer - CLOCK_REALTIME, ns */
 int cw_rt_plan_info(cw_runtime* rt, int arch_id, int batch, int32_t* launches,
                     double* flops_per_image);

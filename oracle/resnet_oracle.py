@@ -18,12 +18,20 @@ import torch
 import torchvision
 
 
+ALIASES = {"inceptionv3": "inception_v3", "resnext50": "resnext50_32x4d"}
+
+
 def torchvision_model(arch_name: str, params: dict[str, np.ndarray]) -> torch.nn.Module:
-    model = getattr(torchvision.models, arch_name)(weights=None)
+    """torchvision's own module for the arch (catalog names accepted), loaded with `params`.
+    Inception-v3's auxiliary classifier (training only; not evaluated in eval mode) keeps
+    torchvision's own init."""
+    name = ALIASES.get(arch_name, arch_name)
+    kw = {"aux_logits": True, "init_weights": False} if name == "inception_v3" else {}
+    model = getattr(torchvision.models, name)(weights=None, **kw)
     sd = model.state_dict()
     new = {}
     for k, v in sd.items():
-        if k.endswith("num_batches_tracked"):
+        if k.endswith("num_batches_tracked") or (k.startswith("AuxLogits.") and k not in params):
             new[k] = v
         else:
             new[k] = torch.from_numpy(np.ascontiguousarray(params[k]))

@@ -25,11 +25,13 @@ class CwError(RuntimeError):
 class cw_op(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "kind", "layer", "in_buf", "out_buf", "res_buf", "cin", "cout", "kh", "kw", "stride",
-        "pad", "relu", "in_h", "in_w", "out_h", "out_w", "kpad", "reserved")]
+        "pad", "relu", "in_h", "in_w", "out_h", "out_w", "kpad", "pad_w", "in_ctot",
+        "out_ctot", "out_coff", "cout_pad", "flags", "pre_layer")]
 
 
 class cw_tensor_loc(C.Structure):
-    _fields_ = [("w_off", C.c_int64), ("b_off", C.c_int64), ("rows", C.c_int32), ("k", C.c_int32)]
+    _fields_ = [("w_off", C.c_int64), ("b_off", C.c_int64), ("rows", C.c_int32), ("k", C.c_int32),
+                ("s_off", C.c_int64)]
 
 
 class cw_model_info(C.Structure):
@@ -88,7 +90,7 @@ SIGNATURES = [
     ("cw_rt_register_blob", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_int64,
                                       C.POINTER(cw_tensor_loc), C.c_int]),
     ("cw_rt_build", C.c_int, [_P]),
-    ("cw_rt_set_input_pool", C.c_int, [_P, _P, C.c_int, C.c_int64]),
+    ("cw_rt_set_input_pool", C.c_int, [_P, C.c_int, _P, C.c_int, C.c_int64]),
     ("cw_rt_clock_offset", C.c_int64, [_P]),
     ("cw_rt_plan_info", C.c_int, [_P, C.c_int, C.c_int, _I32P, C.POINTER(C.c_double)]),
     ("cw_rt_load_sync", C.c_int, [_P, C.c_int, _I32P, C.c_int, _I64P]),

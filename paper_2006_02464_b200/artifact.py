@@ -39,11 +39,17 @@ def from_state_dict(arch_name: str, state_dict: Mapping[str, np.ndarray],
                     page_bytes: int = 16 * 1024 * 1024) -> arch_mod.Blob:
     """Fold and pack a torchvision-named state dict (conv weights + BatchNorm statistics)."""
     spec = arch_mod.build_arch(arch_name)
-    missing = [k for lay in spec.layers
-               for k in ([f"{lay.name}.weight"] + ([f"{lay.name}.bias"] if lay.bn is None else
-                         [f"{lay.bn}.{f}" for f in ("weight", "bias", "running_mean",
-                                                     "running_var")]))
-               if k not in state_dict]
+    bn_keys = ("weight", "bias", "running_mean", "running_var")
+    need = []
+    for lay in spec.layers:
+        if lay.kind != "bn":
+            need.append(f"{lay.name}.weight")
+        if lay.kind == "fc":
+            need.append(f"{lay.name}.bias")
+        for bn in (lay.bn, lay.pre_bn):
+            if bn:
+                need += [f"{bn}.{f}" for f in bn_keys]
+    missing = [k for k in need if k not in state_dict]
     if missing:
         raise ArtifactError(f"{arch_name}: state dict lacks {missing[:4]}"
                             f"{' ...' if len(missing) > 4 else ''}")
@@ -56,7 +62,7 @@ def save(path: str, arch_name: str, blob: arch_mod.Blob) -> None:
     if len(blob.locs) != len(spec.layers):
         raise ArtifactError("blob does not match the architecture")
     data = np.ascontiguousarray(blob.data, dtype=np.uint8)
-    hdr = json.dumps({"arch": arch_name, "page_bytes": blob.page_bytes, "pages": blob.pages,
+    hdr = json.dumps({"arch": spec.name, "page_bytes": blob.page_bytes, "pages": blob.pages,
                       "blob_bytes": int(data.size), "layers": [l.name for l in spec.layers],
                       "locs": [list(map(int, l)) for l in blob.locs],
                       "crc32": zlib.crc32(data.tobytes())}).encode()
@@ -85,12 +91,15 @@ def load(path: str) -> tuple[str, arch_mod.Blob]:
     if zlib.crc32(data.tobytes()) != h["crc32"]:
         raise ArtifactError(f"{path}: blob checksum mismatch")
     spec = arch_mod.build_arch(h["arch"])
-    if h["layers"] != [l.name for l in spec.layers]:
+    if h["layers"] != [l.name or l.pre_bn for l in spec.layers]:
         raise ArtifactError(f"{path}: layer table does not match arch {h['arch']}")
     locs = [tuple(l) for l in h["locs"]]
-    for (w, b, rows, k), lay in zip(locs, spec.layers):
-        if rows != lay.cout or k != lay.kpad or max(w, b) >= data.size:
+    for (w, b, rows, k, so), lay in zip(locs, spec.layers):
+        if lay.kind != "bn" and (rows != lay.cout_pad or k != lay.kpad or
+                                 max(w, b) >= data.size):
             raise ArtifactError(f"{path}: page map entry for {lay.name} is inconsistent")
+        if (so >= 0) != (lay.pre_bn is not None) or so >= data.size:
+            raise ArtifactError(f"{path}: input-BatchNorm entry for {lay.name} is inconsistent")
     if h["pages"] * h["page_bytes"] < data.size:
         raise ArtifactError(f"{path}: blob larger than its pages")
     return h["arch"], arch_mod.Blob(data, locs, h["pages"], h["page_bytes"])

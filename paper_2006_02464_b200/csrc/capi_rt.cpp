@@ -66,8 +66,9 @@ int cw_rt_register_blob(cw_runtime* rt, int blob_id, int arch_id, const void* da
 
 int cw_rt_build(cw_runtime* rt) { return cw::check(rt->rt.build_plans()); }
 
-int cw_rt_set_input_pool(cw_runtime* rt, const float* images, int n, int64_t bytes) {
-  return cw::check(rt->rt.set_input_pool(images, n, bytes));
+int cw_rt_set_input_pool(cw_runtime* rt, int arch_id, const float* images, int n,
+                         int64_t bytes) {
+  return cw::check(rt->rt.set_input_pool(arch_id, images, n, bytes));
 }
 
 int64_t cw_rt_clock_offset(cw_runtime* rt) { return rt->rt.clock_offset(); }

@@ -17,15 +17,18 @@
 
 namespace cw {
 
-constexpr int kMaxLayers = 192;        // ResNet-152 has 156 (155 convs + fc)
+constexpr int kMaxLayers = 192;        // header entries: DenseNet-169 has 173, ResNet-152 156
 constexpr int kMaxBatch = 16;
 constexpr uint32_t kTmapBytes = 128;
 // weight tensor maps: box 64 rows x 64 K at [0, ...), box min(256, Cout) rows at kHdrWideOff
 constexpr uint32_t kHdrWideOff = kMaxLayers * kTmapBytes;
 constexpr uint32_t kHdrBiasOff = 2 * kMaxLayers * kTmapBytes;       // const float* [kMaxLayers]
 constexpr uint32_t kHdrWeightOff = kHdrBiasOff + kMaxLayers * 8;   // const void*  [kMaxLayers]
+// input BatchNorm (DenseNet pre-activation): const float* [kMaxLayers] -> scale[cin_pad],
+// shift[cin_pad]
+constexpr uint32_t kHdrPreOff = kHdrWeightOff + kMaxLayers * 8;
 constexpr uint32_t kHeaderBytes = 65536;                             // reserved at blob start
-static_assert(kHdrWeightOff + kMaxLayers * 8 <= kHeaderBytes, "model header overflow");
+static_assert(kHdrPreOff + kMaxLayers * 8 <= kHeaderBytes, "model header overflow");
 
 struct ActionBlock {
   const uint8_t* hdr;          // model header (page 0 of the model)

@@ -27,6 +27,8 @@ enum MkKind : int32_t {
   MK_AVGPOOL = 4,  // global average pool -> fp32 [b][C]
   MK_FC = 5,       // logits = pooled . W^T + bias -> request output slots
   MK_REDUCE = 6,   // split-K: sum fp32 partial tiles + bias (+ residual) (+ ReLU) -> bf16
+  MK_IM2COL = 7,   // fp32 NCHW request images -> bf16 [M][64] patches (first conv, C=3)
+  MK_BNPOOL = 8,   // BatchNorm + ReLU + 2x2/s2 average pool (DenseNet transition)
 };
 
 constexpr int kMkMaxDeps = 6;
@@ -95,6 +97,15 @@ struct MkLayer {
   float pool_scale;
   // ---- SIMT layers
   int32_t H, W, C, OH, OW, classes, batch, red_parts;
+  // ---- zoo generalisation
+  int32_t pad_w;      // conv: horizontal padding (pad = vertical)
+  int32_t in_ctot;    // SIMT: channel stride of the input buffer
+  int32_t out_ctot;   // SIMT / split-K reduce: channel stride of the output buffer
+  int32_t out_coff;   // ... and the first channel written (conv TMA stores: folded into the map)
+  int32_t n_valid;    // channels actually stored (cout; n_out is cout padded to the N tile)
+  int32_t grouped;    // conv: K walks the tile's own 64-channel block only (ResNeXt groups)
+  int32_t pre_layer;  // BatchNorm + ReLU of the input (conv A tile / pool), header entry; -1
+  int32_t pad2_;
   void* out;              // bf16 NHWC output (conv / reduce / pools), NHWC4 (input)
   const void* res;        // bf16 residual, same shape as out, or null
   float* partial;         // split-K fp32 partials [tile][split][128][bn]
@@ -106,7 +117,7 @@ static_assert(sizeof(MkLayer) % 16 == 0, "MkLayer is copied in 16-byte units");
 // The plan's layer table lives in a __constant__ bank (mk_infer.cu), refreshed by a
 // device-to-device memcpy node at the head of every INFER graph: uniform (ULDC) operand
 // reads for the producer / MMA loops and no shared memory, whatever the depth of the net.
-constexpr int kMkMaxPlanLayers = 250;
+constexpr int kMkMaxPlanLayers = 220;
 static_assert(kMkMaxPlanLayers * sizeof(MkLayer) <= 64000, "constant bank (64 KB)");
 
 struct MkArgs {
@@ -122,6 +133,7 @@ struct MkArgs {
   uint64_t* trace;
   uint32_t flags;            // experiments only (CW_MK_FLAGS): 1 no MMA, 2 no A loads, 4 no B loads
   int32_t pf_depth;          // weight layers L2-prefetched ahead of the running conv
+  int32_t pre_bn;            // 1: some conv applies a BN+ReLU prologue (warps 2-3 run it)
 };
 
 }  // namespace cw

@@ -323,10 +323,14 @@ __device__ __forceinline__ void simt_input(const MkLayer& d, const ActionBlock* 
   }
 }
 
+// 3x3 max pool, stride / padding from the plan (padding = -inf: skipped), input channel
+// stride in_ctot, output at the layer's channel slice of a buffer of stride out_ctot.
 __device__ __forceinline__ void simt_maxpool(const MkLayer& d, int cta, int G, int et) {
   const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(d.in);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(d.out);
   const int chunks = d.C / 8;
   const int total = d.batch * d.OH * d.OW * chunks;
+  const int st = d.stride, pd = d.pad;
   for (int t = cta * kMkEpiThreads + et; t < total; t += G * kMkEpiThreads) {
     const int j = t % chunks;
     const int p = t / chunks;
@@ -338,10 +342,10 @@ __device__ __forceinline__ void simt_maxpool(const MkLayer& d, int cta, int G, i
     for (int r = 0; r < 3; ++r) {
 #pragma unroll
       for (int s = 0; s < 3; ++s) {
-        const int ih = oh * 2 - 1 + r, iw = ow * 2 - 1 + s;
+        const int ih = oh * st - pd + r, iw = ow * st - pd + s;
         if (ih >= 0 && ih < d.H && iw >= 0 && iw < d.W)
           v[r * 3 + s] = __ldcg(reinterpret_cast<const uint4*>(
-              in + (((long long)n * d.H + ih) * d.W + iw) * d.C + j * 8));
+              in + (((long long)n * d.H + ih) * d.W + iw) * d.in_ctot + j * 8));
         else
           v[r * 3 + s] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);  // -inf
       }
@@ -359,30 +363,138 @@ __device__ __forceinline__ void simt_maxpool(const MkLayer& d, int cta, int G, i
     o.y = pack_bf16x2(m[2], m[3]);
     o.z = pack_bf16x2(m[4], m[5]);
     o.w = pack_bf16x2(m[6], m[7]);
-    reinterpret_cast<uint4*>(d.out)[t] = o;
+    *reinterpret_cast<uint4*>(out + (long long)p * d.out_ctot + j * 8) = o;
   }
 }
 
-__device__ __forceinline__ void simt_avgpool(const MkLayer& d, int cta, int G, int et) {
+// Per-channel BatchNorm + ReLU of an input (DenseNet pre-activation): the header's
+// scale[cpad] / shift[cpad] table of layer `pre`, 8 channels from c.
+struct BnRelu8 {
+  float s[8], h[8];
+  __device__ __forceinline__ void load(const float* tab, int cpad, int c) {
+    const float4 s0 = __ldg(reinterpret_cast<const float4*>(tab + c));
+    const float4 s1 = __ldg(reinterpret_cast<const float4*>(tab + c + 4));
+    const float4 h0 = __ldg(reinterpret_cast<const float4*>(tab + cpad + c));
+    const float4 h1 = __ldg(reinterpret_cast<const float4*>(tab + cpad + c + 4));
+    s[0] = s0.x; s[1] = s0.y; s[2] = s0.z; s[3] = s0.w;
+    s[4] = s1.x; s[5] = s1.y; s[6] = s1.z; s[7] = s1.w;
+    h[0] = h0.x; h[1] = h0.y; h[2] = h0.z; h[3] = h0.w;
+    h[4] = h1.x; h[5] = h1.y; h[6] = h1.z; h[7] = h1.w;
+  }
+  __device__ __forceinline__ void apply(float* f) const {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = fmaxf(fmaf(f[e], s[e], h[e]), 0.0f);
+  }
+};
+
+__device__ __forceinline__ const float* pre_table(const uint8_t* hdr, int layer) {
+  return reinterpret_cast<const float* const*>(hdr + kHdrPreOff)[layer];
+}
+
+// Global average pool -> fp32 [b][C]; with an input BatchNorm (DenseNet's norm5 + ReLU)
+// applied to every pixel first.
+__device__ __forceinline__ void simt_avgpool(const MkLayer& d, const uint8_t* hdr, int cta, int G,
+                                             int et) {
   const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(d.in);
   const int chunks = d.C / 8;
   const int total = d.batch * chunks;
   const int HW = d.H * d.W;
+  const int cpad = (d.C + 63) / 64 * 64;
+  const float* tab = d.pre_layer >= 0 ? pre_table(hdr, d.pre_layer) : nullptr;
   float* pooled = reinterpret_cast<float*>(d.out);
   for (int t = cta * kMkEpiThreads + et; t < total; t += G * kMkEpiThreads) {
     const int j = t % chunks;
     const int n = t / chunks;
     float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, f[8];
-    const __nv_bfloat16* base = in + (long long)n * HW * d.C + j * 8;
-    for (int p = 0; p < HW; ++p) {
-      bf16x8_to_f32(__ldcg(reinterpret_cast<const uint4*>(base + (long long)p * d.C)), f);
+    const __nv_bfloat16* base = in + (long long)n * HW * d.in_ctot + j * 8;
+    if (tab) {  // (BN + ReLU per pixel: the scale / shift loads hit L1)
+      for (int p = 0; p < HW; ++p) {
+        bf16x8_to_f32(__ldcg(reinterpret_cast<const uint4*>(base + (long long)p * d.in_ctot)), f);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] += f[e];
+        for (int e = 0; e < 8; ++e)
+          acc[e] += fmaxf(fmaf(f[e], __ldg(tab + j * 8 + e), __ldg(tab + cpad + j * 8 + e)), 0.0f);
+      }
+    } else {
+      for (int p = 0; p < HW; ++p) {
+        bf16x8_to_f32(__ldcg(reinterpret_cast<const uint4*>(base + (long long)p * d.in_ctot)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += f[e];
+      }
     }
     const float inv = 1.0f / (float)HW;
     float4* o = reinterpret_cast<float4*>(pooled + (long long)n * d.C + j * 8);
     o[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
     o[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+  }
+}
+
+// DenseNet transition prefix: BatchNorm + ReLU, then the 2x2 / stride-2 average pool, into
+// a bf16 buffer the transition's 1x1 conv reads (pool before conv: both linear).
+__device__ __forceinline__ void simt_bnpool(const MkLayer& d, const uint8_t* hdr, int cta, int G,
+                                            int et) {
+  const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(d.in);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(d.out);
+  const int chunks = d.C / 8;
+  const int total = d.batch * d.OH * d.OW * chunks;
+  const int cpad = (d.C + 63) / 64 * 64;
+  const float* tab = pre_table(hdr, d.pre_layer);
+  for (int t = cta * kMkEpiThreads + et; t < total; t += G * kMkEpiThreads) {
+    const int j = t % chunks;
+    const int p = t / chunks;
+    const int ow = p % d.OW;
+    const int oh = (p / d.OW) % d.OH;
+    const int n = p / (d.OW * d.OH);
+    BnRelu8 bn;
+    bn.load(tab, cpad, j * 8);
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, f[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int ih = 2 * oh + (q >> 1), iw = 2 * ow + (q & 1);
+      bf16x8_to_f32(__ldcg(reinterpret_cast<const uint4*>(
+                        in + (((long long)n * d.H + ih) * d.W + iw) * d.in_ctot + j * 8)), f);
+      bn.apply(f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += f[e];
+    }
+    uint4 o;
+    o.x = pack_bf16x2(0.25f * acc[0], 0.25f * acc[1]);
+    o.y = pack_bf16x2(0.25f * acc[2], 0.25f * acc[3]);
+    o.z = pack_bf16x2(0.25f * acc[4], 0.25f * acc[5]);
+    o.w = pack_bf16x2(0.25f * acc[6], 0.25f * acc[7]);
+    *reinterpret_cast<uint4*>(out + (long long)p * d.out_ctot + j * 8) = o;
+  }
+}
+
+// First conv of a net whose input is not NHWC4-friendly (Inception-v3: 3 channels at
+// 299x299, 3x3/s2 valid): patches of the fp32 NCHW request images -> bf16 [M][64] rows
+// (k = (r*KW + s)*C + c, zero past KH*KW*C), the A operand of a 1x1-shaped GEMM. One
+// thread per output pixel: consecutive threads read stride-2 columns of the same rows.
+__device__ __forceinline__ void simt_im2col(const MkLayer& d, const ActionBlock* ab, int cta,
+                                            int G, int et) {
+  uint4* out = reinterpret_cast<uint4*>(d.out);
+  const int K = d.kw, C = d.C, st = d.stride, pd = d.pad;
+  const int total = d.batch * d.OH * d.OW;
+  const long long plane = (long long)d.H * d.W;
+  for (int m = cta * kMkEpiThreads + et; m < total; m += G * kMkEpiThreads) {
+    const int ow = m % d.OW;
+    const int oh = (m / d.OW) % d.OH;
+    const int n = m / (d.OW * d.OH);
+    const float* img = ab->in[n];
+    const int kkc = K * K * C;
+    uint4* o = out + (long long)m * 8;
+    for (int q = 0; q < 8; ++q) {
+      float f[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int k = 8 * q + e;
+        const int c = k % C, rs = k / C, s = rs % K, r = rs / K;
+        const int ih = oh * st - pd + r, iw = ow * st - pd + s;
+        f[e] = (k < kkc && ih >= 0 && ih < d.H && iw >= 0 && iw < d.W)
+                   ? __ldg(img + c * plane + ih * d.W + iw) : 0.0f;
+      }
+      o[q] = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
+                        pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));
+    }
   }
 }
 
@@ -594,11 +706,12 @@ __device__ __forceinline__ void simt_reduce(const MkLayer& d, const uint8_t* hdr
   fence_proxy_async_smem();
   named_bar(1, kMkEpiThreads);
   bool issued = false;
-  for (int i = et; i < rr; i += kMkEpiThreads) {
+  const int ncols = min(d.bn, d.n_valid - o.n0);  // padded N-tile columns are not stored
+  for (int i = et; i < rr && ncols > 0; i += kMkEpiThreads) {
     long long m;
     if (!row_pixel(d, o, r0 + i, &m)) continue;
-    bulk_s2g(reinterpret_cast<__nv_bfloat16*>(d.out) + (size_t)m * d.n_out + o.n0,
-             sout_addr + (uint32_t)(i * d.bn * 2), (uint32_t)(d.bn * 2));
+    bulk_s2g(reinterpret_cast<__nv_bfloat16*>(d.out) + (size_t)m * d.out_ctot + o.n0,
+             sout_addr + (uint32_t)(i * d.bn * 2), (uint32_t)(ncols * 2));
     issued = true;
   }
   if (issued) {
@@ -717,6 +830,75 @@ __device__ __forceinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigi
     printf("stem epi: stage %lld, bar %lld, pool %lld\n", s1 - s0, s2 - s1, s3 - s2);
 #endif
 }
+// Warps 2-3: the input BatchNorm + ReLU prologue of DenseNet's pre-activation 1x1 convs:
+// relu(x * scale[c] + shift[c]) applied to the A tile of every k-block in place in shared
+// memory, between its TMA landing (bar_full) and its MMAs (bar_xf). Thread t owns physical
+// 16-byte chunk t & 7 of rows (t >> 3) + 8i: under the 128-byte swizzle (chunk j of row r
+// at j ^ (r & 7)) that is ONE logical chunk, i.e. the same 8 channels, for all its rows,
+// so the k-block's scale/shift of those channels stay in registers. For the other conv
+// layers the warps only follow bar_full's phases (slot walk identical to the MMA warp's).
+__device__ __noinline__ void bn_prologue(const MkLayer* sl, int nl, int cta, int G,
+                                         const uint8_t* hdr, uint8_t* smem, uint32_t bar_full,
+                                         uint32_t bar_xf, int t64) {
+  uint32_t par = 0;
+  const int rg = t64 >> 3, pc = t64 & 7, lc = pc ^ rg;
+  for (int L = 0; L < nl; ++L) {
+    if (sl[L].kind != MK_CONV) continue;
+    const MkLayer& d = sl[L];
+    const int ns = d.slots;
+    const uint32_t sb = (uint32_t)d.slot_bytes;
+    const bool pre = d.pre_layer >= 0;
+    const float* ptab = pre ? reinterpret_cast<const float* const*>(hdr + kHdrPreOff)[d.pre_layer]
+                            : nullptr;
+    const int cpad = d.num_kb * 64;
+    int slot = 0;
+    for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
+      const int z = t % d.splits;
+      const int kb0 = z * d.kb_per_split;
+      int nslots;
+      if (d.mode == 2) {
+        nslots = 1;
+      } else if (d.mode == 3) {
+        nslots = min(d.num_kb, (z + 1) * d.kb_per_split) / 3 - z * d.kb_per_split / 3;
+      } else {
+        const int n = min(d.num_kb, kb0 + d.kb_per_split) - kb0;
+        nslots = (n + d.kpack - 1) / d.kpack;
+      }
+      for (int i = 0; i < nslots; ++i) {
+        if (pre) {  // kpack = 1: slot i holds k-block kb0 + i
+          const int c0 = (kb0 + i) * 64 + lc * 8;
+          const float4 s0 = __ldg(reinterpret_cast<const float4*>(ptab + c0));
+          const float4 s1 = __ldg(reinterpret_cast<const float4*>(ptab + c0 + 4));
+          const float4 h0 = __ldg(reinterpret_cast<const float4*>(ptab + cpad + c0));
+          const float4 h1 = __ldg(reinterpret_cast<const float4*>(ptab + cpad + c0 + 4));
+          const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+          const float sh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+          mbar_wait_to<64>(bar_full + 8 * slot, (par >> slot) & 1, 13);
+          uint8_t* tile = smem + slot * sb;
+#pragma unroll 4
+          for (int r = rg; r < 128; r += 8) {
+            uint4* q = reinterpret_cast<uint4*>(tile + r * 128 + pc * 16);
+            float f[8];
+            bf16x8_to_f32(*q, f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] = fmaf(f[e], sc[e], sh[e]);
+            uint4 o;
+            o.x = pack_bf16x2_relu(f[0], f[1]);
+            o.y = pack_bf16x2_relu(f[2], f[3]);
+            o.z = pack_bf16x2_relu(f[4], f[5]);
+            o.w = pack_bf16x2_relu(f[6], f[7]);
+            *q = o;
+          }
+          fence_proxy_async_smem();  // generic-proxy writes -> the MMA's async-proxy reads
+          mbar_arrive(bar_xf + 8 * slot);
+        }
+        par ^= 1u << slot;
+        if (++slot == ns) slot = 0;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ the kernel
 
 __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_constant__ MkArgs args) {
@@ -748,6 +930,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   const uint32_t bar_simt = bar_tempty + 2 * 8;           // SIMT-layer bulk copies
   const uint32_t bar_res = bar_simt + 8;                  // kMkOutBufs x 8 B: residual chunks
   const uint32_t bar_stemb = bar_res + 8 * kMkOutBufs;    // resident stem weights
+  const uint32_t bar_xf = bar_stemb + 8;                  // kMkMaxSlots: A tile BN-transformed
   uint8_t* bar_area = obufs + kMkOutBufs * kMkOutBufBytes;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_area + kMkBarBytes - 32);
   uint32_t* gen_slot = tmem_slot + 1;
@@ -789,6 +972,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     mbar_init(bar_simt, 1);
     for (int b = 0; b < kMkOutBufs; ++b) mbar_init(bar_res + 8 * b, 1);
     mbar_init(bar_stemb, 1);
+    for (int sl = 0; sl < kMkMaxSlots; ++sl) mbar_init(bar_xf + 8 * sl, 64);
     fence_mbar_init();
     *gen_slot = *reinterpret_cast<const volatile uint32_t*>(args.gen);
   }
@@ -917,11 +1101,12 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                                 ((r * 3 + q) * d.cin_kb + cb) * 64, o.n0 + 64 * j);
               __syncwarp();
             };
+            const int chan0 = d.grouped ? o.n0 : 0;  // grouped: the tile's own channel block
             auto load_a = [&](int g, int s) {
               const int r = g / d.cin_kb, cb = g - r * d.cin_kb;
               if (elect_one())
-                tma_load_4d(sbase + s * sb, ta, bar_full + 8 * s, cb * 64, o.ow0 - 1, o.oh0 + r - 1,
-                            o.img0);
+                tma_load_4d(sbase + s * sb, ta, bar_full + 8 * s, chan0 + cb * 64, o.ow0 - 1,
+                            o.oh0 + r - 1, o.img0);
               __syncwarp();
             };
             auto acquire = [&](int s) {
@@ -982,8 +1167,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           const TileOrigin o = tile_origin(d, tile);
           const int kb0 = z * d.kb_per_split;
           const int kb1 = min(d.num_kb, kb0 + d.kb_per_split);
-          const int wb = o.ow0 * d.stride - d.pad;
+          const int wb = o.ow0 * d.stride - d.pad_w;
           const int hb = o.oh0 * d.stride - d.pad;
+          const int chan0 = d.grouped ? o.n0 : 0;  // grouped: the tile's own channel block
           // A coordinates walk k-blocks in order: (channel block, tap column q, tap row r)
           int a_kb = kb0, a_c0 = 0, a_q = 0, a_r = 0;
           if (d.mode == 1) {
@@ -1032,7 +1218,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
       } else if (mode == 0) {                                                          \
         tma_load_2d(dst_, ta, fb_, a_kb * 64, o.m0);                                   \
       } else if (mode == 1) {                                                          \
-        tma_load_4d(dst_, ta, fb_, a_c0, wb + a_q, hb + a_r, o.img0);                  \
+        tma_load_4d(dst_, ta, fb_, chan0 + a_c0, wb + a_q, hb + a_r, o.img0);          \
       } else {                                                                         \
         tma_load_4d(dst_, ta, fb_, 0, o.ow0, hb + a_kb, o.img0);                       \
       }                                                                                \
@@ -1098,10 +1284,13 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         }
       }
     }
+  } else if ((warp == 2 || warp == 3) && args.pre_bn) {
+    bn_prologue(sl, nl, cta, G, hdr, smem, bar_full, bar_xf, threadIdx.x - 64);
   } else if (warp == 1) {
     {
       // ======================= MMA issuer (whole warp converged; one elected lane issues)
       uint32_t par = 0;  // bit s: parity of the consumptions of slot s so far
+      uint32_t xpar = 0;  // bit s: parity of the BN-transformed consumptions of slot s
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int L = 0; L < nl; ++L) {
@@ -1189,6 +1378,11 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           }
           continue;
         }
+        // a layer with an input BatchNorm consumes each A tile after warps 2-3 transformed
+        // it in place: it waits on bar_xf (own phase bits xpar), and the fill of bar_full
+        // it skipped still advances par
+        const bool pre = d.pre_layer >= 0;
+        const uint32_t bar_in = pre ? bar_xf : bar_full;
         for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
           const int z = t % d.splits;
           const int kb0 = z * d.kb_per_split;
@@ -1197,7 +1391,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           tc_fence_after();
           const uint32_t dtm = tmem + acc * 256;
           for (int i = 0; i < n; i += kpack) {
-            mbar_wait_to<CW_HINT_FULL>(bar_full + 8 * slot, (par >> slot) & 1, 5);
+            mbar_wait_to<CW_HINT_FULL>(bar_in + 8 * slot, ((pre ? xpar : par) >> slot) & 1, 5);
+            if (pre) xpar ^= 1u << slot;
 #ifdef CW_KB_TRACE
             if (cta == 0 && kbm < 64 && lane == 0) kbt[2][kbm] = clock64();
 #endif
@@ -1515,7 +1710,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                        obase + kMkInputStage, bar_simt, simt_phase);
             break;
           case MK_MAXPOOL: simt_maxpool(d, cta, G, et); break;
-          case MK_AVGPOOL: simt_avgpool(d, cta, G, et); break;
+          case MK_AVGPOOL: simt_avgpool(d, hdr, cta, G, et); break;
+          case MK_BNPOOL: simt_bnpool(d, hdr, cta, G, et); break;
+          case MK_IM2COL: simt_im2col(d, ab, cta, G, et); break;
           case MK_FC:
             simt_fc(d, ab, hdr, cta, G, et, reinterpret_cast<float*>(smem), sbase,
                     reinterpret_cast<const __nv_bfloat16*>(obufs), obase,

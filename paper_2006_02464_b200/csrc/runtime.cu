@@ -77,6 +77,7 @@ Runtime::~Runtime() {
       cudaFree(p.d_partial);
     }
     for (void* b : a.bufs) cudaFree(b);
+    if (a.in_pool) cudaFreeHost(a.in_pool);
   }
   for (auto& [id, bl] : blobs_) cudaFreeHost(bl.host);
   for (auto e : exec_events_) cudaEventDestroy(e);
@@ -93,7 +94,6 @@ Runtime::~Runtime() {
   cudaFreeHost(in_recs_);
   cudaFreeHost(out_host_);
   cudaFreeHost(hdr_stage_);
-  cudaFreeHost(in_pool_);
   for (auto s : {s_load_, s_io_, s_cap_, s_out_})
     if (s) cudaStreamDestroy(s);
   if (s_exec_) release_exec_stream(device_);
@@ -155,15 +155,19 @@ std::string Runtime::open(int device, int64_t pages_total, int64_t page_bytes, i
   return calibrate_clock();
 }
 
-std::string Runtime::set_input_pool(const float* data, int n, int64_t bytes) {
+std::string Runtime::set_input_pool(int arch, const float* data, int n, int64_t bytes) {
   CW_TRY(cudaSetDevice(device_));
-  if (in_pool_) CW_TRY(cudaFreeHost(in_pool_));
-  in_pool_ = nullptr;
+  auto it = archs_.find(arch);
+  if (it == archs_.end()) return "unknown arch";
+  Arch& a = it->second;
+  if (bytes != (int64_t)a.in_c * a.in_h * a.in_w * 4) return "input pool image size != arch input";
+  if (a.in_pool) CW_TRY(cudaFreeHost(a.in_pool));
+  a.in_pool = nullptr;
   if (bytes > in_bytes_max_) return "input image larger than IOCache slot";
-  CW_TRY(cudaHostAlloc(&in_pool_, (size_t)n * bytes, cudaHostAllocDefault));
-  memcpy(in_pool_, data, (size_t)n * bytes);
-  in_pool_n_ = n;
-  in_pool_bytes_ = bytes;
+  CW_TRY(cudaHostAlloc(&a.in_pool, (size_t)n * bytes, cudaHostAllocDefault));
+  memcpy(a.in_pool, data, (size_t)n * bytes);
+  a.in_pool_n = n;
+  a.in_pool_bytes = bytes;
   return "";
 }
 
@@ -270,15 +274,21 @@ std::string Runtime::register_arch(int id, const CwOp* ops, int n_ops, int n_lay
     max_b = std::max(max_b, batches[i]);
     a.plans[batches[i]].batch = batches[i];
   }
-  // Workspace buffer sizes at the largest batch.
+  // Workspace buffer sizes at the largest batch (a concat buffer is sized by its channel
+  // stride, whichever op writes or reads it).
   auto grow = [&](int buf, size_t bytes) {
     if (buf < 0) return;
     if ((size_t)buf >= a.buf_bytes.size()) a.buf_bytes.resize(buf + 1, 0);
     a.buf_bytes[buf] = std::max(a.buf_bytes[buf], bytes);
   };
-  for (const CwOp& op : a.ops) {
-    if (op.kind == OP_CONV || op.kind == OP_MAXPOOL || op.kind == OP_AVGPOOL)
-      grow(op.in_buf, (size_t)max_b * op.in_h * op.in_w * op.cin * 2);
+  for (CwOp& op : a.ops) {
+    if (op.in_ctot <= 0) op.in_ctot = op.cin;
+    if (op.out_ctot <= 0) op.out_ctot = op.cout;
+    if (op.pad_w < 0) op.pad_w = op.pad;
+    if (op.kind == OP_CONV && op.cout_pad <= 0) op.cout_pad = (op.cout + 63) / 64 * 64;
+    if (op.kind == OP_CONV || op.kind == OP_MAXPOOL || op.kind == OP_AVGPOOL ||
+        op.kind == OP_BNPOOL)
+      grow(op.in_buf, (size_t)max_b * op.in_h * op.in_w * op.in_ctot * 2);
     if (op.kind == OP_FC) grow(op.in_buf, (size_t)max_b * op.cin * 4);
     if (op.out_buf < 0) continue;
     size_t bytes = 0;
@@ -286,16 +296,21 @@ std::string Runtime::register_arch(int id, const CwOp* ops, int n_ops, int n_lay
       case OP_STEM:  // NHWC4 rows with kMkPadW zero pixels on both sides, kMkPadH zero rows
         bytes = (size_t)max_b * (op.in_h + 2 * kMkPadH) * (op.in_w + 2 * kMkPadW) * 4 * 2;
         break;
-      case OP_CONV: bytes = (size_t)max_b * op.out_h * op.out_w * op.cout * 2; break;
-      case OP_MAXPOOL: bytes = (size_t)max_b * op.out_h * op.out_w * op.cin * 2; break;
+      case OP_IM2COL: bytes = (size_t)max_b * op.out_h * op.out_w * 64 * 2; break;
+      case OP_CONV:
+      case OP_MAXPOOL:
+      case OP_BNPOOL: bytes = (size_t)max_b * op.out_h * op.out_w * op.out_ctot * 2; break;
       case OP_AVGPOOL: bytes = (size_t)max_b * op.cin * 4; break;
       default: break;
     }
     grow(op.out_buf, bytes);
     if (op.kind == OP_CONV)
       a.flops_per_image += 2.0 * op.out_h * op.out_w * op.cout * (double)op.kpad;
-    if (op.kind == OP_CONV && (op.cout % 64 != 0 || (op.kpad % 64 != 0 && op.kpad != 224)))
+    if (op.kind == OP_CONV && (op.cout_pad % 64 != 0 || (op.kpad % 64 != 0 && op.kpad != 224)))
       return "conv shape not 64-aligned";
+    if ((op.kind == OP_CONV || op.kind == OP_MAXPOOL) &&
+        (op.out_ctot % 8 || op.out_coff % 8 || op.in_ctot % 8 != 0) && op.kpad != 224)
+      return "channel strides / offsets must be multiples of 8 (16-byte TMA alignment)";
   }
   archs_[id] = std::move(a);
   return "";
@@ -310,7 +325,12 @@ std::string Runtime::register_blob(int id, int arch, const void* data, size_t by
   b.bytes = bytes;
   b.npages = (int)((bytes + page_bytes_ - 1) / page_bytes_);
   b.locs.assign(locs, locs + n_locs);
+  if (n_locs > kMaxLayers) return "more layers than the model header holds";
   for (const auto& l : b.locs) {
+    if (l.s_off >= 0 && (l.s_off % 16 || l.s_off < (int64_t)kHeaderBytes ||
+                         l.s_off >= (int64_t)bytes))
+      return "bad input-BatchNorm offset";
+    if (l.rows <= 0) continue;  // a BatchNorm-only entry
     const int64_t wend = l.w_off + (int64_t)l.rows * l.k * 2;
     if (l.w_off / page_bytes_ != (wend - 1) / page_bytes_) return "weight tensor straddles a page";
     if (l.w_off % 256 || l.b_off % 16) return "unaligned tensor offset";
@@ -346,7 +366,7 @@ static void box_dims(int nimg, int oh, int ow, int* bw, int* bh, int* bn) {
 //     plus ~0.8 us of fixed latency per tile (bias / residual loads, barriers);
 //   * a split-K reduce layer costs ~3 us plus its partial-tile traffic.
 // Epilogue of task i overlaps the MMAs of task i+1 (two TMEM accumulators).
-static void plan_conv(MkLayer& d, int cout, int G, bool allow_split) {
+static void plan_conv(MkLayer& d, int cout, int G, bool allow_split, bool grouped = false) {
   // a split layer adds a reduce layer and one more whole-GPU dependency (~6 us in the
   // network, measured with tools/sweep_bn.sh + op_profile; CW_SPLIT_US overrides)
   static const double split_us = exp_env("CW_SPLIT_US") ? atof(exp_env("CW_SPLIT_US")) : 6.0;
@@ -358,7 +378,7 @@ static void plan_conv(MkLayer& d, int cout, int G, bool allow_split) {
   for (int i = 0; i < 3; ++i) {
     const int bn = kBn[i];
     if (cout % bn) continue;
-    if (d.mode == 2 && bn != 64) continue;
+    if ((d.mode == 2 || grouped) && bn != 64) continue;  // grouped: one 64-channel block per tile
     const int tiles = d.m_tiles * (cout / bn);
     const int n_tma = 1 + ((bn == std::min(256, cout) && d.kblk == 64) ? 1 : bn / 64);
     const double t_kb = std::max({0.30, 0.08 * n_tma + 0.1, (a_bytes + bn * d.kblk * 2.0) / 140e3});
@@ -384,7 +404,7 @@ static void plan_conv(MkLayer& d, int cout, int G, bool allow_split) {
   // experiment overrides (profiling only): CW_FORCE_BN, CW_FORCE_SPLIT
   if (const char* e = exp_env("CW_FORCE_BN")) {
     const int bn = atoi(e);
-    if (bn > 0 && cout % bn == 0 && (d.mode != 2 || bn == 64)) best_bn = bn;
+    if (bn > 0 && cout % bn == 0 && ((d.mode != 2 && !grouped) || bn == 64)) best_bn = bn;
   }
   if (const char* e = exp_env("CW_FORCE_SPLIT")) {
     const int sp = atoi(e);
@@ -473,6 +493,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
     if (fc_seen) return "the FC op must be the last op of an arch";
     MkLayer d;
     memset(&d, 0, sizeof(d));
+    d.pre_layer = -1;
     d.batch = batch;
     void* in = op.in_buf >= 0 ? a.bufs[op.in_buf] : nullptr;
     void* out = op.out_buf >= 0 ? a.bufs[op.out_buf] : nullptr;
@@ -489,10 +510,14 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
         break;
       }
       case OP_CONV: {
-        if (op.cout > kMkMaxCout) return "conv Cout exceeds kMkMaxCout (shared-memory bias)";
+        const int cout_p = op.cout_pad;
+        if (cout_p > kMkMaxCout) return "conv Cout exceeds kMkMaxCout (shared-memory bias)";
+        const bool grouped = op.flags & OPF_GROUPED64;
+        const bool pre_bn = op.flags & OPF_PRE_BN;
         d.kind = MK_CONV;
         d.wlayer = op.layer;
-        d.n_out = op.cout;
+        d.n_out = cout_p;
+        d.n_valid = op.cout;
         d.relu = op.relu;
         d.nimg = batch;
         d.oh = op.out_h;
@@ -500,12 +525,25 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
         d.kw = op.kw;
         d.stride = op.stride;
         d.pad = op.pad;
+        d.pad_w = op.pad_w;
+        d.grouped = grouped;
+        d.pre_layer = pre_bn ? op.pre_layer : -1;
+        d.out_ctot = op.out_ctot;
+        d.out_coff = op.out_coff;
         d.res = op.res_buf >= 0 ? a.bufs[op.res_buf] : nullptr;
-        d.out = out;
+        if (d.res && (op.out_ctot != op.cout || op.out_coff)) return "residual into a concat slice";
+        // the layer's channel slice of its output buffer: every store of the layer (TMA maps,
+        // split-K reduce rows) addresses it from here with the buffer's channel stride
+        void* out_slice = out ? static_cast<uint8_t*>(out) + (size_t)op.out_coff * 2 : nullptr;
+        d.out = out_slice;
         const CwOp* nxt = oi + 1 < a.ops.size() ? &a.ops[oi + 1] : nullptr;
         const bool from_stem = producer_kind.count(op.in_buf) && producer_kind[op.in_buf] == OP_STEM;
         bool fuse_pool = nxt && nxt->kind == OP_AVGPOOL && nxt->in_buf == op.out_buf &&
-                         op.out_h * op.out_w <= 128 && !from_stem;
+                         op.out_h * op.out_w <= 128 && !from_stem && !(nxt->flags & OPF_PRE_BN) &&
+                         op.out_ctot == op.cout && op.out_coff == 0 && op.cout == cout_p;
+        if (pre_bn && (op.kh != 1 || op.kw != 1 || op.stride != 1 || op.pad || op.pad_w))
+          return "an input BatchNorm prologue needs a 1x1/s1 conv";
+        if (grouped && op.cin != op.cout) return "grouped conv with cin != cout";
         CUtensorMap tm;
         if (from_stem) {
           // 7x7 / stride 2 stem over the NHWC4 rows: k-block = kernel row (32 = 8 px x 4 ch)
@@ -515,8 +553,9 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
           d.kblk = 32;
           d.num_kb = 7;
           const bool fuse_max = nxt && nxt->kind == OP_MAXPOOL && nxt->in_buf == op.out_buf;
-          if (!fuse_max || nxt->out_h * 2 != op.out_h)
-            return "the stem conv must be followed by a 3x3/s2 max pool";
+          if (!fuse_max || nxt->out_h * 2 != op.out_h || nxt->pad != 1 || nxt->stride != 2)
+            return "the stem conv must be followed by a 3x3/s2/p1 max pool";
+          if (cout_p != 64 || op.cout != 64) return "the stem conv must have 64 channels";
           // tiles of 19 pooled columns of one pooled row: 3 x 40 conv pixels (120 rows), all
           // 7 kernel rows in one slot (sub-tiles kMkStemSub apart), weights resident
           d.pool_pw = (kMkStemW - 1) / 2;
@@ -528,39 +567,48 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
           d.tiles_w = (d.OW + d.pool_pw - 1) / d.pool_pw;
           d.tiles_h = d.OH;
           d.m_tiles = d.tiles_w * d.tiles_h * batch;
-          d.out = a.bufs[nxt->out_buf];
+          d.out = static_cast<uint8_t*>(a.bufs[nxt->out_buf]) + (size_t)nxt->out_coff * 2;
+          d.out_ctot = nxt->out_ctot;
           if (!make_tmap_stem(&tm, in, batch, op.in_h + 2 * kMkPadH, op.in_w + 2 * kMkPadW,
                               op.out_w, op.out_h, d.box_w, d.box_h))
             return "tensor map (stem) failed";
-        } else if (!fuse_pool && op.kh == 1 && op.kw == 1 && op.stride == 1 && op.pad == 0) {
+        } else if (!fuse_pool && op.kh == 1 && op.kw == 1 && op.stride == 1 && op.pad == 0 &&
+                   op.pad_w == 0) {
+          // 1x1: A = the [M][cin] matrix of the input buffer (row stride in_ctot; channels
+          // >= cin are out of bounds: zero-filled)
           d.mode = 0;
           d.kblk = 64;
           d.num_kb = op.kpad / 64;
           d.m_total = batch * op.out_h * op.out_w;
           d.m_tiles = (d.m_total + 127) / 128;
-          if (!make_tmap_2d(&tm, in, (uint64_t)op.kpad, (uint64_t)d.m_total, 128))
+          if (!make_tmap_2d(&tm, in, (uint64_t)op.cin, (uint64_t)d.m_total, 128,
+                            (uint64_t)op.in_ctot))
             return "tensor map (2d) failed";
-        } else if (!fuse_pool && op.kh == 3 && op.kw == 3 && op.stride == 1 && op.pad == 1 &&
-                   op.cin % 64 == 0 && op.out_w + 2 <= 128 && exp_env("CW_NO_MODE3") == nullptr) {
+        } else if (!fuse_pool && !pre_bn && op.kh == 3 && op.kw == 3 && op.stride == 1 &&
+                   op.pad == 1 && op.pad_w == 1 && op.out_w + 2 <= 128 &&
+                   exp_env("CW_NO_MODE3") == nullptr) {
           // 3x3 / stride 1: tiles of full rows widened by the 2 padding columns, so the three
           // horizontal taps of a kernel row are ONE TMA box read at row shifts 0, 1, 2 (the
           // two extra columns per row are junk outputs, clipped by the store map)
           d.mode = 3;
           d.kblk = 64;
           d.num_kb = op.kpad / 64;
-          d.cin_kb = op.cin / 64;
+          d.cin_kb = grouped ? 1 : (op.cin + 63) / 64;
+          if (d.num_kb != 9 * d.cin_kb) return "mode-3 conv K layout";
           box_dims(batch, op.out_h, op.out_w + 2, &d.box_w, &d.box_h, &d.box_n);
           d.tiles_w = 1;
           d.tiles_h = (op.out_h + d.box_h - 1) / d.box_h;
           d.m_tiles = d.tiles_h * ((batch + d.box_n - 1) / d.box_n);
-          if (!make_tmap_nhwc(&tm, in, batch, op.in_h, op.in_w, op.cin, d.box_w, d.box_h, d.box_n, 1))
+          if (!make_tmap_nhwc(&tm, in, batch, op.in_h, op.in_w, op.cin, d.box_w, d.box_h,
+                              d.box_n, 1, op.in_ctot))
             return "tensor map (nhwc, mode 3) failed";
         } else {
-          if (op.cin % 64) return "conv Cin must be a multiple of 64";
+          if (pre_bn) return "input BatchNorm prologue on a tap-shifted conv";
           d.mode = 1;
           d.kblk = 64;
           d.num_kb = op.kpad / 64;
-          d.cin_kb = op.cin / 64;
+          d.cin_kb = grouped ? 1 : (op.cin + 63) / 64;
+          if (d.num_kb != op.kh * op.kw * d.cin_kb) return "mode-1 conv K layout";
           if (fuse_pool) {
             d.box_w = op.out_w;
             d.box_h = op.out_h;
@@ -572,34 +620,37 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
           d.tiles_h = (op.out_h + d.box_h - 1) / d.box_h;
           d.m_tiles = d.tiles_w * d.tiles_h * ((batch + d.box_n - 1) / d.box_n);
           if (!make_tmap_nhwc(&tm, in, batch, op.in_h, op.in_w, op.cin, d.box_w, d.box_h, d.box_n,
-                              op.stride))
+                              op.stride, op.in_ctot))
             return "tensor map (nhwc) failed";
         }
         // (the fused pool runs in the epilogue of whole-image tiles: no split-K there)
-        plan_conv(d, op.cout, G, allow_split && !fuse_pool && !d.pool_pw);
+        plan_conv(d, cout_p, G, allow_split && !fuse_pool && !d.pool_pw, grouped);
         d.tmap = (int)p.tmaps.size();
         p.tmaps.push_back(tm);
         d.tmap_out = d.tmap_res = -1;
         if (d.pool_pw) {  // stem: pooled output tiles of pool_pw pixels
           CUtensorMap mo;
-          if (!make_tmap_nhwc(&mo, d.out, batch, d.OH, d.OW, op.cout, d.pool_pw, 1, 1, 1))
+          if (!make_tmap_nhwc(&mo, d.out, batch, d.OH, d.OW, op.cout, d.pool_pw, 1, 1, 1,
+                              d.out_ctot))
             return "tensor map (stem output) failed";
           d.tmap_out = (int)p.tmaps.size();
           p.tmaps.push_back(mo);
         } else if (!fuse_pool && d.splits == 1) {
-          // TMA-store epilogue: 64-column boxes over the output (and residual) tiles
-          auto out_map = [&](CUtensorMap* m, const void* base) {
-            return d.mode == 0 ? make_tmap_2d(m, base, (uint64_t)op.cout, (uint64_t)d.m_total, 128)
-                               : make_tmap_nhwc(m, base, batch, op.out_h, op.out_w, op.cout, d.box_w,
-                                                d.box_h, d.box_n, 1);
+          // TMA-store epilogue: 64-column boxes over the output (and residual) tiles; the
+          // map ends at the layer's real channels (padded N-tile columns are clipped)
+          auto out_map = [&](CUtensorMap* m, const void* base, int ctot) {
+            return d.mode == 0 ? make_tmap_2d(m, base, (uint64_t)op.cout, (uint64_t)d.m_total, 128,
+                                              (uint64_t)ctot)
+                               : make_tmap_nhwc(m, base, batch, op.out_h, op.out_w, op.cout,
+                                                d.box_w, d.box_h, d.box_n, 1, ctot);
           };
           CUtensorMap mo;
-          if (!out_map(&mo, out)) return "tensor map (output) failed";
+          if (!out_map(&mo, out_slice, op.out_ctot)) return "tensor map (output) failed";
           d.tmap_out = (int)p.tmaps.size();
           p.tmaps.push_back(mo);
           if (d.res) {
             CUtensorMap mr;
-            if (!out_map(&mr, d.res)) return "tensor map (residual) failed";
+            if (!out_map(&mr, d.res, op.cout)) return "tensor map (residual) failed";
             d.tmap_res = (int)p.tmaps.size();
             p.tmaps.push_back(mr);
           }
@@ -659,13 +710,19 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
         d.kind = MK_MAXPOOL;
         d.tasks = G;
         d.in = in;
-        d.out = out;
+        d.out = static_cast<uint8_t*>(out) + (size_t)op.out_coff * 2;
         d.H = op.in_h;
         d.W = op.in_w;
         d.C = op.cin;
         d.OH = op.out_h;
         d.OW = op.out_w;
+        d.kw = op.kh;
+        d.stride = op.stride;
+        d.pad = op.pad;
+        d.in_ctot = op.in_ctot;
+        d.out_ctot = op.out_ctot;
         if (op.cin % 8) return "maxpool C must be a multiple of 8";
+        if (op.kh != 3 || op.kw != 3) return "max pool window must be 3x3";
         err = push(d, (int)oi, {op.in_buf}, {op.out_buf});
         break;
       }
@@ -677,7 +734,43 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
         d.H = op.in_h;
         d.W = op.in_w;
         d.C = op.cin;
+        d.in_ctot = op.in_ctot;
+        d.pre_layer = (op.flags & OPF_PRE_BN) ? op.pre_layer : -1;
+        if (op.cin % 8 || op.in_ctot % 8) return "avgpool C must be a multiple of 8";
         err = push(d, (int)oi, {op.in_buf}, {op.out_buf});
+        break;
+      }
+      case OP_BNPOOL: {
+        d.kind = MK_BNPOOL;
+        d.tasks = G;
+        d.in = in;
+        d.out = out;
+        d.H = op.in_h;
+        d.W = op.in_w;
+        d.C = op.cin;
+        d.OH = op.out_h;
+        d.OW = op.out_w;
+        d.in_ctot = op.in_ctot;
+        d.out_ctot = op.out_ctot;
+        d.pre_layer = op.pre_layer;
+        if (op.cin % 8 || op.pre_layer < 0) return "BN pool: C % 8 and an input BatchNorm";
+        err = push(d, (int)oi, {op.in_buf}, {op.out_buf});
+        break;
+      }
+      case OP_IM2COL: {
+        d.kind = MK_IM2COL;
+        d.tasks = G;
+        d.out = out;
+        d.H = op.in_h;
+        d.W = op.in_w;
+        d.C = op.cin;
+        d.OH = op.out_h;
+        d.OW = op.out_w;
+        d.kw = op.kw;
+        d.stride = op.stride;
+        d.pad = op.pad;
+        if (op.kh != op.kw || op.kh * op.kw * op.cin > 64) return "im2col patch > 64 values";
+        err = push(d, (int)oi, {}, {op.out_buf});
         break;
       }
       case OP_FC: {
@@ -742,6 +835,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
     int kpack = 2;
     if (kpack_env > 0) kpack = std::min(kpack_env, 2);  // the MMA loop issues <= 2 per slot
     if ((int)(p.ring_bytes / (kpack * d.sub_bytes)) < min_slots) kpack = 1;
+    if (d.pre_layer >= 0) kpack = 1;  // the BN prologue transforms one A tile per slot
     d.kpack = kpack;
     d.slot_bytes = kpack * d.sub_bytes;
     d.slots = std::min<int>(kMkMaxSlots, p.ring_bytes / d.slot_bytes);
@@ -805,6 +899,9 @@ std::string Runtime::capture(Arch& a, Plan& p) {
   // two weight layers ahead at b=1 (short layers: 277 -> 272 us), one at larger batches
   // (two: b=2 +2.5 us, b=16 +3 us)
   args.pf_depth = p.batch == 1 ? 2 : 1;
+  args.pre_bn = 0;
+  for (const auto& d : p.layers)
+    if (d.kind == MK_CONV && d.pre_layer >= 0) args.pre_bn = 1;
   CW_TRY(cudaStreamBeginCapture(s_cap_, cudaStreamCaptureModeThreadLocal));
   cudaError_t ce = copy_plan(p.d_layers, (int)p.layers.size(), s_cap_);
   launch_gate(ab_, ring_, kRing - 1, ctr_, exec_recs_, s_cap_);
@@ -872,8 +969,10 @@ std::string Runtime::load_async(int blob, const int32_t* pages, int npages, int6
   };
   const float** bias_tab = reinterpret_cast<const float**>(hdr + kHdrBiasOff);
   const void** w_tab = reinterpret_cast<const void**>(hdr + kHdrWeightOff);
+  const float** pre_tab = reinterpret_cast<const float**>(hdr + kHdrPreOff);
   for (size_t l = 0; l < b.locs.size(); ++l) {
     const CwTensorLoc& t = b.locs[l];
+    if (t.s_off >= 0) pre_tab[l] = reinterpret_cast<const float*>(addr(t.s_off));
     if (t.rows <= 0) continue;
     uint8_t* w = addr(t.w_off);
     CUtensorMap* tm = reinterpret_cast<CUtensorMap*>(hdr + l * kTmapBytes);
@@ -913,9 +1012,9 @@ std::string Runtime::input_async(int arch, const int32_t* slots, const uint64_t*
   const Arch* a = this->arch(arch);
   if (!a) return "unknown arch";
   const int64_t bytes = (int64_t)a->in_c * a->in_h * a->in_w * 4;
-  if (!in_pool_ || in_pool_bytes_ != bytes) return "input pool not set for this input shape";
+  if (!a->in_pool || a->in_pool_bytes != bytes) return "input pool not set for this arch";
   for (int j = 0; j < batch; ++j) {
-    const float* src = in_pool_ + (request_ids[j] % in_pool_n_) * (bytes / 4);
+    const float* src = a->in_pool + (request_ids[j] % a->in_pool_n) * (bytes / 4);
     CW_TRY(cudaMemcpyAsync(slot_in(slots[j]), src, bytes, cudaMemcpyHostToDevice, s_io_));
   }
   const uint64_t s = in_seq_++;

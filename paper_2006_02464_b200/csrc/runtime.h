@@ -26,22 +26,25 @@ namespace cw {
 
 // Mirrors struct cw_op in include/cw.h.
 struct CwOp {
-  int32_t kind;  // 0 stem im2col, 1 conv, 2 maxpool, 3 avgpool, 4 fc
+  int32_t kind;  // OpKind
   int32_t layer;
   int32_t in_buf, out_buf, res_buf;
   int32_t cin, cout, kh, kw, stride, pad, relu;
   int32_t in_h, in_w, out_h, out_w;
   int32_t kpad;
-  int32_t reserved;
+  int32_t pad_w, in_ctot, out_ctot, out_coff, cout_pad, flags, pre_layer;
 };
-enum OpKind { OP_STEM = 0, OP_CONV = 1, OP_MAXPOOL = 2, OP_AVGPOOL = 3, OP_FC = 4 };
+enum OpKind { OP_STEM = 0, OP_CONV = 1, OP_MAXPOOL = 2, OP_AVGPOOL = 3, OP_FC = 4,
+              OP_IM2COL = 5, OP_BNPOOL = 6 };
+enum OpFlags { OPF_GROUPED64 = 1, OPF_PRE_BN = 2 };
 
-// Mirrors struct cw_tensor_loc: where one layer's weights/bias sit in a blob.
+// Mirrors struct cw_tensor_loc: where one layer's tensors sit in a blob (-1 = absent).
 struct CwTensorLoc {
   int64_t w_off;  // bf16 [rows][k] at this blob byte offset
   int64_t b_off;  // fp32 [rows]
   int32_t rows;
   int32_t k;
+  int64_t s_off;  // fp32 [2][cin_pad]: BatchNorm scale / shift applied to the layer's input
 };
 
 // One (arch, batch) INFER plan: the megakernel's layer table (mk.h) in device
@@ -74,6 +77,9 @@ struct Arch {
   std::vector<size_t> buf_bytes;
   std::map<int, Plan> plans;
   double flops_per_image = 0;
+  float* in_pool = nullptr;  // pinned synthetic request inputs of this arch (image r % n)
+  int in_pool_n = 0;
+  int64_t in_pool_bytes = 0;
 };
 
 struct Blob {
@@ -181,8 +187,8 @@ class Runtime {
   }
   int64_t io_slots() const { return io_slots_; }
   int64_t output_stride_floats() const { return out_floats_max_; }
-  // Fill the input pool with `n` images of `bytes` each (pinned copy).
-  std::string set_input_pool(const float* data, int n, int64_t bytes);
+  // Fill an arch's input pool with `n` images of `bytes` each (pinned copy).
+  std::string set_input_pool(int arch, const float* data, int n, int64_t bytes);
 
  private:
   std::string build_plan(Arch& a, int batch, bool allow_split = true);
@@ -210,9 +216,6 @@ class Runtime {
   StampRecord* in_recs_ = nullptr;   // mapped host
   float* out_host_ = nullptr;        // pinned host, kRing x kMaxBatch x out_floats
   uint8_t* hdr_stage_ = nullptr;     // pinned host, kRing/16 headers
-  float* in_pool_ = nullptr;         // pinned host input pool
-  int in_pool_n_ = 0;
-  int64_t in_pool_bytes_ = 0;
   uint64_t exec_seq_ = 0;
   uint64_t load_seq_ = 0;
   uint64_t in_seq_ = 0;

@@ -25,10 +25,10 @@ bool tmap_init() {
 }
 
 bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows,
-                  uint32_t box_rows) {
+                  uint32_t box_rows, uint64_t ld) {
   if (!tmap_init()) return false;
   cuuint64_t dims[2] = {k, rows};
-  cuuint64_t strides[1] = {k * 2};
+  cuuint64_t strides[1] = {(ld ? ld : k) * 2};
   cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
   return g_encode(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
@@ -38,10 +38,12 @@ bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows,
 }
 
 bool make_tmap_nhwc(CUtensorMap* out, const void* base, uint64_t n, uint64_t h, uint64_t w,
-                    uint64_t c, uint32_t box_w, uint32_t box_h, uint32_t box_n, uint32_t stride) {
+                    uint64_t c, uint32_t box_w, uint32_t box_h, uint32_t box_n, uint32_t stride,
+                    uint64_t ctot) {
   if (!tmap_init()) return false;
+  const uint64_t ct = ctot ? ctot : c;
   cuuint64_t dims[4] = {c, w, h, n};
-  cuuint64_t strides[3] = {c * 2, w * c * 2, h * w * c * 2};
+  cuuint64_t strides[3] = {ct * 2, w * ct * 2, h * w * ct * 2};
   cuuint32_t box[4] = {64, box_w * stride, box_h * stride, box_n};
   cuuint32_t estr[4] = {1, stride, stride, 1};
   return g_encode(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,

@@ -10,13 +10,18 @@ namespace cw {
 // Resolve cuTensorMapEncodeTiled; returns false when no driver is present.
 bool tmap_init();
 
-// [rows][k] bf16 row-major matrix, box = 64 (k) x box_rows, 128B swizzle.
-bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows, uint32_t box_rows);
+// [rows][k] bf16 row-major matrix (row stride ld elements, default k), box = 64 (k) x
+// box_rows, 128B swizzle. Columns >= k are out of bounds: zero on loads, clipped on stores
+// (a channel slice of a concat buffer: base at the slice, k = its width, ld = the stride).
+bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows, uint32_t box_rows,
+                  uint64_t ld = 0);
 
-// NHWC bf16 activation tensor, box = 64 channels x (box_w*stride) x (box_h*stride) x box_n
-// with element stride `stride` on W and H (loads box_w x box_h x box_n pixels).
+// NHWC bf16 activation tensor of c channels (pixel stride ctot channels, default c), box =
+// 64 channels x (box_w*stride) x (box_h*stride) x box_n with element stride `stride` on W
+// and H (loads box_w x box_h x box_n pixels).
 bool make_tmap_nhwc(CUtensorMap* out, const void* base, uint64_t n, uint64_t h, uint64_t w,
-                    uint64_t c, uint32_t box_w, uint32_t box_h, uint32_t box_n, uint32_t stride);
+                    uint64_t c, uint32_t box_w, uint32_t box_h, uint32_t box_n, uint32_t stride,
+                    uint64_t ctot = 0);
 
 // [rows][cols] fp32 row-major matrix, box = 32 (cols) x box_rows, 128B swizzle.
 bool make_tmap_2d_f32(CUtensorMap* out, const void* base, uint64_t cols, uint64_t rows,

@@ -71,9 +71,9 @@ class DeviceRuntime:
     def build(self):
         check(lib.cw_rt_build(self.h), "build")
 
-    def set_input_pool(self, images: np.ndarray):
+    def set_input_pool(self, images: np.ndarray, arch_id: int = 0):
         images = np.ascontiguousarray(images, dtype=np.float32)
-        check(lib.cw_rt_set_input_pool(self.h, images.ctypes.data, images.shape[0],
+        check(lib.cw_rt_set_input_pool(self.h, arch_id, images.ctypes.data, images.shape[0],
                                        images[0].nbytes), "set_input_pool")
 
     def plan_info(self, arch_id: int, batch: int) -> tuple[int, float]:

@@ -347,17 +347,18 @@ class B200Worker:
                 if weights_dir:  # model artifacts (artifact.py): <dir>/<arch>.cwm
                     from . import artifact
                     name, blob = artifact.load(os.path.join(weights_dir, f"{base}.cwm"))
-                    if name != base or blob.page_bytes != cat.page_bytes:
+                    if name != arch_mod.torchvision_name(base) or blob.page_bytes != cat.page_bytes:
                         raise CwError(f"{base}.cwm: arch {name}, page_bytes {blob.page_bytes} "
                                       f"(catalog: {base}, {cat.page_bytes})")
                     blobs[base] = blob
                     continue
                 blobs[base] = _random_init_blob(base, weights_seed, cat.page_bytes)
-            pool_shape = {(s.in_c, s.in_h, s.in_w) for s in specs.values()}
-            if len(pool_shape) != 1:
-                raise CwError("one input shape per worker is supported")
-            first = next(iter(specs.values()))
-            pool = arch_mod.make_inputs(input_pool, first)
+            # synthetic request inputs per input shape (request id r -> image r % input_pool)
+            pools = {}
+            for spec in specs.values():
+                key = (spec.in_c, spec.in_h, spec.in_w)
+                if key not in pools:
+                    pools[key] = arch_mod.make_inputs(input_pool, spec)
             for g in range(gpu_count):
                 rt = self.engine.runtime(g)
                 for base, spec in specs.items():
@@ -366,7 +367,7 @@ class B200Worker:
                                       for b in p.batch_sizes})
                     rt.register_arch(bi, spec, batches=batches)
                     rt.register_blob(bi, bi, blobs[base])
-                rt.set_input_pool(pool)
+                    rt.set_input_pool(pools[(spec.in_c, spec.in_h, spec.in_w)], bi)
             self.engine.start()
             # poll_results=False: the results are consumed elsewhere (server.serve(native=True)
             # hands the engine to the native serving loop, csrc/net.cpp)

@@ -28,7 +28,7 @@ def test_binding_covers_header():
 
 
 def test_abi_version_and_struct_sizes():
-    assert _lib.lib.cw_abi_version() == 1
-    assert ctypes.sizeof(_lib.cw_op) == 18 * 4
-    assert ctypes.sizeof(_lib.cw_tensor_loc) == 24
+    assert _lib.lib.cw_abi_version() == 2
+    assert ctypes.sizeof(_lib.cw_op) == 24 * 4
+    assert ctypes.sizeof(_lib.cw_tensor_loc) == 32
     assert ctypes.sizeof(_lib.cw_action) == 8 + 4 * 4 + 3 * 8 + 16 * 8
