@@ -63,7 +63,7 @@ constexpr uint32_t kMkScratch = 32768;
 constexpr uint32_t kMkPoolStage = 49152;  // stem: pooled pixels of one tile (TMA-store source)
 constexpr uint32_t kMkTmemCols = 512;      // two accumulators of up to 256 columns
 constexpr int kMkMaxSlots = 16;            // smem ring slots (per-layer slot size)
-constexpr uint32_t kMkBarBytes = 512;
+constexpr uint32_t kMkBarBytes = 1024;
 constexpr int kMkMaxCout = 2048;  // shared-memory bias of one layer (fp32)
 // Epilogue staging: kMkOutBufs buffers of one 128-row x 64-column bf16 chunk (16 KB, 128-byte
 // swizzle): a chunk's residual lands there by TMA, the epilogue rewrites it in place with the

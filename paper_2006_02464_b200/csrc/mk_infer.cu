@@ -173,12 +173,22 @@ __device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
 // in-flight bulk copies (the producer's weight prefetch), ~0.5 us per layer boundary
 // (b=16 595 -> 568 us, b=1 356 -> 324 us). The counter only grows, so the acquire load
 // reads a value of the release sequence of every contributing red.release.
-__device__ __forceinline__ void wait_count(const uint32_t* c, uint32_t target, int site) {
+__device__ __noinline__ void mk_dep_timeout(int site, int layer, int dep, uint32_t have,
+                                            uint32_t want) {
+  printf("cw megakernel: dependency timeout (site %d, block %d, layer %d waits for layer %d: "
+         "count %u of %u)\n", site, blockIdx.x, layer, dep, have, want);
+  __trap();
+}
+
+__device__ __forceinline__ void wait_count(const uint32_t* c, uint32_t target, int site,
+                                           int layer = -1, int dep = -1) {
   if ((int32_t)(ld_relaxed_u32(c) - target) < 0) {
     const uint64_t t0 = globaltimer();
     uint32_t it = 0;
     while ((int32_t)(ld_relaxed_u32(c) - target) < 0) {
-      if ((++it & 63) == 0 && globaltimer() - t0 > kMkTimeoutNs) mk_timeout(site);
+      // (twice the in-layer timeout: a layer that hangs reports its own wait site first)
+      if ((++it & 63) == 0 && globaltimer() - t0 > 2 * kMkTimeoutNs)
+        mk_dep_timeout(site, layer, dep, ld_relaxed_u32(c), target);
     }
   }
   (void)ld_acquire_u32(c);
@@ -192,7 +202,7 @@ __device__ __forceinline__ void wait_deps(const MkLayer* sl, int L, const uint32
   const int nd = sl[L].ndeps;
   for (int i = 0; i < nd; ++i) {
     const int p = sl[L].deps[i];
-    wait_count(counters + p, gen1 * (uint32_t)sl[p].tasks, site);
+    wait_count(counters + p, gen1 * (uint32_t)sl[p].tasks, site, L, p);
   }
 }
 
@@ -832,67 +842,56 @@ __device__ __forceinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigi
 }
 // Warps 2-3: the input BatchNorm + ReLU prologue of DenseNet's pre-activation 1x1 convs:
 // relu(x * scale[c] + shift[c]) applied to the A tile of every k-block in place in shared
-// memory, between its TMA landing (bar_full) and its MMAs (bar_xf). Thread t owns physical
-// 16-byte chunk t & 7 of rows (t >> 3) + 8i: under the 128-byte swizzle (chunk j of row r
-// at j ^ (r & 7)) that is ONE logical chunk, i.e. the same 8 channels, for all its rows,
-// so the k-block's scale/shift of those channels stay in registers. For the other conv
-// layers the warps only follow bar_full's phases (slot walk identical to the MMA warp's).
+// memory, between its TMA landing and its MMAs. The producer completes such a layer's
+// fills on bar_fpre (not bar_full) and the MMA waits on bar_xf, so these warps only see the
+// phases of BN layers: they can neither run ahead of a fill (parity aliasing) nor fall two
+// phases behind one (the slot is refilled only after the MMA, i.e. after them). Thread t
+// owns physical 16-byte chunk t & 7 of rows (t >> 3) + 8i: under the 128-byte swizzle (chunk
+// j of row r at j ^ (r & 7)) that is ONE logical chunk, i.e. the same 8 channels, for all
+// its rows, so the k-block's scale/shift of those channels stay in registers.
 __device__ __noinline__ void bn_prologue(const MkLayer* sl, int nl, int cta, int G,
-                                         const uint8_t* hdr, uint8_t* smem, uint32_t bar_full,
+                                         const uint8_t* hdr, uint8_t* smem, uint32_t bar_fpre,
                                          uint32_t bar_xf, int t64) {
-  uint32_t par = 0;
+  uint32_t par = 0;  // bit s: parity of the BN-layer fills of slot s seen so far
   const int rg = t64 >> 3, pc = t64 & 7, lc = pc ^ rg;
   for (int L = 0; L < nl; ++L) {
-    if (sl[L].kind != MK_CONV) continue;
+    if (sl[L].kind != MK_CONV || sl[L].pre_layer < 0) continue;
     const MkLayer& d = sl[L];
     const int ns = d.slots;
     const uint32_t sb = (uint32_t)d.slot_bytes;
-    const bool pre = d.pre_layer >= 0;
-    const float* ptab = pre ? reinterpret_cast<const float* const*>(hdr + kHdrPreOff)[d.pre_layer]
-                            : nullptr;
+    const float* ptab = reinterpret_cast<const float* const*>(hdr + kHdrPreOff)[d.pre_layer];
     const int cpad = d.num_kb * 64;
     int slot = 0;
     for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
-      const int z = t % d.splits;
-      const int kb0 = z * d.kb_per_split;
-      int nslots;
-      if (d.mode == 2) {
-        nslots = 1;
-      } else if (d.mode == 3) {
-        nslots = min(d.num_kb, (z + 1) * d.kb_per_split) / 3 - z * d.kb_per_split / 3;
-      } else {
-        const int n = min(d.num_kb, kb0 + d.kb_per_split) - kb0;
-        nslots = (n + d.kpack - 1) / d.kpack;
-      }
-      for (int i = 0; i < nslots; ++i) {
-        if (pre) {  // kpack = 1: slot i holds k-block kb0 + i
-          const int c0 = (kb0 + i) * 64 + lc * 8;
-          const float4 s0 = __ldg(reinterpret_cast<const float4*>(ptab + c0));
-          const float4 s1 = __ldg(reinterpret_cast<const float4*>(ptab + c0 + 4));
-          const float4 h0 = __ldg(reinterpret_cast<const float4*>(ptab + cpad + c0));
-          const float4 h1 = __ldg(reinterpret_cast<const float4*>(ptab + cpad + c0 + 4));
-          const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-          const float sh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-          mbar_wait_to<64>(bar_full + 8 * slot, (par >> slot) & 1, 13);
-          uint8_t* tile = smem + slot * sb;
-#pragma unroll 4
-          for (int r = rg; r < 128; r += 8) {
-            uint4* q = reinterpret_cast<uint4*>(tile + r * 128 + pc * 16);
-            float f[8];
-            bf16x8_to_f32(*q, f);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) f[e] = fmaf(f[e], sc[e], sh[e]);
-            uint4 o;
-            o.x = pack_bf16x2_relu(f[0], f[1]);
-            o.y = pack_bf16x2_relu(f[2], f[3]);
-            o.z = pack_bf16x2_relu(f[4], f[5]);
-            o.w = pack_bf16x2_relu(f[6], f[7]);
-            *q = o;
-          }
-          fence_proxy_async_smem();  // generic-proxy writes -> the MMA's async-proxy reads
-          mbar_arrive(bar_xf + 8 * slot);
-        }
+      const int kb0 = (t % d.splits) * d.kb_per_split;
+      const int n = min(d.num_kb, kb0 + d.kb_per_split) - kb0;  // kpack = 1: a k-block per slot
+      for (int i = 0; i < n; ++i) {
+        const int c0 = (kb0 + i) * 64 + lc * 8;
+        const float4 s0 = __ldg(reinterpret_cast<const float4*>(ptab + c0));
+        const float4 s1 = __ldg(reinterpret_cast<const float4*>(ptab + c0 + 4));
+        const float4 h0 = __ldg(reinterpret_cast<const float4*>(ptab + cpad + c0));
+        const float4 h1 = __ldg(reinterpret_cast<const float4*>(ptab + cpad + c0 + 4));
+        const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+        const float sh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        mbar_wait_to<64>(bar_fpre + 8 * slot, (par >> slot) & 1, 13);
         par ^= 1u << slot;
+        uint8_t* tile = smem + slot * sb;
+#pragma unroll 4
+        for (int r = rg; r < 128; r += 8) {
+          uint4* q = reinterpret_cast<uint4*>(tile + r * 128 + pc * 16);
+          float f[8];
+          bf16x8_to_f32(*q, f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) f[e] = fmaf(f[e], sc[e], sh[e]);
+          uint4 o;
+          o.x = pack_bf16x2_relu(f[0], f[1]);
+          o.y = pack_bf16x2_relu(f[2], f[3]);
+          o.z = pack_bf16x2_relu(f[4], f[5]);
+          o.w = pack_bf16x2_relu(f[6], f[7]);
+          *q = o;
+        }
+        fence_proxy_async_smem();  // generic-proxy writes -> the MMA's async-proxy reads
+        mbar_arrive(bar_xf + 8 * slot);
         if (++slot == ns) slot = 0;
       }
     }
@@ -931,6 +930,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   const uint32_t bar_res = bar_simt + 8;                  // kMkOutBufs x 8 B: residual chunks
   const uint32_t bar_stemb = bar_res + 8 * kMkOutBufs;    // resident stem weights
   const uint32_t bar_xf = bar_stemb + 8;                  // kMkMaxSlots: A tile BN-transformed
+  const uint32_t bar_fpre = bar_xf + 8 * kMkMaxSlots;     // kMkMaxSlots: fills of BN layers
   uint8_t* bar_area = obufs + kMkOutBufs * kMkOutBufBytes;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_area + kMkBarBytes - 32);
   uint32_t* gen_slot = tmem_slot + 1;
@@ -972,7 +972,10 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     mbar_init(bar_simt, 1);
     for (int b = 0; b < kMkOutBufs; ++b) mbar_init(bar_res + 8 * b, 1);
     mbar_init(bar_stemb, 1);
-    for (int sl = 0; sl < kMkMaxSlots; ++sl) mbar_init(bar_xf + 8 * sl, 64);
+    for (int sl = 0; sl < kMkMaxSlots; ++sl) {
+      mbar_init(bar_xf + 8 * sl, 64);
+      mbar_init(bar_fpre + 8 * sl, 1);
+    }
     fence_mbar_init();
     *gen_slot = *reinterpret_cast<const volatile uint32_t*>(args.gen);
   }
@@ -1158,6 +1161,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         const int nbox = wide ? 1 : d.bn / 64;
         const int cin = d.cin_kb * 64;
         const int mode = d.mode, kw = d.kw, kblk = d.kblk, kpack = d.kpack;
+        // a BN-prologue layer's fills complete on bar_fpre (warps 2-3 transform, then bar_xf)
+        const uint32_t fullb = d.pre_layer >= 0 ? bar_fpre : bar_full;
         const uint32_t b_off = (uint32_t)d.b_off, sub = (uint32_t)d.sub_bytes;
         int slot = 0;
         bool waited = false;
@@ -1184,7 +1189,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   do {                                                                              \
     mbar_wait_to<CW_HINT_EMPTY>(bar_empty + 8 * (s_), ((par >> (s_)) & 1) ^ 1, 3);  \
     par ^= 1u << (s_);                                                              \
-    if (elect_one()) mbar_arrive_expect_tx(bar_full + 8 * (s_), tx1 * (uint32_t)(m_)); \
+    if (elect_one()) mbar_arrive_expect_tx(fullb + 8 * (s_), tx1 * (uint32_t)(m_));    \
     __syncwarp();                                                                   \
   } while (0)
 #define CW_LOAD_B(kb_, dst0_, s_)                                                   \
@@ -1193,7 +1198,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     const int kx_ = (kb_) * kblk;                                                   \
     if (elect_one())                                                                \
       for (int j = 0; j < (no_b ? 0 : nbox); ++j)                                   \
-        tma_load_2d(dst_ + j * b_box, tb, bar_full + 8 * (s_), kx_, o.n0 + 64 * j);  \
+        tma_load_2d(dst_ + j * b_box, tb, fullb + 8 * (s_), kx_, o.n0 + 64 * j);      \
     __syncwarp();                                                                   \
   } while (0)
 #define CW_ADV_A()                                                                      \
@@ -1212,7 +1217,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   } while (0)
 #define CW_LOAD_A(dst_, s_)                                                            \
   do {                                                                                 \
-    const uint32_t fb_ = bar_full + 8 * (s_);                                          \
+    const uint32_t fb_ = fullb + 8 * (s_);                                             \
     if (elect_one()) {                                                                 \
       if (no_a) {                                                                      \
       } else if (mode == 0) {                                                          \
@@ -1285,7 +1290,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
       }
     }
   } else if ((warp == 2 || warp == 3) && args.pre_bn) {
-    bn_prologue(sl, nl, cta, G, hdr, smem, bar_full, bar_xf, threadIdx.x - 64);
+    bn_prologue(sl, nl, cta, G, hdr, smem, bar_fpre, bar_xf, threadIdx.x - 64);
+
   } else if (warp == 1) {
     {
       // ======================= MMA issuer (whole warp converged; one elected lane issues)
@@ -1392,11 +1398,10 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           const uint32_t dtm = tmem + acc * 256;
           for (int i = 0; i < n; i += kpack) {
             mbar_wait_to<CW_HINT_FULL>(bar_in + 8 * slot, ((pre ? xpar : par) >> slot) & 1, 5);
-            if (pre) xpar ^= 1u << slot;
 #ifdef CW_KB_TRACE
             if (cta == 0 && kbm < 64 && lane == 0) kbt[2][kbm] = clock64();
 #endif
-            par ^= 1u << slot;
+            (pre ? xpar : par) ^= 1u << slot;  // (a BN layer's fills never touch bar_full)
             if (first) {
               if (lane == 0 && args.trace) args.trace[((size_t)L * G + cta) * 4 + 3] = globaltimer();
               first = false;

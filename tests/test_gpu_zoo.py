@@ -39,7 +39,8 @@ def net(request, gpu):
     name = request.param
     spec = arch.build_arch(name)
     blob = arch.pack_blob(spec, arch.fold(spec, arch.make_params(spec, seed=0)))
-    rt = DeviceRuntime(device=gpu, pages_total=blob.pages + 3, io_slots=16)
+    rt = DeviceRuntime(device=gpu, pages_total=blob.pages + 3, io_slots=16,
+                       in_bytes_max=spec.in_c * spec.in_h * spec.in_w * 4)
     rt.__enter__()
     rt.register_arch(0, spec, batches=(1, 2, 8, 16))
     rt.register_blob(0, 0, blob)

@@ -15,14 +15,15 @@ from paper_2006_02464_b200.device import DeviceRuntime  # noqa: E402
 def run(b, h, cin, cout, k, stride):
     pad = k // 2
     spec = arch.ArchSpec("probe")
-    spec.layers.append(arch.Layer(0, "c", "bn", cin, cout, k, stride, pad, k * k * cin))
+    spec.layers.append(arch.Layer(0, "c", "bn", cin, cout, k, k, stride, pad, pad, k * k * cin,
+                                  cout_pad=cout))
     oh = (h + 2 * pad - k) // stride + 1
     spec.ops.append(arch._op(arch.OP_CONV, layer=0, in_buf=0, out_buf=1, cin=cin, cout=cout, kh=k,
                              kw=k, stride=stride, pad=pad, relu=1, in_h=h, in_w=h, out_h=oh,
                              out_w=oh, kpad=k * k * cin))
     rng = np.random.default_rng(0)
     wt = rng.standard_normal((cout, k * k * cin)).astype(np.float32) * 0.01
-    blob = arch.pack_blob(spec, [(wt, np.zeros(cout, np.float32))])
+    blob = arch.pack_blob(spec, [(wt, np.zeros(cout, np.float32), None)])
     with DeviceRuntime(pages_total=8, io_slots=16) as rt:
         rt.register_arch(0, spec, batches=(b,))
         rt.register_blob(0, 0, blob)
