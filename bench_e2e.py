@@ -161,26 +161,37 @@ def run_controller(addresses, cat_text: str, epoch_ns: int, horizon_ns: int, gro
     }
 
 
+_READY_S: dict = {}  # observed worker startup time per (kind, catalog size), seconds
+
+
 def run_leg(kind: str, group_fn, copies: int, pages: int, horizon_ns: int, devices,
-            startup_s: float, seed: int = 0, workdir: str | None = None) -> dict:
+            startup_s: float, seed: int = 0, workdir: str | None = None,
+            cat_text: str | None = None) -> dict:
     """Start one worker per device, run the reference controller against all of them for
-    `horizon_ns`, score with summarize. `group_fn(workload)` builds the client groups."""
+    `horizon_ns`, score with summarize. `group_fn(workload)` builds the client groups;
+    `cat_text` overrides the ResNet-50 x `copies` catalog."""
     harness, workload, profiles = sloserve()
     workdir = workdir or tempfile.mkdtemp(prefix="cw_bench_")
-    cat = catalog_text(kind, copies)
+    cat = cat_text if cat_text is not None else catalog_text(kind, copies)
     cat_path = os.path.join(workdir, f"catalog_{kind}.txt")
     with open(cat_path, "w") as f:
         f.write(cat)
     # One shared CLOCK_REALTIME epoch, set in the future so it is "now" when the controller
     # starts, after the workers have built their plans (SURVEY App. A: an old epoch would
-    # back-date the first arrivals).
-    epoch = time.time_ns() + int(startup_s * 1e9)
+    # back-date the first arrivals). The lead is the startup time observed for the same kind
+    # of worker earlier in this process (+50 %), else `startup_s`.
+    key = (kind, len(cat))
+    lead = min(startup_s, 1.5 * _READY_S[key] + 3.0) if key in _READY_S else startup_s
+    t_launch = time.time()
+    epoch = time.time_ns() + int(lead * 1e9)
     procs, addrs = [], []
     try:
         for i, dev in enumerate(devices):
-            p, port = start_worker(kind, cat_path, pages, epoch, dev, i, timeout_s=startup_s)
+            p, port = start_worker(kind, cat_path, pages, epoch, dev, i,
+                                   timeout_s=max(startup_s, 300.0))
             procs.append(p)
             addrs.append(f"127.0.0.1:{port}")
+        _READY_S[key] = max(_READY_S.get(key, 0.0), time.time() - t_launch)
         wait = epoch - time.time_ns()
         if wait > 0:
             time.sleep(wait / 1e9)
@@ -198,5 +209,7 @@ def run_leg(kind: str, group_fn, copies: int, pages: int, horizon_ns: int, devic
             except subprocess.TimeoutExpired:
                 p.kill()
     out["workers"] = len(devices)
+    out["epoch_lead_s"] = lead
+    out["epoch_late_s"] = max(0.0, -wait / 1e9)
     out["worker_kind"] = kind
     return out

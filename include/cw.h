@@ -47,7 +47,8 @@ int cw_device_count(void);
  * a buffer of stride out_ctot (concats are convs writing disjoint slices of one buffer). */
 typedef struct cw_op {
   int32_t kind; /* 0 input (NHWC4 rows), 1 conv (tensor core), 2 maxpool, 3 global avgpool,
-                   4 fc, 5 im2col (fp32 images -> [M][64]), 6 BN+ReLU+2x2 avgpool */
+                   4 fc, 5 im2col (fp32 images -> [M][64]), 6 BN+ReLU+2x2 avgpool,
+                   7 softmax of the FC's logits (optional last op) */
   int32_t layer; /* index into the model header (conv / fc weights) */
   int32_t in_buf, out_buf, res_buf; /* workspace buffer ids, -1 = none */
   int32_t cin, cout, kh, kw, stride, pad, relu; /* pad: vertical padding */

@@ -41,7 +41,7 @@ HEADER_BYTES = 65536
 BN_EPS = 1e-5
 
 # op kinds (mirror CwOp in csrc/runtime.h and cw_op in include/cw.h)
-OP_STEM, OP_CONV, OP_MAXPOOL, OP_AVGPOOL, OP_FC, OP_IM2COL, OP_BNPOOL = range(7)
+OP_STEM, OP_CONV, OP_MAXPOOL, OP_AVGPOOL, OP_FC, OP_IM2COL, OP_BNPOOL, OP_SOFTMAX = range(8)
 # op flags
 F_GROUPED64 = 1   # grouped conv, groups within 64-channel blocks (ResNeXt): K = taps x 64
 F_PRE_BN = 2      # BatchNorm + ReLU applied to the A operand in shared memory (DenseNet)
@@ -480,14 +480,18 @@ def torchvision_name(name: str) -> str:
     return ALIASES.get(name, name)
 
 
-def build_arch(name: str) -> ArchSpec:
-    """Layer table + op list of a torchvision-definition network (catalog base name)."""
+def build_arch(name: str, softmax: bool = False) -> ArchSpec:
+    """Layer table + op list of a torchvision-definition network (catalog base name).
+    softmax=True appends the softmax tail: the request outputs are class probabilities
+    instead of logits."""
     tv = torchvision_name(name)
     if tv not in _BUILDERS:
         raise KeyError(f"no B200 implementation for architecture {name!r} "
                        f"(supported: {', '.join(SUPPORTED)})")
     spec = _BUILDERS[tv](tv)
     spec.name = tv
+    if softmax:
+        spec.ops.append(_op(OP_SOFTMAX, cin=spec.classes, cout=spec.classes))
     return spec
 
 

@@ -5,7 +5,7 @@
         [--gpus N] [--pages N] [--clock wall] [--jitter none] [--seed N]
         [--epoch-ns N] [--telemetry FILE]
         [--worker-id N] [--devices 0,1,...] [--mode cuda|sim] [--weights-seed N]
-        [--native-net] [--weights DIR]
+        [--native-net] [--weights DIR] [--softmax]
     python -m paper_2006_02464_b200 pack --arch resnet50 (--state-dict SD.npz | --random-seed N)
         --out resnet50.cwm
 """
@@ -50,6 +50,8 @@ def main(argv=None) -> int:
                    help="serve the controller socket from native threads (csrc/net.cpp)")
     p.add_argument("--weights", default="",
                    help="directory of <arch>.cwm model artifacts (default: random-init weights)")
+    p.add_argument("--softmax", action="store_true",
+                   help="INFER outputs class probabilities (softmax tail) instead of logits")
     k = sub.add_parser("pack", help="fold + pack a torchvision-named state dict (.npz) into a "
                                     ".cwm model artifact")
     k.add_argument("--arch", required=True)
@@ -71,7 +73,7 @@ def main(argv=None) -> int:
                  ready_fd=args.ready_fd if args.ready_fd >= 0 else None,
                  worker_id=args.worker_id, devices=devices, mode=args.mode,
                  weights_seed=args.weights_seed, native=args.native_net,
-                 weights_dir=args.weights or None)
+                 weights_dir=args.weights or None, softmax=args.softmax)
     return 0
 
 

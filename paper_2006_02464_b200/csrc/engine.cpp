@@ -132,6 +132,7 @@ void Engine::call_at(int64_t t, Event ev) {
 int Engine::submit(const cw_action& a, int64_t at) {
   if (failed_) return fail("engine failed after a device error; see the first error");
   if (cfg_.mode == 0) {
+    std::lock_guard<std::mutex> lk(state_mu_);
     auto* copy = new cw_action(a);
     Event ev{};
     ev.type = EV_DELIVER;
@@ -162,6 +163,7 @@ int Engine::poll(cw_result* out, int max, int64_t timeout_us) {
 
 int Engine::sim_deliver(const cw_action& a, int64_t now) {
   if (cfg_.mode != 0) return -1;
+  std::lock_guard<std::mutex> lk(state_mu_);  // (state readers: pages(), io_in_use())
   sim_now_ = std::max(sim_now_, now);
   on_action(new cw_action(a));
   return 0;
@@ -183,6 +185,7 @@ int Engine::stats(int g, int64_t* out, int max) {
 
 int Engine::sim_run_to(int64_t t, uint64_t seq) {
   if (cfg_.mode != 0) return -1;
+  std::lock_guard<std::mutex> lk(state_mu_);
   int n = 0;
   while (!timers_.empty()) {
     const Event& top = timers_.top();
@@ -203,6 +206,7 @@ int Engine::sim_run_to(int64_t t, uint64_t seq) {
 }
 
 int Engine::sim_take_new(int64_t* times, uint64_t* seqs, int max) {
+  std::lock_guard<std::mutex> lk(state_mu_);
   int n = 0;
   while (n < max && !sim_new_.empty()) {
     times[n] = sim_new_.front().first;
@@ -215,6 +219,7 @@ int Engine::sim_take_new(int64_t* times, uint64_t* seqs, int max) {
 
 int Engine::sim_run(int64_t until) {
   if (cfg_.mode != 0) return -1;
+  std::lock_guard<std::mutex> lk(state_mu_);
   // SimLoop.run_until (timebase.py:79-89).
   int n = 0;
   while (!timers_.empty()) {

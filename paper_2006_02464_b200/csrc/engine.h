@@ -171,7 +171,10 @@ class Engine {
   int poll(cw_result* out, int max, int64_t timeout_us);
   int sim_run(int64_t until);
   int64_t now() const;
-  int64_t next_event_time() const { return timers_.empty() ? -1 : timers_.top().t; }
+  int64_t next_event_time() {
+    std::lock_guard<std::mutex> lk(state_mu_);
+    return timers_.empty() ? -1 : timers_.top().t;
+  }
   int pages(int g, int64_t* free, int32_t* models, int32_t* counts, int max, int32_t* n);
   int64_t io_in_use(int g);
   // A CUDA failure is fatal to the engine (never turned into a protocol status): the engine

@@ -29,6 +29,7 @@ enum MkKind : int32_t {
   MK_REDUCE = 6,   // split-K: sum fp32 partial tiles + bias (+ residual) (+ ReLU) -> bf16
   MK_IM2COL = 7,   // fp32 NCHW request images -> bf16 [M][64] patches (first conv, C=3)
   MK_BNPOOL = 8,   // BatchNorm + ReLU + 2x2/s2 average pool (DenseNet transition)
+  MK_SOFTMAX = 9,  // logits -> probabilities in the request output slots (optional tail)
 };
 
 constexpr int kMkMaxDeps = 6;
@@ -134,6 +135,7 @@ struct MkArgs {
   uint32_t flags;            // experiments only (CW_MK_FLAGS): 1 no MMA, 2 no A loads, 4 no B loads
   int32_t pf_depth;          // weight layers L2-prefetched ahead of the running conv
   int32_t pre_bn;            // 1: some conv applies a BN+ReLU prologue (warps 2-3 run it)
+  int32_t softmax;           // 1: the last layer is a softmax tail (warps 2-3 run it)
 };
 
 }  // namespace cw

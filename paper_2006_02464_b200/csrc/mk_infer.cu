@@ -58,7 +58,10 @@ __constant__ MkLayer c_plan[kMkMaxPlanLayers];  // the running INFER's plan (see
 #define CW_RES_DIST 3
 #endif
 constexpr int kResDist = CW_RES_DIST;
-constexpr uint64_t kMkTimeoutNs = 2000000000ull;  // 2 s: far above any INFER
+#ifndef CW_TIMEOUT_NS
+#define CW_TIMEOUT_NS 2000000000ull  // 2 s: far above any INFER (sanitizer builds: raised)
+#endif
+constexpr uint64_t kMkTimeoutNs = CW_TIMEOUT_NS;
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
@@ -649,6 +652,42 @@ __device__ __forceinline__ void simt_fc(const MkLayer& d, const ActionBlock* ab,
 #endif
     named_bar(1, kMkEpiThreads);  // weights (and sred) read before the next block's copy
   }
+}
+
+// Optional softmax tail (the last plan layer), run by warps 2-3 so the epilogue warps' code
+// (and register allocation) is untouched: once the FC layer completed, request n's logits
+// in its IOCache output slot -> probabilities in place. One CTA per request; 64 threads,
+// max and sum of exp by warp shuffles and two shared-memory words per warp.
+__device__ __noinline__ void softmax_tail(const MkLayer* sl, int nl, int cta, int G,
+                                          const ActionBlock* ab, uint32_t* counters,
+                                          uint32_t gen1, float* sred, int t64) {
+  const MkLayer& d = sl[nl - 1];
+  if (first_task(d, cta, G) >= d.tasks) return;
+  if (t64 == 0) wait_deps(sl, nl - 1, counters, gen1, 14);
+  named_bar(3, 64);
+  const int lane = t64 & 31, w = t64 >> 5;
+  int done = 0;
+  for (int n = first_task(d, cta, G); n < d.tasks; n += G, ++done) {
+    float* x = ab->out[n];
+    float m = -INFINITY;
+    for (int j = t64; j < d.classes; j += 64) m = fmaxf(m, __ldcg(x + j));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) sred[w] = m;
+    named_bar(3, 64);
+    m = fmaxf(sred[0], sred[1]);
+    float s = 0.0f;
+    for (int j = t64; j < d.classes; j += 64) s += __expf(__ldcg(x + j) - m);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) sred[2 + w] = s;
+    named_bar(3, 64);
+    const float inv = 1.0f / (sred[2] + sred[3]);
+    for (int j = t64; j < d.classes; j += 64) x[j] = __expf(__ldcg(x + j) - m) * inv;
+    named_bar(3, 64);  // sred reused by the next request
+  }
+  // the probabilities are read by nothing in this grid (mk_done / Output copies follow it)
+  if (t64 == 0) red_after_bulk_add(counters + nl - 1, (uint32_t)done);
 }
 
 // Split-K reduction of one task: rows [part*red_rows, +red_rows) of one tile.
@@ -1289,8 +1328,11 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         }
       }
     }
-  } else if ((warp == 2 || warp == 3) && args.pre_bn) {
-    bn_prologue(sl, nl, cta, G, hdr, smem, bar_fpre, bar_xf, threadIdx.x - 64);
+  } else if ((warp == 2 || warp == 3) && (args.pre_bn || args.softmax)) {
+    if (args.pre_bn) bn_prologue(sl, nl, cta, G, hdr, smem, bar_fpre, bar_xf, threadIdx.x - 64);
+    if (args.softmax)
+      softmax_tail(sl, nl, cta, G, ab, counters, gen1,
+                   reinterpret_cast<float*>(bar_area + kMkBarBytes - 64), threadIdx.x - 64);
 
   } else if (warp == 1) {
     {
@@ -1704,6 +1746,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
       } else {
         // SIMT layer (every CTA takes part; MK_REDUCE: its own task list)
         const MkLayer& d = sl[L];
+        if (d.kind == MK_SOFTMAX) continue;  // run by warps 2-3 (softmax_tail)
         if (d.kind == MK_REDUCE && first_task(d, cta, G) >= d.tasks) continue;
         if (et == 0) wait_deps(sl, L, counters, gen1, 9);
         named_bar(1, kMkEpiThreads);
@@ -1723,6 +1766,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                     reinterpret_cast<const __nv_bfloat16*>(obufs), obase,
                     reinterpret_cast<float*>(obufs + 3 * kMkOutBufBytes), bar_simt, simt_phase);
             break;
+
           case MK_REDUCE: {
             done = 0;
             for (int t = first_task(d, cta, G); t < d.tasks; t += G, ++done)
@@ -1735,9 +1779,11 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         if (args.trace && et == 0) args.trace[((size_t)L * G + cta) * 4 + 2] = globaltimer();
         named_bar(1, kMkEpiThreads);
         if (et == 0) {
-          // reduce rows left by bulk copies; the FC's logits are read by nothing in this
-          // grid (mk_done and the output copies are ordered after its completion)
-          if (d.kind == MK_REDUCE || d.kind == MK_FC) red_after_bulk_add(counters + L, (uint32_t)done);
+          // reduce rows left by bulk copies; the last layer's outputs (FC logits or the
+          // softmax) are read by nothing in this grid (mk_done and the output copies are
+          // ordered after its completion); an FC followed by a softmax releases its stores
+          if (d.kind == MK_REDUCE || (d.kind == MK_FC && !args.softmax))
+            red_after_bulk_add(counters + L, (uint32_t)done);
           else red_release_add(counters + L, (uint32_t)done);  // generic stores
         }
       }

@@ -419,20 +419,35 @@ static void plan_conv(MkLayer& d, int cout, int G, bool allow_split, bool groupe
 }
 
 namespace {
-// Buffer-level hazard tracking -> per-layer dependency lists (RAW, WAR, WAW),
+// One buffer access of a layer: channels [c0, c1) of workspace buffer `buf` (concats are
+// disjoint channel slices of one buffer: their writers do not order each other).
+struct Access {
+  int buf;
+  int c0 = 0, c1 = 1 << 30;
+};
+
+// Buffer / channel-range hazard tracking -> per-layer dependency lists (RAW, WAR, WAW),
 // transitively reduced.
 struct DepTracker {
-  std::map<int, int> last_writer;
-  std::map<int, std::vector<int>> readers;
+  struct Use {
+    int layer, c0, c1;
+  };
+  std::map<int, std::vector<Use>> writers, readers;
   std::vector<std::vector<char>> reach;  // reach[L][p]: L (transitively) waits for p
 
-  std::string add(MkLayer& d, int L, const std::vector<int>& reads, const std::vector<int>& writes) {
+  static bool overlap(const Use& u, const Access& a) { return u.c0 < a.c1 && a.c0 < u.c1; }
+
+  std::string add(MkLayer& d, int L, const std::vector<Access>& reads,
+                  const std::vector<Access>& writes) {
     std::vector<int> deps;
-    for (int b : reads)
-      if (last_writer.count(b)) deps.push_back(last_writer[b]);
-    for (int b : writes) {
-      if (last_writer.count(b)) deps.push_back(last_writer[b]);
-      for (int r : readers[b]) deps.push_back(r);
+    for (const Access& a : reads)
+      for (const Use& w : writers[a.buf])
+        if (overlap(w, a)) deps.push_back(w.layer);
+    for (const Access& a : writes) {
+      for (const Use& w : writers[a.buf])
+        if (overlap(w, a)) deps.push_back(w.layer);
+      for (const Use& r : readers[a.buf])
+        if (overlap(r, a)) deps.push_back(r.layer);
     }
     std::sort(deps.begin(), deps.end());
     deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
@@ -453,15 +468,22 @@ struct DepTracker {
     if ((int)kept.size() > kMkMaxDeps) return "too many layer dependencies";
     d.ndeps = (int)kept.size();
     for (size_t i = 0; i < kept.size(); ++i) d.deps[i] = kept[i];
-    for (int b : reads) readers[b].push_back(L);
-    for (int b : writes) {
-      last_writer[b] = L;
-      readers[b].clear();
+    for (const Access& a : reads) readers[a.buf].push_back({L, a.c0, a.c1});
+    for (const Access& a : writes) {
+      // uses inside the new write's range are ordered before it: later accesses that
+      // overlap them overlap it too, and wait for it (transitively for them)
+      auto covered = [&](const Use& u) { return u.c0 >= a.c0 && u.c1 <= a.c1; };
+      auto& ws = writers[a.buf];
+      ws.erase(std::remove_if(ws.begin(), ws.end(), covered), ws.end());
+      auto& rs = readers[a.buf];
+      rs.erase(std::remove_if(rs.begin(), rs.end(), covered), rs.end());
+      ws.push_back({L, a.c0, a.c1});
     }
     return "";
   }
 };
 constexpr int kBufPartial = 1000;  // pseudo-buffer: the split-K partial workspace
+constexpr int kBufLogits = 1001;   // pseudo-buffer: the request output slots (FC -> softmax)
 }  // namespace
 
 std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
@@ -476,8 +498,8 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
   int rot = 0;
   std::map<int, int> producer_kind;  // buffer -> op kind that last wrote it
   bool fc_seen = false;
-  auto push = [&](MkLayer& d, int oi, const std::vector<int>& rd,
-                  const std::vector<int>& wr) -> std::string {
+  auto push = [&](MkLayer& d, int oi, const std::vector<Access>& rd,
+                  const std::vector<Access>& wr) -> std::string {
     const int L = (int)p.layers.size();
     if (L >= kMkMaxPlanLayers) return "plan has too many layers";
     std::string err = deps.add(d, L, rd, wr);
@@ -490,7 +512,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
   };
   for (size_t oi = 0; oi < a.ops.size(); ++oi) {
     const CwOp& op = a.ops[oi];
-    if (fc_seen) return "the FC op must be the last op of an arch";
+    if (fc_seen && op.kind != OP_SOFTMAX) return "the FC op must be the last op (or a softmax)";
     MkLayer d;
     memset(&d, 0, sizeof(d));
     d.pre_layer = -1;
@@ -506,7 +528,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
         d.W = op.in_w;
         d.out = out;
         if (op.in_w % 4) return "input width must be a multiple of 4";
-        err = push(d, (int)oi, {}, {op.out_buf});
+        err = push(d, (int)oi, {}, {Access{op.out_buf}});
         break;
       }
       case OP_CONV: {
@@ -655,21 +677,22 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
             p.tmaps.push_back(mr);
           }
         }
-        std::vector<int> rd = {op.in_buf}, wr;
+        const Access out_acc{op.out_buf, op.out_coff, op.out_coff + op.cout};
+        std::vector<Access> rd = {Access{op.in_buf, 0, op.cin}}, wr;
         if (d.pool_pw) {
-          wr.push_back(nxt->out_buf);
+          wr.push_back(Access{nxt->out_buf, nxt->out_coff, nxt->out_coff + nxt->cout});
           ++oi;  // the max pool op is done in this layer's epilogue
         } else if (fuse_pool) {
           d.pool_out = reinterpret_cast<float*>(a.bufs[nxt->out_buf]);
           d.pool_scale = 1.0f / (float)(op.out_h * op.out_w);
           d.out = nullptr;
-          wr.push_back(nxt->out_buf);
+          wr.push_back(Access{nxt->out_buf});
           ++oi;  // the avgpool op is done in this layer's epilogue
         } else if (d.splits == 1) {
-          wr.push_back(op.out_buf);
+          wr.push_back(out_acc);
         }
         if (d.splits > 1) {
-          wr.push_back(kBufPartial);
+          wr.push_back(Access{kBufPartial});
           const size_t tiles = (size_t)d.m_tiles * d.n_tiles;
           partial_need = std::max(partial_need, tiles * d.splits * 128 * d.bn * 4);
           MkLayer r = d;
@@ -697,11 +720,11 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
           r.red_rows = (rows + parts - 1) / parts;
           r.red_parts = (rows + r.red_rows - 1) / r.red_rows;
           r.tasks = (int)tiles * r.red_parts;
-          std::vector<int> rrd = {kBufPartial};
-          if (op.res_buf >= 0) rrd.push_back(op.res_buf);
-          err = push(r, (int)oi, rrd, {op.out_buf});
+          std::vector<Access> rrd = {Access{kBufPartial}};
+          if (op.res_buf >= 0) rrd.push_back(Access{op.res_buf});
+          err = push(r, (int)oi, rrd, {out_acc});
         } else {
-          if (op.res_buf >= 0) rd.push_back(op.res_buf);
+          if (op.res_buf >= 0) rd.push_back(Access{op.res_buf});
           err = push(d, (int)oi, rd, wr);
         }
         break;
@@ -723,7 +746,8 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
         d.out_ctot = op.out_ctot;
         if (op.cin % 8) return "maxpool C must be a multiple of 8";
         if (op.kh != 3 || op.kw != 3) return "max pool window must be 3x3";
-        err = push(d, (int)oi, {op.in_buf}, {op.out_buf});
+        err = push(d, (int)oi, {Access{op.in_buf, 0, op.cin}},
+                   {Access{op.out_buf, op.out_coff, op.out_coff + op.cin}});
         break;
       }
       case OP_AVGPOOL: {
@@ -737,7 +761,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
         d.in_ctot = op.in_ctot;
         d.pre_layer = (op.flags & OPF_PRE_BN) ? op.pre_layer : -1;
         if (op.cin % 8 || op.in_ctot % 8) return "avgpool C must be a multiple of 8";
-        err = push(d, (int)oi, {op.in_buf}, {op.out_buf});
+        err = push(d, (int)oi, {Access{op.in_buf, 0, op.cin}}, {Access{op.out_buf}});
         break;
       }
       case OP_BNPOOL: {
@@ -754,7 +778,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
         d.out_ctot = op.out_ctot;
         d.pre_layer = op.pre_layer;
         if (op.cin % 8 || op.pre_layer < 0) return "BN pool: C % 8 and an input BatchNorm";
-        err = push(d, (int)oi, {op.in_buf}, {op.out_buf});
+        err = push(d, (int)oi, {Access{op.in_buf, 0, op.cin}}, {Access{op.out_buf}});
         break;
       }
       case OP_IM2COL: {
@@ -770,7 +794,16 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
         d.stride = op.stride;
         d.pad = op.pad;
         if (op.kh != op.kw || op.kh * op.kw * op.cin > 64) return "im2col patch > 64 values";
-        err = push(d, (int)oi, {}, {op.out_buf});
+        err = push(d, (int)oi, {}, {Access{op.out_buf}});
+        break;
+      }
+      case OP_SOFTMAX: {
+        if (!fc_seen) return "softmax must follow the FC op";
+        d.kind = MK_SOFTMAX;
+        d.tasks = batch;  // one CTA per request
+        d.classes = op.cout;
+        if (op.cout % 4) return "softmax classes must be a multiple of 4";
+        err = push(d, (int)oi, {Access{kBufLogits}}, {Access{kBufLogits}});
         break;
       }
       case OP_FC: {
@@ -783,7 +816,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
         if (op.cin % 64) return "fc input features must be a multiple of 64";
         if (batch > 16) return "fc batch must be <= 16";
         fc_seen = true;
-        err = push(d, (int)oi, {op.in_buf}, {});
+        err = push(d, (int)oi, {Access{op.in_buf}}, {Access{kBufLogits}});
         break;
       }
       default:
@@ -843,7 +876,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
     if (d.slots < 2) return "ring too small for a conv tile";
   }
   if (fc_seen) {
-    const MkLayer& f = p.layers.back();
+    const MkLayer& f = p.layers.back().kind == MK_FC ? p.layers.back() : p.layers[p.layers.size() - 2];
     if ((size_t)batch * f.C * 4 > p.ring_bytes) return "fc: pooled features exceed the ring";
     if ((size_t)8 * f.C * 2 > (size_t)kMkOutBufs * kMkOutBufBytes) return "fc: weight block exceeds staging";
   }
@@ -902,6 +935,7 @@ std::string Runtime::capture(Arch& a, Plan& p) {
   args.pre_bn = 0;
   for (const auto& d : p.layers)
     if (d.kind == MK_CONV && d.pre_layer >= 0) args.pre_bn = 1;
+  args.softmax = p.layers.back().kind == MK_SOFTMAX;
   CW_TRY(cudaStreamBeginCapture(s_cap_, cudaStreamCaptureModeThreadLocal));
   cudaError_t ce = copy_plan(p.d_layers, (int)p.layers.size(), s_cap_);
   launch_gate(ab_, ring_, kRing - 1, ctr_, exec_recs_, s_cap_);

@@ -35,7 +35,7 @@ struct CwOp {
   int32_t pad_w, in_ctot, out_ctot, out_coff, cout_pad, flags, pre_layer;
 };
 enum OpKind { OP_STEM = 0, OP_CONV = 1, OP_MAXPOOL = 2, OP_AVGPOOL = 3, OP_FC = 4,
-              OP_IM2COL = 5, OP_BNPOOL = 6 };
+              OP_IM2COL = 5, OP_BNPOOL = 6, OP_SOFTMAX = 7 };
 enum OpFlags { OPF_GROUPED64 = 1, OPF_PRE_BN = 2 };
 
 // Mirrors struct cw_tensor_loc: where one layer's tensors sit in a blob (-1 = absent).

@@ -293,7 +293,7 @@ class B200Worker:
                  keep_records: bool = True, *, mode: str = "cuda", devices=None,
                  weights_seed: int = 0, input_pool: int = 64, epoch_ns: int | None = None,
                  keep_outputs: bool = False, poll_results: bool = True,
-                 weights_dir: str | None = None):
+                 weights_dir: str | None = None, softmax: bool = False):
         if mode not in ("cuda", "sim"):
             raise ValueError(f"mode must be 'cuda' or 'sim', not {mode!r}")
         if jitter is not None and getattr(jitter, "kind", "none") != "none" and \
@@ -320,7 +320,8 @@ class B200Worker:
         specs = {}
         if mode == "cuda":
             for base in cat.bases():
-                specs[base] = arch_mod.build_arch(base)    # raises for unsupported nets
+                # (raises for unsupported nets); softmax: outputs are class probabilities
+                specs[base] = arch_mod.build_arch(base, softmax=softmax)
             in_max = max(s.in_c * s.in_h * s.in_w * 4 for s in specs.values())
             out_max = max(s.classes * 4 for s in specs.values())
             per_req = min([p.input_bytes + p.output_bytes for p in cat.models

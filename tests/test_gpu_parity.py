@@ -263,3 +263,33 @@ def test_every_batch_size_matches_frozen_golden_logits(gpu):
             assert c["ok"], (b, c)
     finally:
         w.close()
+
+
+def test_softmax_tail_probabilities(gpu):
+    """The optional FC/softmax tail (B200Worker(softmax=True), `worker --softmax`): the
+    outputs are the softmax of the golden logits (max-abs probability error <= 2% of the
+    largest probability, top-1 identical) and every row sums to 1."""
+    import torch
+    golden = np.load(os.path.join(GOLDEN, "logits_resnet50.npz"))["logits"]
+    probs = torch.softmax(torch.from_numpy(golden), dim=1).numpy()
+    col = Collector()
+    w = B200Worker(0, catalog.parse(CAT_ALL_B), None, col, pages_per_gpu=8, mode="cuda",
+                   devices=[gpu], epoch_ns=time.time_ns(), keep_outputs=True, input_pool=16,
+                   softmax=True)
+    try:
+        t = time.time_ns() - w.epoch_ns
+        w.on_action(Action(1, ActionKind.LOAD, 0, t, t + WIDE))
+        assert int(col.wait(1).status) == 1
+        for k, b in enumerate((1, 16)):
+            t = time.time_ns() - w.epoch_ns
+            w.on_action(Action(10 + k, ActionKind.INFER, 0, t, t + WIDE, tuple(range(b))))
+            assert int(col.wait(10 + k).status) == 1
+            deadline = time.time() + 5
+            while 10 + k not in w.outputs and time.time() < deadline:
+                time.sleep(0.005)
+            got = w.outputs[10 + k]
+            np.testing.assert_allclose(got.sum(1), 1.0, atol=1e-4)
+            c = resnet_oracle.compare(got, probs[:b])
+            assert c["ok"], (b, c)
+    finally:
+        w.close()

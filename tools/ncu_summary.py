@@ -22,14 +22,19 @@ WANT = [
 ]
 summary = {"how": "ncu --set full --clock-control none -k regex:mk_infer -s 6 -c 1 "
                   "python tools/ncu_target.py resnet50 <b> 8 4 (weights rotate over 4 copies)"}
-for b in (16, 1):
-    path = os.path.join(OUT, f"ncu_mk_b{b}.raw.csv")
-    if not os.path.exists(path):
-        continue
+def one(path):
     rows = list(csv.reader(open(path)))
     head, units, vals = rows[0], rows[1], rows[2]
-    summary[f"b{b}"] = {n: f"{vals[head.index(n)]} {units[head.index(n)]}".strip()
-                        for n in WANT if n in head}
+    return {n: f"{vals[head.index(n)]} {units[head.index(n)]}".strip() for n in WANT if n in head}
+
+
+for b in (16, 1):
+    path = os.path.join(OUT, f"ncu_mk_b{b}.raw.csv")
+    if os.path.exists(path):
+        summary[f"b{b}"] = one(path)
+for f in sorted(os.listdir(OUT)):
+    if f.startswith("ncu_mk_") and f.endswith("_b16.raw.csv") and f != "ncu_mk_b16.raw.csv":
+        summary[f[len("ncu_mk_"):-len(".raw.csv")]] = one(os.path.join(OUT, f))
 os.makedirs(os.path.join(HERE, "profiles"), exist_ok=True)
 with open(os.path.join(HERE, "profiles", f"{ROUND}_ncu_full_mk_infer_summary.json"), "w") as f:
     json.dump(summary, f, indent=1)

@@ -13,7 +13,8 @@ reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 copies = int(sys.argv[4]) if len(sys.argv) > 4 else 1  # > 2: weights rotate through HBM
 spec = arch.build_arch(name)
 blob = arch.pack_blob(spec, arch.fold(spec, arch.make_params(spec, 0)))
-with DeviceRuntime(pages_total=copies * blob.pages, io_slots=16) as rt:
+with DeviceRuntime(pages_total=copies * blob.pages, io_slots=16,
+                   in_bytes_max=spec.in_c * spec.in_h * spec.in_w * 4) as rt:
     rt.register_arch(0, spec, batches=(b,))
     rt.register_blob(0, 0, blob)
     rt.build()
