@@ -382,6 +382,73 @@ def e2e_line(r: dict, args, n_gpus: int) -> dict:
     }
 
 
+def h2d_link_peak(dev: int) -> float:
+    """Pinned host -> device copy bandwidth of this box (GB/s): LOAD's roofline."""
+    import torch
+    n = 256 << 20
+    src = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    dst = torch.empty(n, dtype=torch.uint8, device=f"cuda:{dev}")
+    dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 0.0
+    for _ in range(5):
+        e0.record()
+        dst.copy_(src, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, n / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    return best
+
+
+def reference_worker_closed_loop(n_per_batch: int = 200) -> dict:
+    """SURVEY §8(d) CPU-baseline leg (i): the reference's own worker path on this host --
+    EmulatedWorker on its WallLoop (baseline/_ref), closed-loop INFERs of the reference
+    catalog's resnet50 at b = 1 and 16 -- and the realized spread of its emulated spans
+    (Exec + Output, result.end - result.start) next to the profiled duration."""
+    bench_e2e.sloserve()
+    from sloserve import profiles
+    from sloserve.protocol import Action, ActionKind
+    from sloserve.timebase import WallClock, WallLoop
+    from sloserve.worker import EmulatedWorker
+
+    cat = profiles.reference_catalog()
+    mid = next(e.model_id for e in cat.entries if e.replica_of == "resnet50")
+    loop = WallLoop(WallClock(), name="ref-worker").start()
+    done = threading.Event()
+    box = {}
+
+    def send(r):
+        box["r"] = r
+        done.set()
+
+    w = EmulatedWorker(0, cat, loop, send, pages_per_gpu=500)
+    aid = [0]
+
+    def call(kind, b=0):
+        aid[0] += 1
+        done.clear()
+        t = loop.now()
+        loop.call_soon(w.on_action, Action(aid[0], kind, mid, t, t + 10**9, tuple(range(b))))
+        done.wait(10)
+        return box["r"]
+
+    call(ActionKind.LOAD)
+    out = {}
+    for b in (1, 16):
+        spans = []
+        for _ in range(n_per_batch):
+            r = call(ActionKind.INFER, b)
+            spans.append(r.end - r.start)
+        p50 = pct(spans, 50)
+        out[str(b)] = {"n": n_per_batch, "span_p50_ms": p50 / 1e6,
+                       "span_p9999_ms": pct(spans, 99.99) / 1e6,
+                       "p9999_over_p50": pct(spans, 99.99) / p50,
+                       "profiled_exec_ms": cat.profile(mid).exec_duration[b] / 1e6}
+    loop.stop()
+    return out
+
+
 def cpu_baseline(spec, params, budget_s: float) -> dict:
     import torch
 
@@ -493,8 +560,20 @@ def main():
                 "satisfaction": c["satisfaction"], "cold_starts": c["cold_starts"],
                 "loads": c["loads"], "actions": c["actions"], "mean_batch": c["mean_batch"],
                 "latency_p99_ms": c["latency_p99_ms"], "horizon_s": c["horizon_s"]}
+        try:
+            link = h2d_link_peak(d.local)
+            line["load"].update({"link_gbs": link, "frac": res["load_gbs"] / link,
+                                 "roofline": "pinned H2D link bandwidth of this box (256 MiB "
+                                             "copy, best of 5)"})
+        except Exception as exc:  # noqa: BLE001 (diagnostic leg)
+            line["load"]["link_error"] = str(exc)
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(res["spec"], res["params"], budget_s=15.0)
+            try:
+                line["cpu_baseline"]["reference_worker_closed_loop"] = \
+                    reference_worker_closed_loop()
+            except Exception as exc:  # noqa: BLE001
+                line["cpu_baseline"]["reference_worker_closed_loop"] = {"error": str(exc)}
         print(json.dumps(line), flush=True)
     d.close()
 

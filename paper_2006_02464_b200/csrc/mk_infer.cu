@@ -63,6 +63,17 @@ constexpr int kResDist = CW_RES_DIST;
 #endif
 constexpr uint64_t kMkTimeoutNs = CW_TIMEOUT_NS;
 
+// L2 residency policies: the weights stream (every INFER may run another model copy: evict
+// first), a layer's outputs are the next layer's inputs (evict last: keep the activation
+// working set in the 126 MB L2 instead of writing it back), a residual is read for the
+// last time (evict first). CW_NO_L2_HINTS: every access at normal priority.
+#ifdef CW_NO_L2_HINTS
+constexpr uint64_t kHintW = 0x1000000000000000ull, kHintOut = 0x1000000000000000ull,
+                   kHintRes = 0x1000000000000000ull;
+#else
+constexpr uint64_t kHintW = kL2EvictFirst, kHintOut = kL2EvictLast, kHintRes = kL2EvictFirst;
+#endif
+
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1139,8 +1150,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
               if (elect_one())
                 for (int q = 0; q < 3; ++q)
                   for (int j = 0; j < nbox; ++j)
-                    tma_load_2d(sbase + s * sb + b_off + q * b3 + j * b_box, tb, bar_full + 8 * s,
-                                ((r * 3 + q) * d.cin_kb + cb) * 64, o.n0 + 64 * j);
+                    tma_load_2d_hint(sbase + s * sb + b_off + q * b3 + j * b_box, tb,
+                                     bar_full + 8 * s, ((r * 3 + q) * d.cin_kb + cb) * 64,
+                                     o.n0 + 64 * j, kHintW);
               __syncwarp();
             };
             const int chan0 = d.grouped ? o.n0 : 0;  // grouped: the tile's own channel block
@@ -1237,7 +1249,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     const int kx_ = (kb_) * kblk;                                                   \
     if (elect_one())                                                                \
       for (int j = 0; j < (no_b ? 0 : nbox); ++j)                                   \
-        tma_load_2d(dst_ + j * b_box, tb, fullb + 8 * (s_), kx_, o.n0 + 64 * j);      \
+        tma_load_2d_hint(dst_ + j * b_box, tb, fullb + 8 * (s_), kx_, o.n0 + 64 * j,    \
+                         kHintW);                                                       \
     __syncwarp();                                                                   \
   } while (0)
 #define CW_ADV_A()                                                                      \
@@ -1629,8 +1642,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
               auto issue_res = [&](uint32_t b, int c) {
                 const uint32_t dst = obase + b * kMkOutBufBytes, bar = bar_res + 8 * b;
                 mbar_arrive_expect_tx(bar, a_rows(d) * 128u);  // the box: tile rows x 64 cols
-                if (m2d) tma_load_2d(dst, tmr, bar, o.n0 + 64 * c, o.m0);
-                else tma_load_4d(dst, tmr, bar, o.n0 + 64 * c, o.ow0, o.oh0, o.img0);
+                if (m2d) tma_load_2d_hint(dst, tmr, bar, o.n0 + 64 * c, o.m0, kHintRes);
+                else tma_load_4d_hint(dst, tmr, bar, o.n0 + 64 * c, o.ow0, o.oh0, o.img0, kHintRes);
               };
               if (tmr && et == 0) {
                 for (int j = 0; j < nch && j < kResDist; ++j) {
@@ -1711,8 +1724,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                 CW_KET(30 + c);
                 if (et == 0) {
                   const uint32_t src = obase + b * kMkOutBufBytes;
-                  if (m2d) tma_store_2d(tmo, src, o.n0 + 64 * c, o.m0);
-                  else tma_store_4d(tmo, src, o.n0 + 64 * c, o.ow0, o.oh0, o.img0);
+                  if (m2d) tma_store_2d_hint(tmo, src, o.n0 + 64 * c, o.m0, kHintOut);
+                  else tma_store_4d_hint(tmo, src, o.n0 + 64 * c, o.ow0, o.oh0, o.img0, kHintOut);
                   bulk_commit();
                   if (tmr && c + kResDist < nch) {
                     // buffer of chunk c + kResDist - kMkOutBufs is free
