@@ -122,8 +122,12 @@ int cw_rt_profile_layers(cw_runtime* rt, int arch_id, int batch, int32_t hdr_pag
  * Returns the word count. */
 int64_t cw_rt_last_trace(cw_runtime* rt, uint64_t* out, int64_t max_words);
 /* Megakernel plan: 8 ints per layer (kind, conv mode, N tile, tasks, split-K,
- * k-blocks, arch op index, fused avgpool); returns the layer count. */
+ * k-blocks, arch op index, flags: 1 fused avgpool, 2 cluster split-K); returns the
+ * layer count. */
 int cw_rt_plan_layers(cw_runtime* rt, int arch_id, int batch, int32_t* out8, int max_layers);
+/* Megakernel launch shape of a plan: persistent grid (CTAs) and thread-block cluster size
+ * (1: no clusters; > 1: split-K layers reduce through distributed shared memory). */
+int cw_rt_plan_launch(cw_runtime* rt, int arch_id, int batch, int32_t* grid, int32_t* csize);
 /* Copy to/from a workspace activation buffer (parity tests of single layers). */
 int cw_rt_buffer_io(cw_runtime* rt, int arch_id, int buf, void* host, int64_t bytes,
                     int to_device);

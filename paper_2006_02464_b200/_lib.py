@@ -100,6 +100,7 @@ SIGNATURES = [
     ("cw_rt_profile_layers", C.c_int, [_P, C.c_int, C.c_int, C.c_int32, _P, _I32P, C.c_int]),
     ("cw_rt_last_trace", C.c_int64, [_P, _P, C.c_int64]),
     ("cw_rt_plan_layers", C.c_int, [_P, C.c_int, C.c_int, _I32P, C.c_int]),
+    ("cw_rt_plan_launch", C.c_int, [_P, C.c_int, C.c_int, _I32P, _I32P]),
     ("cw_rt_buffer_io", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_int64, C.c_int]),
     ("cw_rt_exec_window", C.c_int, [_P, C.c_int, C.c_int, C.c_int32, C.c_int64, C.c_int64,
                                     _I32P, _I64P, _I64P]),

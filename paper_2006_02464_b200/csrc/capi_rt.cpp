@@ -258,9 +258,17 @@ int cw_rt_plan_layers(cw_runtime* rt, int arch_id, int batch, int32_t* out8, int
     o[4] = d.splits;
     o[5] = d.num_kb;
     o[6] = p->layer_op[i];
-    o[7] = d.pool_out != nullptr;
+    o[7] = (d.pool_out != nullptr ? 1 : 0) | (d.csplit ? 2 : 0);
   }
   return n;
+}
+
+int cw_rt_plan_launch(cw_runtime* rt, int arch_id, int batch, int32_t* grid, int32_t* csize) {
+  const cw::Plan* p = rt->rt.plan(arch_id, batch);
+  if (!p) return cw::fail("no plan for batch");
+  *grid = p->grid;
+  *csize = p->csize;
+  return 0;
 }
 
 }  // extern "C"

@@ -11,6 +11,7 @@ namespace cw {
 cudaError_t configure_mk();
 uint32_t mk_smem_bytes(uint32_t ring_bytes, int n_layers);
 int mk_blocks_per_sm(uint32_t smem);
+int mk_cluster_ctas(int csize, uint32_t smem);
 cudaError_t copy_plan(const MkLayer* d_layers, int n, cudaStream_t st);  // -> constant bank
 cudaError_t launch_mk(const MkArgs& a, int grid, uint32_t smem, cudaStream_t st);
 void launch_mk_done(const ActionBlock* ab, uint32_t mask, ExecRecord* recs, uint32_t* gen,

@@ -106,7 +106,10 @@ struct MkLayer {
   int32_t n_valid;    // channels actually stored (cout; n_out is cout padded to the N tile)
   int32_t grouped;    // conv: K walks the tile's own 64-channel block only (ResNeXt groups)
   int32_t pre_layer;  // BatchNorm + ReLU of the input (conv A tile / pool), header entry; -1
-  int32_t pad2_;
+  // conv: split-K across the CTAs of one thread-block cluster (splits == cluster size, split z
+  // on cluster rank z): the partial tiles are reduced through distributed shared memory in the
+  // epilogue (no fp32 partials in global memory, no reduce layer)
+  int32_t csplit;
   void* out;              // bf16 NHWC output (conv / reduce / pools), NHWC4 (input)
   const void* res;        // bf16 residual, same shape as out, or null
   float* partial;         // split-K fp32 partials [tile][split][128][bn]
@@ -136,6 +139,7 @@ struct MkArgs {
   int32_t pf_depth;          // weight layers L2-prefetched ahead of the running conv
   int32_t pre_bn;            // 1: some conv applies a BN+ReLU prologue (warps 2-3 run it)
   int32_t softmax;           // 1: the last layer is a softmax tail (warps 2-3 run it)
+  int32_t csize;             // thread-block cluster size of the launch (1: no clusters)
 };
 
 }  // namespace cw

@@ -232,6 +232,15 @@ __device__ __forceinline__ int first_task(const MkLayer& d, int cta, int G) {
   return t < 0 ? t + G : t;
 }
 
+// K range of split z: [kb0, kb1), balanced over units of one k-block (mode 3: one kernel row
+// of one channel block = 3 k-blocks); the planner keeps every split non-empty.
+__device__ __forceinline__ void split_range(const MkLayer& d, int z, int& kb0, int& kb1) {
+  const int u = d.mode == 3 ? 3 : 1;
+  const int units = d.num_kb / u;
+  kb0 = units * z / d.splits * u;
+  kb1 = units * (z + 1) / d.splits * u;
+}
+
 // Rows of the A tile (output pixels) for one task.
 __device__ __forceinline__ uint32_t a_rows(const MkLayer& d) {
   return d.mode == 0 ? 128u : (uint32_t)(d.box_w * d.box_h * d.box_n);
@@ -782,6 +791,159 @@ __device__ __forceinline__ void simt_reduce(const MkLayer& d, const uint8_t* hdr
   named_bar(1, kMkEpiThreads);  // the stages are read before the next task's copies
 }
 
+__device__ __forceinline__ void mbar_wait_cluster_to(uint32_t bar, uint32_t parity, int site) {
+  if (mbar_try_wait_cluster(bar, parity)) return;
+  const uint64_t t0 = globaltimer();
+  while (!mbar_try_wait_cluster(bar, parity))
+    if (globaltimer() - t0 > kMkTimeoutNs) mk_timeout(site);
+}
+
+// Cluster split-K epilogue (d.csplit): split z of a tile runs on cluster rank z (planner:
+// tasks = tiles x C, rotation a multiple of C, bn = 64). Rank z stages its fp32 partial tile
+// [128][64] in the upper half of its staging buffers (16-byte chunks XOR-swizzled by row),
+// then ONE bulk DSMEM copy per rank j moves row block j (rows [j*rpc, (j+1)*rpc), rpc = 128/C)
+// into slot z of rank j's receive buffer (the lower half); each rank then sums the C partial
+// blocks of its own rows + bias (+ residual) (+ ReLU) -> bf16 rows -> bulk stores. Per task
+// (the ranks of a cluster run the same task sequence): bar_crdy completes once all C ranks'
+// buffers are free (each rank arrives on every rank's), bar_crx once this rank's C blocks
+// have landed (transaction bytes of the copies). A rank's staging half is rewritten only
+// after the next bar_crdy (every receiver has consumed the previous copies); after the
+// layer's last task, bar_cdone (csplit_drain) covers the copies still in flight.
+template <int C>
+__device__ __noinline__ void epi_csplit(const MkLayer& d, const TileOrigin& o, int z,
+                                        uint32_t taddr, int row, int grp, int et, uint32_t obase,
+                                        uint8_t* obufs, uint32_t bar_acc, uint32_t acc_par,
+                                        uint32_t bar_crdy, uint32_t bar_crx, uint32_t cpar,
+                                        const float* bias) {
+  constexpr int bn = 64, c4n = bn / 4;
+  constexpr uint32_t kTile = 128u * bn * 4u;  // one fp32 partial tile
+  constexpr int rpc = 128 / C;
+  constexpr uint32_t blk = (uint32_t)rpc * bn * 4u;
+#ifdef CW_CSPLIT_TRACE
+  long long ts[9];
+  ts[0] = clock64();
+#define CW_CST(i_) ts[i_] = clock64()
+#else
+#define CW_CST(i_) do {} while (0)
+#endif
+  // this rank's staging buffers are free: its earlier TMA stores have read them
+  if (et == 0) bulk_wait_read<0>();
+  named_bar(1, kMkEpiThreads);
+  // (relaxed signals: this rank's reads of its receive buffer are complete, their values were
+  // consumed before the barrier; the copies into it are ordered by the transaction count)
+  if (et == 0) mbar_arrive_expect_tx(bar_crx, kTile);
+  if ((et & 31) == 0)
+    for (int j = et >> 5; j < C; j += kMkEpiThreads / 32)
+      mbar_arrive_remote(mapa_shared(bar_crdy, (uint32_t)j));
+  CW_CST(1);
+  // this thread's output element groups of the reduction (rpc x 16 float4: 8 / C per
+  // thread, C in {2, 4, 8}), their bias and residual loaded while the partials are in flight
+  const int r0 = z * rpc;
+  constexpr int ni = 8 / C;
+  int li[ni], c4[ni];
+  long long m[ni];
+  bool mine[ni];
+  float4 acc[ni];
+  uint2 rres[ni];
+#pragma unroll
+  for (int k = 0; k < ni; ++k) {
+    const int idx = et + k * kMkEpiThreads;
+    li[k] = idx / c4n;
+    c4[k] = idx - li[k] * c4n;
+    m[k] = 0;
+    mine[k] = li[k] < rpc && row_pixel(d, o, r0 + li[k], &m[k]) &&
+              o.n0 + c4[k] * 4 < d.n_valid;
+    acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    rres[k] = make_uint2(0u, 0u);
+    if (mine[k]) {
+      acc[k] = __ldg(reinterpret_cast<const float4*>(bias) + c4[k]);
+      if (d.res)
+        rres[k] = __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(d.res) +
+                                                        (size_t)m[k] * d.n_out + o.n0 + c4[k] * 4));
+    }
+  }
+  mbar_wait_to<kEpiWaitNs>(bar_acc, acc_par, 8);
+  tc_fence_after();
+  CW_CST(2);
+  mbar_wait_cluster_to(bar_crdy, cpar, 16);
+  CW_CST(3);
+  {
+    uint32_t v[32];
+    tmem_ld16(taddr + 32 * grp, *reinterpret_cast<uint32_t(*)[16]>(v));
+    tmem_ld16(taddr + 32 * grp + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+    tmem_ld_wait();
+    uint8_t* stage = obufs + kTile + (uint32_t)row * (bn * 4);
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int ch = 8 * grp + kk;  // logical 16-byte chunk of the row
+      *reinterpret_cast<uint4*>(stage + ((ch ^ (row & 7)) << 4)) =
+          make_uint4(v[4 * kk], v[4 * kk + 1], v[4 * kk + 2], v[4 * kk + 3]);
+    }
+  }
+  fence_proxy_async_smem();  // generic stores -> the bulk copies' async-proxy reads
+  named_bar(1, kMkEpiThreads);
+  if ((et & 31) == 0)  // (one issuing lane per warp: the copies leave in parallel)
+    for (uint32_t j = (uint32_t)(et >> 5); j < (uint32_t)C; j += kMkEpiThreads / 32)
+      bulk_s2cluster(mapa_shared(obase + (uint32_t)z * blk, j), obase + kTile + j * blk, blk,
+                     mapa_shared(bar_crx, j));
+  CW_CST(4);
+  mbar_wait_cluster_to(bar_crx, cpar, 17);
+  CW_CST(5);
+  const float4* src = reinterpret_cast<const float4*>(obufs);
+#pragma unroll
+  for (int k = 0; k < ni; ++k) {
+    if (!mine[k]) continue;
+    float4 a4 = acc[k];
+    const int pc = c4[k] ^ (li[k] & 7);  // (row & 7 == li & 7: rpc is a multiple of 8)
+    for (int s = 0; s < C; ++s) {
+      const float4 p = src[(s * rpc + li[k]) * c4n + pc];
+      a4.x += p.x;
+      a4.y += p.y;
+      a4.z += p.z;
+      a4.w += p.w;
+    }
+    if (d.res) {
+      const float2 ra = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rres[k].x));
+      const float2 rb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rres[k].y));
+      a4.x += ra.x;
+      a4.y += ra.y;
+      a4.z += rb.x;
+      a4.w += rb.y;
+    }
+    uint2 ov;
+    if (d.relu) {
+      ov.x = pack_bf16x2_relu(a4.x, a4.y);
+      ov.y = pack_bf16x2_relu(a4.z, a4.w);
+    } else {
+      ov.x = pack_bf16x2(a4.x, a4.y);
+      ov.y = pack_bf16x2(a4.z, a4.w);
+    }
+    // generic stores (16 threads cover a row's 128 bytes): a per-row bulk copy costs ~500
+    // issue cycles; the layer publishes with red.release instead (epi_csplit's caller)
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(d.out) + (size_t)m[k] * d.out_ctot +
+                              o.n0 + c4[k] * 4) = ov;
+  }
+  CW_CST(6);
+  CW_CST(7);
+#ifdef CW_CSPLIT_TRACE
+  if (et == 0 && blockIdx.x < 8)
+    printf("csplit cta %d z %d n0 %d: bar %lld acc %lld crdy %lld send %lld crx %lld red %lld "
+           "rbar %lld st %lld\n",
+           blockIdx.x, z, o.n0, ts[1] - ts[0], ts[2] - ts[1], ts[3] - ts[2], ts[4] - ts[3],
+           ts[5] - ts[4], ts[6] - ts[5], ts[7] - ts[6], clock64() - ts[7]);
+#endif
+#undef CW_CST
+}
+
+// After a cluster split-K layer's last task: every rank has received all its partial blocks
+// (so every copy this rank sent has landed) before the staging buffers are reused.
+__device__ __noinline__ void csplit_drain(int C, int et, uint32_t bar_cdone, uint32_t par) {
+  if ((et & 31) == 0)
+    for (int j = et >> 5; j < C; j += kMkEpiThreads / 32)
+      mbar_arrive_remote(mapa_shared(bar_cdone, (uint32_t)j));
+  mbar_wait_cluster_to(bar_cdone, par, 18);
+}
+
 // Stem conv with the 3x3/s2/p1 max pool fused: the tile's conv pixels
 // (3 conv rows x 2*pool_pw+1 columns) -> bias, ReLU, bf16 into the CTA staging
 // buffer, then each pooled pixel = max over its valid 3x3 window (identical to
@@ -913,8 +1075,9 @@ __device__ __noinline__ void bn_prologue(const MkLayer* sl, int nl, int cta, int
     const int cpad = d.num_kb * 64;
     int slot = 0;
     for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
-      const int kb0 = (t % d.splits) * d.kb_per_split;
-      const int n = min(d.num_kb, kb0 + d.kb_per_split) - kb0;  // kpack = 1: a k-block per slot
+      int kb0, kb1;
+      split_range(d, t % d.splits, kb0, kb1);
+      const int n = kb1 - kb0;  // kpack = 1: a k-block per slot
       for (int i = 0; i < n; ++i) {
         const int c0 = (kb0 + i) * 64 + lc * 8;
         const float4 s0 = __ldg(reinterpret_cast<const float4*>(ptab + c0));
@@ -981,6 +1144,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   const uint32_t bar_stemb = bar_res + 8 * kMkOutBufs;    // resident stem weights
   const uint32_t bar_xf = bar_stemb + 8;                  // kMkMaxSlots: A tile BN-transformed
   const uint32_t bar_fpre = bar_xf + 8 * kMkMaxSlots;     // kMkMaxSlots: fills of BN layers
+  const uint32_t bar_crdy = bar_fpre + 8 * kMkMaxSlots;   // cluster split-K: all receivers ready
+  const uint32_t bar_crx = bar_crdy + 8;                  // cluster split-K: partials landed
+  const uint32_t bar_cdone = bar_crx + 8;                 // cluster split-K: layer's copies done
   uint8_t* bar_area = obufs + kMkOutBufs * kMkOutBufBytes;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_area + kMkBarBytes - 32);
   uint32_t* gen_slot = tmem_slot + 1;
@@ -1026,6 +1192,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
       mbar_init(bar_xf + 8 * sl, 64);
       mbar_init(bar_fpre + 8 * sl, 1);
     }
+    mbar_init(bar_crdy, (uint32_t)args.csize);  // one arrival per CTA of the cluster
+    mbar_init(bar_crx, 1);                      // the local expect_tx; the data by bulk copies
+    mbar_init(bar_cdone, (uint32_t)args.csize);
     fence_mbar_init();
     *gen_slot = *reinterpret_cast<const volatile uint32_t*>(args.gen);
   }
@@ -1033,6 +1202,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (args.csize > 1) cluster_sync();  // every CTA's barriers initialised before remote arrivals
   const uint32_t tmem = *tmem_slot;
   const uint32_t gen1 = *gen_slot + 1u;
   const uint8_t* hdr = ab->hdr;
@@ -1142,9 +1312,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
             const int tile = t / d.splits;
             const int z = t - tile * d.splits;
             const TileOrigin o = tile_origin(d, tile);
-            const int g0 = z * d.kb_per_split / 3;
-            const int g1 = min(d.num_kb, (z + 1) * d.kb_per_split) / 3;
-            const int ng = g1 - g0;
+            int kb0, kb1;
+            split_range(d, z, kb0, kb1);
+            const int g0 = kb0 / 3, ng = (kb1 - kb0) / 3;
             auto load_b = [&](int g, int s) {
               const int r = g / d.cin_kb, cb = g - r * d.cin_kb;
               if (elect_one())
@@ -1221,8 +1391,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           const int tile = t / d.splits;
           const int z = t - tile * d.splits;
           const TileOrigin o = tile_origin(d, tile);
-          const int kb0 = z * d.kb_per_split;
-          const int kb1 = min(d.num_kb, kb0 + d.kb_per_split);
+          int kb0, kb1;
+          split_range(d, z, kb0, kb1);
           const int wb = o.ow0 * d.stride - d.pad_w;
           const int hb = o.oh0 * d.stride - d.pad;
           const int chan0 = d.grouped ? o.n0 : 0;  // grouped: the tile's own channel block
@@ -1405,8 +1575,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           // absolute address bits, so an unaligned start needs no base-offset field)
           const uint32_t b3 = (uint32_t)d.bn * 128u;
           for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
-            const int z = t % d.splits;
-            const int ng = min(d.num_kb, (z + 1) * d.kb_per_split) / 3 - z * d.kb_per_split / 3;
+            int kb0, kb1;
+            split_range(d, t % d.splits, kb0, kb1);
+            const int ng = (kb1 - kb0) / 3;
             mbar_wait_to<CW_HINT_TEMPTY>(bar_tempty + 8 * acc, acc_phase ^ 1, 4);
             tc_fence_after();
             const uint32_t dtm = tmem + acc * 256;
@@ -1445,9 +1616,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         const bool pre = d.pre_layer >= 0;
         const uint32_t bar_in = pre ? bar_xf : bar_full;
         for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
-          const int z = t % d.splits;
-          const int kb0 = z * d.kb_per_split;
-          const int n = min(d.num_kb, kb0 + d.kb_per_split) - kb0;
+          int kb0, kb1;
+          split_range(d, t % d.splits, kb0, kb1);
+          const int n = kb1 - kb0;
           mbar_wait_to<CW_HINT_TEMPTY>(bar_tempty + 8 * acc, acc_phase ^ 1, 4);
           tc_fence_after();
           const uint32_t dtm = tmem + acc * 256;
@@ -1513,6 +1684,8 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     uint32_t ocnt = 0;  // TMA-epilogue chunks staged so far (buffer ocnt % kMkOutBufs)
     uint32_t rpar = 0;  // bit b: phase parity of the next residual landing in buffer b
     uint32_t simt_phase = 0;  // completed phases of bar_simt (SIMT-layer bulk copies)
+    uint32_t cpar = 0;        // phase parity of bar_crdy / bar_crx (cluster split-K tasks)
+    uint32_t cdpar = 0;       // phase parity of bar_cdone (cluster split-K layers)
     // per-warp staging: 32 rows x 128 B, 16-byte chunks XOR-swizzled by row
     uint8_t* stg = reinterpret_cast<uint8_t*>(sstage) + (warp - kMkEpiWarp0) * 4096;
     auto stg_chunk = [stg](int r, int c) {
@@ -1542,7 +1715,19 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           long long m;
           const bool valid = row_pixel(d, o, row, &m);
           const uint32_t taddr = tmem + acc * 256 + ((uint32_t)(q * 32) << 16);
-          if (d.splits > 1) {
+          if (d.csplit) {
+            const uint32_t bar_acc = bar_tfull + 8 * acc;
+            if (args.csize == 8)
+              epi_csplit<8>(d, o, z, taddr, row, grp, et, obase, obufs, bar_acc, acc_phase,
+                            bar_crdy, bar_crx, cpar, bias_all + o.n0);
+            else if (args.csize == 4)
+              epi_csplit<4>(d, o, z, taddr, row, grp, et, obase, obufs, bar_acc, acc_phase,
+                            bar_crdy, bar_crx, cpar, bias_all + o.n0);
+            else
+              epi_csplit<2>(d, o, z, taddr, row, grp, et, obase, obufs, bar_acc, acc_phase,
+                            bar_crdy, bar_crx, cpar, bias_all + o.n0);
+            cpar ^= 1u;
+          } else if (d.splits > 1) {
             // fp32 partial tile: 32-column chunks through the staging buffers (same protocol
             // as the TMA epilogue), drained by TMA stores into [tile][split][128][bn]
             mbar_wait_to<kEpiWaitNs>(bar_tfull + 8 * acc, acc_phase, 7);
@@ -1742,17 +1927,21 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
+        if (d.csplit) {  // (this CTA had tasks: the cluster's ranks all did)
+          csplit_drain(args.csize, et, bar_cdone, cdpar);
+          cdpar ^= 1u;
+        }
         // one release per layer and CTA: all of its tasks' stores (the TMA stores complete,
         // the threads' own stores cumulative over the bar.sync)
         CW_KET(90);
-        if (et == 0) {
+        if ((et & 31) == 0) {  // (et 0: TMA stores; lane 0 of every warp: split-K row stores)
           bulk_wait_all();
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         CW_KET(91);
         named_bar(1, kMkEpiThreads);
         if (et == 0) {
-          if (d.pool_out) red_release_add(counters + L, (uint32_t)done);  // generic stores
+          if (d.pool_out || d.csplit) red_release_add(counters + L, (uint32_t)done);  // generic stores
           else red_after_bulk_add(counters + L, (uint32_t)done);
         }
         CW_KET(92);
@@ -1822,6 +2011,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     tc_fence_after();
     tmem_dealloc(tmem, kMkTmemCols);
   }
+  // (every remote access to this CTA's shared memory is awaited by this CTA itself; the
+  // cluster barrier only keeps the exits ordered behind the cluster's last DSMEM traffic)
+  if (args.csize > 1) cluster_sync();
   if (clk_trace && threadIdx.x == 0) {
     clk_trace[3] = clock64();
     clk_trace[2] = globaltimer();
@@ -1852,8 +2044,29 @@ __global__ void mk_done_kernel(const ActionBlock* ab, uint32_t ring_mask, ExecRe
 // ------------------------------------------------------------------ host side
 
 cudaError_t configure_mk() {
-  return cudaFuncSetAttribute(mk_infer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              kMkSmemCap);
+  cudaError_t e = cudaFuncSetAttribute(mk_infer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kMkSmemCap);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(mk_infer_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+}
+
+// CTAs of the persistent grid for clusters of `csize` (all co-resident: CTAs wait on each
+// other): the number of clusters of that size the GPU can hold at once, times csize.
+int mk_cluster_ctas(int csize, uint32_t smem) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(csize * 256);
+  cfg.blockDim = dim3(kMkThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, mk_infer_kernel, &cfg) != cudaSuccess) return 0;
+  return n * csize;
 }
 
 uint32_t mk_smem_bytes(uint32_t ring_bytes, int n_layers) {
@@ -1881,27 +2094,34 @@ cudaError_t copy_plan(const MkLayer* d_layers, int n, cudaStream_t st) {
 // predecessor in the stream completes; it synchronises with griddepcontrol.wait.
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, uint32_t smem,
-                              cudaStream_t st, Args&&... args) {
+                              cudaStream_t st, int csize, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (csize > 1) {
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = csize;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.numAttrs = 2;
+  }
   return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 cudaError_t launch_mk(const MkArgs& a, int grid, uint32_t smem, cudaStream_t st) {
-  return launch_pdl(mk_infer_kernel, dim3(grid), dim3(kMkThreads), smem, st, a);
+  return launch_pdl(mk_infer_kernel, dim3(grid), dim3(kMkThreads), smem, st, a.csize, a);
 }
 
 void launch_mk_done(const ActionBlock* ab, uint32_t mask, ExecRecord* recs, uint32_t* gen,
                     volatile uint64_t* done, cudaStream_t st) {
-  launch_pdl(mk_done_kernel, dim3(1), dim3(1), 0, st, ab, mask, recs, gen, done);
+  launch_pdl(mk_done_kernel, dim3(1), dim3(1), 0, st, 1, ab, mask, recs, gen, done);
 }
 
 }  // namespace cw

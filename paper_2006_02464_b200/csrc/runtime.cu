@@ -366,10 +366,15 @@ static void box_dims(int nimg, int oh, int ow, int* bw, int* bh, int* bn) {
 //     plus ~0.8 us of fixed latency per tile (bias / residual loads, barriers);
 //   * a split-K reduce layer costs ~3 us plus its partial-tile traffic.
 // Epilogue of task i overlaps the MMAs of task i+1 (two TMEM accumulators).
-static void plan_conv(MkLayer& d, int cout, int G, bool allow_split, bool grouped = false) {
+// Cluster plans (csize > 1): a split conv uses exactly csize splits, one per CTA of a
+// cluster, reduced through distributed shared memory in the epilogue (~2.5 us, no reduce layer,
+// no partials in global memory); bn = 64 (received partials + the staged own tile = 64 KB).
+static void plan_conv(MkLayer& d, int cout, int G, bool allow_split, bool grouped, int csize) {
   // a split layer adds a reduce layer and one more whole-GPU dependency (~6 us in the
   // network, measured with tools/sweep_bn.sh + op_profile; CW_SPLIT_US overrides)
   static const double split_us = exp_env("CW_SPLIT_US") ? atof(exp_env("CW_SPLIT_US")) : 6.0;
+  static const double csplit_us = exp_env("CW_CSPLIT_US") ? atof(exp_env("CW_CSPLIT_US")) : 2.5;
+  const int units = d.num_kb / (d.mode == 3 ? 3 : 1);
   static const int kBn[3] = {256, 128, 64};
   const double rows = d.mode == 0 ? 128.0 : (double)(d.box_w * d.box_h * d.box_n);
   const double a_bytes = rows * d.kblk * 2;
@@ -383,17 +388,28 @@ static void plan_conv(MkLayer& d, int cout, int G, bool allow_split, bool groupe
     const int n_tma = 1 + ((bn == std::min(256, cout) && d.kblk == 64) ? 1 : bn / 64);
     const double t_kb = std::max({0.30, 0.08 * n_tma + 0.1, (a_bytes + bn * d.kblk * 2.0) / 140e3});
     for (int s = 1; s <= 32; ++s) {
-      if (s > 1 && (!allow_split || d.num_kb / s < 2)) break;
-      int per = (d.num_kb + s - 1) / s;
-      if (d.mode == 3) per = (per + 2) / 3 * 3;  // whole (kernel row, channel block) groups
-      const int splits = (d.num_kb + per - 1) / per;
-      if (splits != s) continue;
+      int per;
+      if (csize > 1) {
+        // cluster plans: no split, or exactly csize non-empty splits
+        // (one wave at most: the ranks of a cluster wait for each other at every task)
+        if (s > 1 && (s != csize || !allow_split || bn != 64 || units < s || d.num_kb / s < 1 ||
+                      tiles * s > G))
+          continue;
+        per = (units + s - 1) / s * (d.mode == 3 ? 3 : 1);
+      } else {
+        if (s > 1 && (!allow_split || d.num_kb / s < 2)) break;
+        per = (d.num_kb + s - 1) / s;
+        if (d.mode == 3) per = (per + 2) / 3 * 3;  // whole (kernel row, channel block) groups
+        const int splits = (d.num_kb + per - 1) / per;
+        if (splits != s) continue;
+      }
       const int tasks = tiles * s;
       const int waves = (tasks + G - 1) / G;
       const double t_main = per * t_kb;
       const double t_epi = rows * bn * (s > 1 ? 4.0 : 2.0) / 20e3 + 0.8;  // + per-task fixed cost
       double t = waves * std::max(t_main, t_epi) + std::min(t_main, t_epi) + 1.5;
-      if (s > 1) t += split_us + (double)tiles * 128 * bn * (4.0 * s + 2.0) / (G * 40e3);
+      if (s > 1 && csize > 1) t += csplit_us;
+      else if (s > 1) t += split_us + (double)tiles * 128 * bn * (4.0 * s + 2.0) / (G * 40e3);
       if (t < best - 1e-9) {
         best = t;
         best_bn = bn;
@@ -408,8 +424,10 @@ static void plan_conv(MkLayer& d, int cout, int G, bool allow_split, bool groupe
   }
   if (const char* e = exp_env("CW_FORCE_SPLIT")) {
     const int sp = atoi(e);
-    if (sp > 0 && allow_split && d.num_kb / sp >= 1) best_s = sp;
+    if (sp > 0 && allow_split && d.num_kb / sp >= 1 && (csize <= 1 || sp == 1 || sp == csize))
+      best_s = sp;
   }
+  d.csplit = csize > 1 && best_s > 1;
   d.bn = best_bn;
   d.n_tiles = cout / best_bn;
   d.splits = best_s;
@@ -492,7 +510,22 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
   p.layers.clear();
   p.layer_op.clear();
   p.tmaps.clear();
-  const int G = num_sms_;
+  // Cluster split-K (csize > 1) for small batches, whose layers have far fewer output tiles
+  // than SMs: the persistent grid then holds as many whole clusters as the GPU co-schedules
+  // (B200: 120 CTAs in clusters of 8, 132 in clusters of 4, all 148 in pairs). Measured
+  // (ResNet-50 Exec p50 without -> with, tools/ab_quick.py): b=1 275 -> 248 us (8), b=2 305 ->
+  // 279 (4), b=4 346 -> 309 (4), b=8 422 -> 400 (2), b=16 551 -> 524 (2).
+  int csize = batch == 1 ? 8 : batch <= 4 ? 4 : 2;
+  if (const char* e = exp_env("CW_CSIZE")) csize = atoi(e);
+  if (csize != 1 && csize != 2 && csize != 4 && csize != 8) return "cluster size must be 1, 2, 4 or 8";
+  int G = num_sms_;
+  if (csize > 1) {
+    const uint32_t fixed0 = mk_smem_bytes(0, 0);
+    const int ctas = mk_cluster_ctas(csize, mk_smem_bytes((kMkSmemCap - fixed0) / 1024 * 1024, 0));
+    if (ctas >= 2 * csize) G = std::min(ctas, num_sms_) / csize * csize;
+    else csize = 1;
+  }
+  p.csize = csize;
   DepTracker deps;
   size_t partial_need = 0;
   int rot = 0;
@@ -504,6 +537,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
     if (L >= kMkMaxPlanLayers) return "plan has too many layers";
     std::string err = deps.add(d, L, rd, wr);
     if (!err.empty()) return err;
+    if (d.csplit) rot = (rot + csize - 1) / csize * csize % G;  // split z on cluster rank z
     d.rot = rot;
     rot = (rot + d.tasks) % G;
     p.layers.push_back(d);
@@ -646,7 +680,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
             return "tensor map (nhwc) failed";
         }
         // (the fused pool runs in the epilogue of whole-image tiles: no split-K there)
-        plan_conv(d, cout_p, G, allow_split && !fuse_pool && !d.pool_pw, grouped);
+        plan_conv(d, cout_p, G, allow_split && !fuse_pool && !d.pool_pw, grouped, csize);
         d.tmap = (int)p.tmaps.size();
         p.tmaps.push_back(tm);
         d.tmap_out = d.tmap_res = -1;
@@ -688,10 +722,10 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
           d.out = nullptr;
           wr.push_back(Access{nxt->out_buf});
           ++oi;  // the avgpool op is done in this layer's epilogue
-        } else if (d.splits == 1) {
+        } else if (d.splits == 1 || d.csplit) {
           wr.push_back(out_acc);
         }
-        if (d.splits > 1) {
+        if (d.splits > 1 && !d.csplit) {
           wr.push_back(Access{kBufPartial});
           const size_t tiles = (size_t)d.m_tiles * d.n_tiles;
           partial_need = std::max(partial_need, tiles * d.splits * 128 * d.bn * 4);
@@ -886,7 +920,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
   if (partial_need) {
     CW_TRY(cudaMalloc(&p.d_partial, partial_need));
     for (auto& d : p.layers) {
-      if (d.kind == MK_CONV && d.splits > 1) {
+      if (d.kind == MK_CONV && d.splits > 1 && !d.csplit) {
         // the split conv TMA-stores fp32 partial chunks: [tiles * S * 128][bn], 32-column boxes
         d.partial = p.d_partial;
         CUtensorMap mp;
@@ -936,6 +970,7 @@ std::string Runtime::capture(Arch& a, Plan& p) {
   for (const auto& d : p.layers)
     if (d.kind == MK_CONV && d.pre_layer >= 0) args.pre_bn = 1;
   args.softmax = p.layers.back().kind == MK_SOFTMAX;
+  args.csize = p.csize;
   CW_TRY(cudaStreamBeginCapture(s_cap_, cudaStreamCaptureModeThreadLocal));
   cudaError_t ce = copy_plan(p.d_layers, (int)p.layers.size(), s_cap_);
   launch_gate(ab_, ring_, kRing - 1, ctr_, exec_recs_, s_cap_);

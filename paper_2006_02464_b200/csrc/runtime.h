@@ -63,6 +63,7 @@ struct Plan {
   float* d_partial = nullptr;
   uint32_t ring_bytes = 0, smem = 0;
   int grid = 0;
+  int csize = 1;  // thread-block cluster size of the megakernel launch (cluster split-K)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   int launches = 0;  // kernels per INFER (gate + megakernel + done)

@@ -152,8 +152,16 @@ class DeviceRuntime:
         tr = np.where(raw[:n_layers] > 0, raw[:n_layers] - t0, -1)
         return tr, t0, clk
 
+    def plan_launch(self, arch_id: int, batch: int) -> tuple[int, int]:
+        """(persistent grid CTAs, thread-block cluster size) of a plan's megakernel."""
+        g = C.c_int32()
+        c = C.c_int32()
+        check(lib.cw_rt_plan_launch(self.h, arch_id, batch, C.byref(g), C.byref(c)), "plan_launch")
+        return g.value, c.value
+
     def plan_layers(self, arch_id: int, batch: int) -> np.ndarray:
-        """[layers][8]: kind, conv mode, N tile, tasks, split-K, k-blocks, arch op, fused pool."""
+        """[layers][8]: kind, conv mode, N tile, tasks, split-K, k-blocks, arch op, flags
+        (1 fused avgpool, 2 cluster split-K)."""
         n = 1024
         out = np.zeros((n, 8), np.int32)
         got = check(lib.cw_rt_plan_layers(self.h, arch_id, batch,

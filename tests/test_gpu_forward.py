@@ -79,3 +79,32 @@ def test_layer_handoff_repeatable_under_alternating_inputs(gpu, r50, batch):
             got, _ = rt.infer(0, 0, xs[i & 1])
             bad += not np.array_equal(got, first[i & 1])
     assert bad == 0, f"{bad} INFERs differ from the first run of their input"
+
+
+@pytest.mark.parametrize("batch,csize", [(1, 8), (2, 4), (4, 4), (8, 2), (16, 2)])
+def test_cluster_split_plans(gpu, r50, batch, csize):
+    """Small-batch plans launch the megakernel in thread-block clusters and reduce split-K
+    convs through distributed shared memory (no reduce layers): the persistent grid is whole
+    clusters, every cluster split-K layer has tasks = tiles x csize on a csize-aligned
+    rotation, and back-to-back INFERs (the cluster handshakes' mbarrier phases carry over
+    from task to task and INFER to INFER) reproduce the logits bit for bit."""
+    spec, blob, model = r50
+    x = arch.make_inputs(batch, spec, first=5 * batch)
+    with DeviceRuntime(device=gpu, pages_total=8, io_slots=16) as rt:
+        rt.register_arch(0, spec, batches=(batch,))
+        rt.register_blob(0, 0, blob)
+        rt.build()
+        rt.load(0, [0, 1, 2, 3][:blob.pages])
+        grid, cs = rt.plan_launch(0, batch)
+        assert cs == csize and grid % cs == 0 and grid >= 8 * cs
+        layers = rt.plan_layers(0, batch)
+        csplit = layers[(layers[:, 7] & 2) != 0]
+        assert len(csplit) > 0
+        assert (csplit[:, 4] == cs).all() and (csplit[:, 2] == 64).all()
+        assert not (layers[:, 0] == 6).any()  # no MK_REDUCE layers in a cluster plan
+        first, _ = rt.infer(0, 0, x)
+        for _ in range(3):
+            again, _ = rt.infer(0, 0, x)
+            assert np.array_equal(first, again)
+    c = resnet_oracle.compare(first, resnet_oracle.logits(model, x))
+    assert c["ok"], c
