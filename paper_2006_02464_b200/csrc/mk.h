@@ -110,6 +110,11 @@ struct MkLayer {
   // on cluster rank z): the partial tiles are reduced through distributed shared memory in the
   // epilogue (no fp32 partials in global memory, no reduce layer)
   int32_t csplit;
+  // conv: a second K segment accumulated into the same tile (a bottleneck's projection
+  // shortcut fused into its conv3: K = [conv3's input | the block input], the shortcut's
+  // 1x1 / stride f_stride conv read through its own A map f_tmap and weight layer f_wlayer);
+  // k-blocks [num_kb - f_kb, num_kb) belong to it; f_kb == 0: no second segment
+  int32_t f_tmap, f_wlayer, f_kb, f_stride;
   void* out;              // bf16 NHWC output (conv / reduce / pools), NHWC4 (input)
   const void* res;        // bf16 residual, same shape as out, or null
   float* partial;         // split-K fp32 partials [tile][split][128][bn]
@@ -121,7 +126,7 @@ static_assert(sizeof(MkLayer) % 16 == 0, "MkLayer is copied in 16-byte units");
 // The plan's layer table lives in a __constant__ bank (mk_infer.cu), refreshed by a
 // device-to-device memcpy node at the head of every INFER graph: uniform (ULDC) operand
 // reads for the producer / MMA loops and no shared memory, whatever the depth of the net.
-constexpr int kMkMaxPlanLayers = 220;
+constexpr int kMkMaxPlanLayers = 210;
 static_assert(kMkMaxPlanLayers * sizeof(MkLayer) <= 64000, "constant bank (64 KB)");
 
 struct MkArgs {

@@ -1233,14 +1233,17 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
             if (Ln >= nl) break;
             if ((sl[Ln].kind == MK_FC || sl[Ln].mode != 2) && elect_one()) {
               const MkLayer& dn = sl[Ln];
-              const uint8_t* w =
-                  reinterpret_cast<const uint8_t* const*>(hdr + kHdrWeightOff)[dn.wlayer];
-              const uint32_t bytes = dn.kind == MK_FC
-                                         ? (uint32_t)dn.classes * (uint32_t)dn.C * 2u
-                                         : (uint32_t)dn.n_out * (uint32_t)(dn.num_kb * dn.kblk) * 2u;
-              const uint32_t per = ((bytes + G - 1) / G + 255u) & ~255u;
-              const uint32_t off = (uint32_t)cta * per;
-              if (off < bytes) bulk_prefetch_l2(w + off, min(per, bytes - off));
+              const uint8_t* const* wt = reinterpret_cast<const uint8_t* const*>(hdr + kHdrWeightOff);
+              // (a fused shortcut: its weight layer is the second segment)
+              for (int sg = 0; sg < (dn.kind == MK_CONV && dn.f_kb ? 2 : 1); ++sg) {
+                const uint8_t* w = wt[sg ? dn.f_wlayer : dn.wlayer];
+                const uint32_t kbs = dn.kind == MK_FC ? 0u : (uint32_t)(sg ? dn.f_kb : dn.num_kb - dn.f_kb);
+                const uint32_t bytes = dn.kind == MK_FC ? (uint32_t)dn.classes * (uint32_t)dn.C * 2u
+                                                        : (uint32_t)dn.n_out * kbs * (uint32_t)dn.kblk * 2u;
+                const uint32_t per = ((bytes + G - 1) / G + 255u) & ~255u;
+                const uint32_t off = (uint32_t)cta * per;
+                if (off < bytes) bulk_prefetch_l2(w + off, min(per, bytes - off));
+              }
             }
             __syncwarp();
           }
@@ -1254,10 +1257,20 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         const bool wide = d.kblk == 64 && d.bn == min(256, d.n_out);
         const CUtensorMap* tb = reinterpret_cast<const CUtensorMap*>(
             hdr + (wide ? kHdrWideOff : 0) + d.wlayer * kTmapBytes);
+        // a fused shortcut (k-blocks [seg1, num_kb)): its own A map and weight layer
+        const int seg1 = d.num_kb - d.f_kb;
+        const CUtensorMap* ta2 = args.tmaps + d.f_tmap;
+        const CUtensorMap* tb2 = reinterpret_cast<const CUtensorMap*>(
+            hdr + (wide ? kHdrWideOff : 0) + d.f_wlayer * kTmapBytes);
         if (elect_one()) {
           tmap_acquire(tb);
           tmap_prefetch(ta);
           tmap_prefetch(tb);
+          if (d.f_kb) {
+            tmap_acquire(tb2);
+            tmap_prefetch(ta2);
+            tmap_prefetch(tb2);
+          }
         }
         __syncwarp();
         const int ns = d.slots;
@@ -1395,6 +1408,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           split_range(d, z, kb0, kb1);
           const int wb = o.ow0 * d.stride - d.pad_w;
           const int hb = o.oh0 * d.stride - d.pad;
+          const int wb2 = o.ow0 * d.f_stride, hb2 = o.oh0 * d.f_stride;  // fused shortcut (1x1)
           const int chan0 = d.grouped ? o.n0 : 0;  // grouped: the tile's own channel block
           // A coordinates walk k-blocks in order: (channel block, tap column q, tap row r)
           int a_kb = kb0, a_c0 = 0, a_q = 0, a_r = 0;
@@ -1416,11 +1430,12 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
 #define CW_LOAD_B(kb_, dst0_, s_)                                                   \
   do {                                                                              \
     const uint32_t dst_ = (dst0_) + b_off;                                          \
-    const int kx_ = (kb_) * kblk;                                                   \
+    const bool s2_ = (kb_) >= seg1;                                                 \
+    const int kx_ = ((kb_) - (s2_ ? seg1 : 0)) * kblk;                              \
     if (elect_one())                                                                \
       for (int j = 0; j < (no_b ? 0 : nbox); ++j)                                   \
-        tma_load_2d_hint(dst_ + j * b_box, tb, fullb + 8 * (s_), kx_, o.n0 + 64 * j,    \
-                         kHintW);                                                       \
+        tma_load_2d_hint(dst_ + j * b_box, s2_ ? tb2 : tb, fullb + 8 * (s_), kx_,   \
+                         o.n0 + 64 * j, kHintW);                                    \
     __syncwarp();                                                                   \
   } while (0)
 #define CW_ADV_A()                                                                      \
@@ -1442,6 +1457,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
     const uint32_t fb_ = fullb + 8 * (s_);                                             \
     if (elect_one()) {                                                                 \
       if (no_a) {                                                                      \
+      } else if (a_kb >= seg1) {                                                       \
+        if (mode == 0) tma_load_2d(dst_, ta2, fb_, (a_kb - seg1) * 64, o.m0);          \
+        else tma_load_4d(dst_, ta2, fb_, (a_kb - seg1) * 64, wb2, hb2, o.img0);        \
       } else if (mode == 0) {                                                          \
         tma_load_2d(dst_, ta, fb_, a_kb * 64, o.m0);                                   \
       } else if (mode == 1) {                                                          \
@@ -1702,7 +1720,14 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         if (d.splits == 1) {
           // the layer's whole folded-BN bias (weights: no dependency), once per layer: no
           // per-task global loads or barriers (the previous layer ended on a barrier)
-          for (int i = et; i < d.n_out; i += kMkEpiThreads) sbias[i] = __ldg(bias_all + i);
+          if (d.f_kb) {  // fused shortcut: the two folded-BN biases add up
+            const float* bias_sc =
+                reinterpret_cast<const float* const*>(hdr + kHdrBiasOff)[d.f_wlayer];
+            for (int i = et; i < d.n_out; i += kMkEpiThreads)
+              sbias[i] = __ldg(bias_all + i) + __ldg(bias_sc + i);
+          } else {
+            for (int i = et; i < d.n_out; i += kMkEpiThreads) sbias[i] = __ldg(bias_all + i);
+          }
         }
         if (et == 0) wait_deps(sl, L, counters, gen1, 6);
         named_bar(1, kMkEpiThreads);
@@ -1850,15 +1875,16 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
                 auto chunk = [buf, row](int k) {
                   return reinterpret_cast<uint4*>(buf + row * 128 + ((k ^ (row & 7)) << 4));
                 };
+                // this thread's row: its group's 32 columns of the chunk (groups 4 grp .. +3),
+                // in flight while the residual chunk is awaited
+                uint32_t v[32];
+                tmem_ld16(taddr + 64 * c + 32 * grp, *reinterpret_cast<uint32_t(*)[16]>(v));
+                tmem_ld16(taddr + 64 * c + 32 * grp + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
                 if (tmr) {
                   mbar_wait_to<64>(bar_res + 8 * b, (rpar >> b) & 1, 11);
                   rpar ^= 1u << b;
                 }
                 CW_KET(10 + c);
-                // this thread's row: its group's 32 columns of the chunk (groups 4 grp .. +3)
-                uint32_t v[32];
-                tmem_ld16(taddr + 64 * c + 32 * grp, *reinterpret_cast<uint32_t(*)[16]>(v));
-                tmem_ld16(taddr + 64 * c + 32 * grp + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
                 uint4 rv[4];
                 if (tmr) {
 #pragma unroll

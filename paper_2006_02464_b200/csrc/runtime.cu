@@ -544,9 +544,47 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
     p.layer_op.push_back(oi);
     return "";
   };
+  // A bottleneck's projection shortcut (1x1 / stride s conv, no ReLU, no residual) whose output
+  // is read only as the residual of the NEXT op, a 1x1 / stride 1 conv of the same output shape,
+  // runs inside that conv as a second K segment: one layer, no shortcut tensor in memory, no
+  // residual read, one rounding (the kernel sequence is ours to choose).
+  auto fusable_shortcut = [&](size_t i) -> bool {
+    if (i + 1 >= a.ops.size()) return false;
+    const CwOp& s = a.ops[i];
+    const CwOp& c = a.ops[i + 1];
+    if (s.kind != OP_CONV || c.kind != OP_CONV) return false;
+    if (s.relu || s.res_buf >= 0 || s.flags || c.flags || s.kh != 1 || s.kw != 1 || s.pad ||
+        s.pad_w || (s.stride != 1 && s.stride != 2))
+      return false;
+    if (c.kh != 1 || c.kw != 1 || c.stride != 1 || c.pad || c.pad_w || c.res_buf != s.out_buf)
+      return false;
+    if (c.cout != s.cout || c.cout_pad != s.cout_pad || c.out_h != s.out_h || c.out_w != s.out_w ||
+        s.out_ctot != s.cout || s.out_coff || c.out_ctot != c.cout || c.out_coff)
+      return false;
+    if (s.kpad % 64 || c.kpad % 64 || s.cin % 64 || c.cin % 64) return false;
+    if (c.in_buf == s.out_buf) return false;
+    // small batches: a deep shortcut (stages 3-4: 8-16 k-blocks) ran on SMs the 3x3 conv before
+    // it leaves idle; serialised into conv3 it costs more than the layer it saves (ResNet-50
+    // b=1: stage 1 -2.4 us, stage 2 -1.8, stage 3 +2.0, stage 4 +4.3; b=16: -8.5 .. -0.5)
+    if (batch < 8 && s.kpad / 64 > 4) return false;
+    // the shortcut tensor must be dead after the conv: no later read before a rewrite
+    for (size_t j = i + 2; j < a.ops.size(); ++j) {
+      const CwOp& o = a.ops[j];
+      if (o.in_buf == s.out_buf || o.res_buf == s.out_buf) return false;
+      if (o.out_buf == s.out_buf) break;
+    }
+    return true;
+  };
+  const bool fuse_shortcuts = exp_env("CW_NO_FUSE_SC") == nullptr;  // (experiments: A/B)
+  int shortcut = -1;  // op index of the shortcut fused into the next conv
   for (size_t oi = 0; oi < a.ops.size(); ++oi) {
     const CwOp& op = a.ops[oi];
     if (fc_seen && op.kind != OP_SOFTMAX) return "the FC op must be the last op (or a softmax)";
+    if (fuse_shortcuts && fusable_shortcut(oi)) {
+      shortcut = (int)oi;
+      continue;
+    }
+    const CwOp* sc = (shortcut >= 0 && (size_t)shortcut + 1 == oi) ? &a.ops[shortcut] : nullptr;
     MkLayer d;
     memset(&d, 0, sizeof(d));
     d.pre_layer = -1;
@@ -586,7 +624,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
         d.pre_layer = pre_bn ? op.pre_layer : -1;
         d.out_ctot = op.out_ctot;
         d.out_coff = op.out_coff;
-        d.res = op.res_buf >= 0 ? a.bufs[op.res_buf] : nullptr;
+        d.res = (op.res_buf >= 0 && !sc) ? a.bufs[op.res_buf] : nullptr;
         if (d.res && (op.out_ctot != op.cout || op.out_coff)) return "residual into a concat slice";
         // the layer's channel slice of its output buffer: every store of the layer (TMA maps,
         // split-K reduce rows) addresses it from here with the buffer's channel stride
@@ -629,7 +667,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
                               op.out_w, op.out_h, d.box_w, d.box_h))
             return "tensor map (stem) failed";
         } else if (!fuse_pool && op.kh == 1 && op.kw == 1 && op.stride == 1 && op.pad == 0 &&
-                   op.pad_w == 0) {
+                   op.pad_w == 0 && !(sc && sc->stride != 1)) {
           // 1x1: A = the [M][cin] matrix of the input buffer (row stride in_ctot; channels
           // >= cin are out of bounds: zero-filled)
           d.mode = 0;
@@ -679,10 +717,32 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
                               op.stride, op.in_ctot))
             return "tensor map (nhwc) failed";
         }
-        // (the fused pool runs in the epilogue of whole-image tiles: no split-K there)
-        plan_conv(d, cout_p, G, allow_split && !fuse_pool && !d.pool_pw, grouped, csize);
+        CUtensorMap tm2;
+        if (sc) {
+          // the shortcut's K segment: its input through a map with the SAME row tiling (mode 0:
+          // [M][cin] rows of the block input; mode 1: the box over the strided input pixels)
+          void* sin = a.bufs[sc->in_buf];
+          const bool ok = d.mode == 0
+                              ? make_tmap_2d(&tm2, sin, (uint64_t)sc->cin, (uint64_t)d.m_total, 128,
+                                             (uint64_t)sc->in_ctot)
+                              : make_tmap_nhwc(&tm2, sin, batch, sc->in_h, sc->in_w, sc->cin,
+                                               d.box_w, d.box_h, d.box_n, sc->stride, sc->in_ctot);
+          if (!ok) return "tensor map (fused shortcut) failed";
+          if (d.mode != 0 && d.mode != 1) return "fused shortcut on an unsupported conv mode";
+          d.f_kb = sc->kpad / 64;
+          d.f_wlayer = sc->layer;
+          d.f_stride = sc->stride;
+          d.num_kb += d.f_kb;
+        }
+        // (the fused pool runs in the epilogue of whole-image tiles: no split-K there; nor in a
+        // layer with a fused shortcut, whose bias is the sum of two layers')
+        plan_conv(d, cout_p, G, allow_split && !fuse_pool && !d.pool_pw && !sc, grouped, csize);
         d.tmap = (int)p.tmaps.size();
         p.tmaps.push_back(tm);
+        if (sc) {
+          d.f_tmap = (int)p.tmaps.size();
+          p.tmaps.push_back(tm2);
+        }
         d.tmap_out = d.tmap_res = -1;
         if (d.pool_pw) {  // stem: pooled output tiles of pool_pw pixels
           CUtensorMap mo;
@@ -713,6 +773,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
         }
         const Access out_acc{op.out_buf, op.out_coff, op.out_coff + op.cout};
         std::vector<Access> rd = {Access{op.in_buf, 0, op.cin}}, wr;
+        if (sc) rd.push_back(Access{sc->in_buf, 0, sc->cin});
         if (d.pool_pw) {
           wr.push_back(Access{nxt->out_buf, nxt->out_coff, nxt->out_coff + nxt->cout});
           ++oi;  // the max pool op is done in this layer's epilogue
@@ -758,7 +819,7 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
           if (op.res_buf >= 0) rrd.push_back(Access{op.res_buf});
           err = push(r, (int)oi, rrd, {out_acc});
         } else {
-          if (op.res_buf >= 0) rd.push_back(Access{op.res_buf});
+          if (op.res_buf >= 0 && !sc) rd.push_back(Access{op.res_buf});
           err = push(d, (int)oi, rd, wr);
         }
         break;
