@@ -948,6 +948,51 @@ __device__ __noinline__ void csplit_drain(int C, int et, uint32_t bar_cdone, uin
 // (3 conv rows x 2*pool_pw+1 columns) -> bias, ReLU, bf16 into the CTA staging
 // buffer, then each pooled pixel = max over its valid 3x3 window (identical to
 // pooling the bf16 conv output; padding = -inf = skipped).
+// One epilogue thread's share of one 64-column chunk of the TMA epilogue: its row's 32
+// accumulator columns `v` (in registers) + folded-BN bias (+ the residual chunk that landed in
+// the staging buffer) (+ ReLU) -> bf16, rewritten in place (128-byte swizzle). Branch-free
+// per (residual, ReLU) variant with every shared-memory load issued before the math (the
+// generic version's branches and its bias loads ordered behind stores measured ~550 cycles
+// per chunk, the whole epilogue warp's latency chain).
+template <bool RES, bool RELU>
+__device__ __forceinline__ void epi_chunk32(const uint32_t (&v)[32], const float* bias32,
+                                            uint8_t* buf, int row, int grp) {
+  const float4* bp = reinterpret_cast<const float4*>(__builtin_assume_aligned(bias32, 16));
+  float4 bq[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) bq[i] = bp[i];
+  uint4 rv[4];
+  if constexpr (RES) {
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      rv[kk] = *reinterpret_cast<const uint4*>(buf + row * 128 + (((4 * grp + kk) ^ (row & 7)) << 4));
+  }
+  uint32_t w[16];
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) {
+    const float bb[8] = {bq[2 * kk].x, bq[2 * kk].y, bq[2 * kk].z, bq[2 * kk].w,
+                         bq[2 * kk + 1].x, bq[2 * kk + 1].y, bq[2 * kk + 1].z, bq[2 * kk + 1].w};
+    float f[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[8 * kk + e]);
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) fadd2(f[e], f[e + 1], bb[e], bb[e + 1]);
+    if constexpr (RES) {
+      float rf[8];
+      bf16x8_to_f32(rv[kk], rf);
+#pragma unroll
+      for (int e = 0; e < 8; e += 2) fadd2(f[e], f[e + 1], rf[e], rf[e + 1]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      w[4 * kk + e] = RELU ? pack_bf16x2_relu(f[2 * e], f[2 * e + 1]) : pack_bf16x2(f[2 * e], f[2 * e + 1]);
+  }
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+    *reinterpret_cast<uint4*>(buf + row * 128 + (((4 * grp + kk) ^ (row & 7)) << 4)) =
+        make_uint4(w[4 * kk], w[4 * kk + 1], w[4 * kk + 2], w[4 * kk + 3]);
+}
+
 __device__ __forceinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigin o, uint32_t taddr,
                                            const float* bias, uint8_t* pb, uint8_t* ps,
                                            uint32_t ps_addr, const CUtensorMap* tmo, int row,
@@ -963,30 +1008,8 @@ __device__ __forceinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigi
     tmem_ld16(taddr + 32 * grp, *reinterpret_cast<uint32_t(*)[16]>(v));
     tmem_ld16(taddr + 32 * grp + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
     tmem_ld_wait();
-    if (row < d.box_w * d.box_h) {
-      uint4 wv[4];
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int k = 4 * grp + kk;
-        const float4 b0 = *reinterpret_cast<const float4*>(bias + 8 * k);
-        const float4 b1 = *reinterpret_cast<const float4*>(bias + 8 * k + 4);
-        const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-        float f[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[8 * kk + e]);
-#pragma unroll
-        for (int e = 0; e < 8; e += 2) fadd2(f[e], f[e + 1], bb[e], bb[e + 1]);
-        wv[kk].x = pack_bf16x2_relu(f[0], f[1]);
-        wv[kk].y = pack_bf16x2_relu(f[2], f[3]);
-        wv[kk].z = pack_bf16x2_relu(f[4], f[5]);
-        wv[kk].w = pack_bf16x2_relu(f[6], f[7]);
-      }
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int k = 4 * grp + kk;
-        *reinterpret_cast<uint4*>(pb + row * 128 + ((k ^ (row & 7)) << 4)) = wv[kk];
-      }
-    }
+    // (rows >= box_w * box_h of the staged tile are junk the pooling never reads)
+    epi_chunk32<false, true>(v, bias + 32 * grp, pb, row, grp);
   }
 #ifdef CW_KB_TRACE
   s1 = clock64();
@@ -1109,51 +1132,6 @@ __device__ __noinline__ void bn_prologue(const MkLayer* sl, int nl, int cta, int
       }
     }
   }
-}
-
-// One epilogue thread's share of one 64-column chunk of the TMA epilogue: its row's 32
-// accumulator columns `v` (in registers) + folded-BN bias (+ the residual chunk that landed in
-// the staging buffer) (+ ReLU) -> bf16, rewritten in place (128-byte swizzle). Branch-free
-// per (residual, ReLU) variant with every shared-memory load issued before the math (the
-// generic version's branches and its bias loads ordered behind stores measured ~550 cycles
-// per chunk, the whole epilogue warp's latency chain).
-template <bool RES, bool RELU>
-__device__ __forceinline__ void epi_chunk32(const uint32_t (&v)[32], const float* bias32,
-                                            uint8_t* buf, int row, int grp) {
-  const float4* bp = reinterpret_cast<const float4*>(__builtin_assume_aligned(bias32, 16));
-  float4 bq[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) bq[i] = bp[i];
-  uint4 rv[4];
-  if constexpr (RES) {
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk)
-      rv[kk] = *reinterpret_cast<const uint4*>(buf + row * 128 + (((4 * grp + kk) ^ (row & 7)) << 4));
-  }
-  uint32_t w[16];
-#pragma unroll
-  for (int kk = 0; kk < 4; ++kk) {
-    const float bb[8] = {bq[2 * kk].x, bq[2 * kk].y, bq[2 * kk].z, bq[2 * kk].w,
-                         bq[2 * kk + 1].x, bq[2 * kk + 1].y, bq[2 * kk + 1].z, bq[2 * kk + 1].w};
-    float f[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[8 * kk + e]);
-#pragma unroll
-    for (int e = 0; e < 8; e += 2) fadd2(f[e], f[e + 1], bb[e], bb[e + 1]);
-    if constexpr (RES) {
-      float rf[8];
-      bf16x8_to_f32(rv[kk], rf);
-#pragma unroll
-      for (int e = 0; e < 8; e += 2) fadd2(f[e], f[e + 1], rf[e], rf[e + 1]);
-    }
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      w[4 * kk + e] = RELU ? pack_bf16x2_relu(f[2 * e], f[2 * e + 1]) : pack_bf16x2(f[2 * e], f[2 * e + 1]);
-  }
-#pragma unroll
-  for (int kk = 0; kk < 4; ++kk)
-    *reinterpret_cast<uint4*>(buf + row * 128 + (((4 * grp + kk) ^ (row & 7)) << 4)) =
-        make_uint4(w[4 * kk], w[4 * kk + 1], w[4 * kk + 2], w[4 * kk + 3]);
 }
 
 // ------------------------------------------------------------------ the kernel
