@@ -278,6 +278,39 @@ int cw_net_serve(cw_engine* e, int fd, const uint8_t* handshake_frame, int64_t h
                  int64_t epoch_ns, cw_net_record* recs, int64_t rec_cap, int64_t* n_recs,
                  int64_t* n_actions);
 
+/* ------------------------------------------------------------------ cw_sched_*
+ * The controller fast path: the reference's Scheduler +
+ * ControllerState decision logic in native code, driven event by event by a thin shim that
+ * replaces sloserve.scheduler.Scheduler behind the unmodified harness
+ * (paper_2006_02464_b200/native_scheduler.py). Entry point -> reference method it replaces:
+ *   cw_sched_create     Scheduler.__init__ (scheduler.py:118-140), _ModelRuntime (:80-109)
+ *   cw_sched_handshake  Scheduler.on_handshake (scheduler.py:146-150)
+ *   cw_sched_request    Scheduler.on_request (scheduler.py:155-168) and what it pumps
+ *   cw_sched_result     Scheduler.on_result (scheduler.py:585-607), ControllerState.record_result
+ *                       (controller_state.py:264-285)
+ *   cw_sched_timer      Scheduler._deadline_check (scheduler.py:216-227) / _executor_wake (:671-678)
+ * Every call returns the number of output records (16 x int64 each, cw_sched_records) the
+ * shim replays in order: 1 action (send_action), 2 response (send_response), 3 timer
+ * (loop.call_at back into cw_sched_timer), 4 action-sink row. Action request ids are in
+ * cw_sched_ids. cfg[7]: work_horizon, capacity_horizon, lead_slack, tardy_slack,
+ * unload_tardy, estimator_window, default_slo (SchedulerConfig, scheduler.py:51-60). */
+typedef struct cw_sched cw_sched;
+cw_sched* cw_sched_create(int32_t n_models, const int32_t* n_sizes, const int32_t* sizes,
+                          const int64_t* exec_dur, const int64_t* input_transfer,
+                          const int64_t* output_transfer, const int64_t* weights_transfer,
+                          const int32_t* pages_needed, const int64_t* cfg, double load_eps);
+void cw_sched_destroy(cw_sched* s);
+int cw_sched_handshake(cw_sched* s, int32_t worker_id, int32_t gpu_count, int64_t pages_total);
+int cw_sched_request(cw_sched* s, int64_t now, uint64_t request_id, int64_t model_id, int64_t slo);
+int cw_sched_result(cw_sched* s, int64_t now, uint64_t action_id, int32_t status, int64_t start,
+                    int64_t end, int64_t device_duration);
+int cw_sched_timer(cw_sched* s, int64_t now, int32_t kind, int64_t a, int64_t b, int64_t c);
+const int64_t* cw_sched_records(cw_sched* s);
+const uint64_t* cw_sched_ids(cw_sched* s, int64_t* n);
+int64_t cw_sched_live(cw_sched* s);
+/* CPython 3.12 sum() of floats (Neumaier), as the load statistics use it (for tests). */
+double cw_sched_fsum(const double* x, int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -128,6 +128,18 @@ SIGNATURES = [
     ("cw_wire_encode_handshake", C.c_int64, [C.c_uint32, C.c_uint32, C.c_uint64,
                                              C.POINTER(C.c_uint32), C.c_int32, C.c_char_p,
                                              C.c_int64]),
+    ("cw_sched_create", _P, [C.c_int32, _I32P, _I32P, _I64P, _I64P, _I64P, _I64P, _I32P,
+                             _I64P, C.c_double]),
+    ("cw_sched_destroy", None, [_P]),
+    ("cw_sched_handshake", C.c_int, [_P, C.c_int32, C.c_int32, C.c_int64]),
+    ("cw_sched_request", C.c_int, [_P, C.c_int64, C.c_uint64, C.c_int64, C.c_int64]),
+    ("cw_sched_result", C.c_int, [_P, C.c_int64, C.c_uint64, C.c_int32, C.c_int64, C.c_int64,
+                                  C.c_int64]),
+    ("cw_sched_timer", C.c_int, [_P, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_int64]),
+    ("cw_sched_records", _I64P, [_P]),
+    ("cw_sched_ids", C.POINTER(C.c_uint64), [_P, _I64P]),
+    ("cw_sched_live", C.c_int64, [_P]),
+    ("cw_sched_fsum", C.c_double, [C.POINTER(C.c_double), C.c_int64]),
     ("cw_net_serve", C.c_int, [_P, C.c_int, C.c_char_p, C.c_int64, C.c_int64,
                                C.POINTER(cw_net_record), C.c_int64, _I64P, _I64P]),
 ]

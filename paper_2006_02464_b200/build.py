@@ -35,7 +35,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall", "-I", CSRC,
           "-I", os.path.join(REPO, "include")]
 SOURCES = ["mk_infer.cu", "simt_kernels.cu", "runtime.cu", "tmap.cpp", "engine.cpp",
-           "capi_rt.cpp", "capi_engine.cpp", "net.cpp"]
+           "capi_rt.cpp", "capi_engine.cpp", "net.cpp", "sched.cpp"]
 
 
 def _headers() -> list[str]:
