@@ -567,6 +567,20 @@ def main():
                                              "copy, best of 5)"})
         except Exception as exc:  # noqa: BLE001 (diagnostic leg)
             line["load"]["link_error"] = str(exc)
+        try:
+            # the controller fast path against the reference scheduler in
+            # the same simulated harness (8 GPUs, 64 models, 20k req/s offered, 1 s)
+            sys.path.insert(0, os.path.join(REPO, "tools"))
+            import sched_throughput
+            ct = sched_throughput.run(20000.0, 1.0, 8, 64)
+            line["controller"] = {
+                "workload": "reference harness, sim mode: 8 emulated GPUs, 64 resnet50 copies, "
+                            "open loop 20k req/s offered, SLO 100 ms, 1 s horizon",
+                "reference_requests_per_wall_s": ct["reference"]["requests_per_wall_s"],
+                "native_requests_per_wall_s": ct["native"]["requests_per_wall_s"],
+                "speedup": ct["speedup"], "same_summary": ct["same_summary"]}
+        except Exception as exc:  # noqa: BLE001 (diagnostic leg)
+            line["controller"] = {"error": str(exc)}
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(res["spec"], res["params"], budget_s=15.0)
             try:
