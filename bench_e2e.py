@@ -125,8 +125,22 @@ def cold_group(workload, copies: int, rate: float):
 
 
 def run_controller(addresses, cat_text: str, epoch_ns: int, horizon_ns: int, groups,
-                   seed: int = 0) -> dict:
+                   seed: int = 0, native_sched: bool = False) -> dict:
+    """native_sched: the controller runs this repo's NativeScheduler (the reference
+    Scheduler's decisions in C++, SURVEY §8f rank 1) in place of sloserve.scheduler.Scheduler;
+    everything else (harness, clients, wire, summarize) stays the reference's."""
     harness, workload, profiles = sloserve()
+    ref_sched = harness.Scheduler
+    if native_sched:
+        from paper_2006_02464_b200.native_scheduler import NativeScheduler
+        harness.Scheduler = NativeScheduler
+    try:
+        return _run_controller(harness, addresses, cat_text, epoch_ns, horizon_ns, groups, seed)
+    finally:
+        harness.Scheduler = ref_sched
+
+
+def _run_controller(harness, addresses, cat_text, epoch_ns, horizon_ns, groups, seed):
     cfg = harness.ExperimentConfig(
         name="bench", seed=seed, mode="wall", transport="tcp", horizon_ns=horizon_ns,
         catalog_text=cat_text, workers=[harness.WorkerSpec(address=a) for a in addresses],
@@ -166,7 +180,7 @@ _READY_S: dict = {}  # observed worker startup time per (kind, catalog size), se
 
 def run_leg(kind: str, group_fn, copies: int, pages: int, horizon_ns: int, devices,
             startup_s: float, seed: int = 0, workdir: str | None = None,
-            cat_text: str | None = None) -> dict:
+            cat_text: str | None = None, native_sched: bool = False) -> dict:
     """Start one worker per device, run the reference controller against all of them for
     `horizon_ns`, score with summarize. `group_fn(workload)` builds the client groups;
     `cat_text` overrides the ResNet-50 x `copies` catalog."""
@@ -196,7 +210,7 @@ def run_leg(kind: str, group_fn, copies: int, pages: int, horizon_ns: int, devic
         if wait > 0:
             time.sleep(wait / 1e9)
         groups = group_fn(workload)
-        out = run_controller(addrs, cat, epoch, horizon_ns, groups, seed)
+        out = run_controller(addrs, cat, epoch, horizon_ns, groups, seed, native_sched)
     finally:
         # the harness closes its sockets but its reader threads keep them open for a while
         # (the worker would see EOF ~10 s later): the counts come from the controller's own

@@ -1760,8 +1760,6 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           const int tile = t / d.splits;
           const int z = t - tile * d.splits;
           const TileOrigin o = tile_origin(d, tile);
-          long long m;
-          const bool valid = row_pixel(d, o, row, &m);
           const uint32_t taddr = tmem + acc * 256 + ((uint32_t)(q * 32) << 16);
           if (d.csplit) {
             const uint32_t bar_acc = bar_tfull + 8 * acc;
@@ -1819,6 +1817,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
             } else if (d.pool_out) {
               // Last conv: + bias (+ residual), ReLU, then a deterministic in-CTA
               // global average pool (the tile holds whole images).
+              // (this row's pixel: only the pooled epilogue addresses rows itself)
+              long long m;
+              const bool valid = row_pixel(d, o, row, &m);
               const __nv_bfloat16* res_row =
                   (d.res && valid) ? reinterpret_cast<const __nv_bfloat16*>(d.res) + m * d.n_out + o.n0
                                    : nullptr;
