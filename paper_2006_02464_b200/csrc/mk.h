@@ -49,12 +49,17 @@ constexpr int kMkRegsCtl = 120;
 constexpr int kMkRegsEpi = 192;
 static_assert(kMkRegsCtl * 128 + kMkRegsEpi * 256 <= 65536, "register file");
 constexpr uint32_t kMkATile = 128 * 128;   // A tile: 128 rows x 128 B
-constexpr int kMkPadW = 4;                 // MK_INPUT: zero pixels left of every row
+// MK_INPUT: zero pixels left (and right) of every row. 4: conv column j of the 7x7/s2 stem
+// reads padded pixels 2j .. 2j+7 (input columns 2j-4 .. 2j+3: the weights' K slot 0 is the
+// zero tap), i.e. the 64 bytes at byte 16j of the row: 16-byte aligned rows of the stem's
+// implicit-im2col A operand (see the stem in mk_infer.cu)
+constexpr int kMkPadW = 4;
 constexpr int kMkPadH = 3;                 // MK_INPUT: zero rows above and below every image
-// stem (mode 2): one task = 3 conv rows x kMkStemW conv columns (120 rows of the A tile);
-// its A operand (all 7 kernel rows) is ONE 5D TMA box of 7 sub-tiles of kMkStemSub bytes
-constexpr int kMkStemW = 40;
-constexpr uint32_t kMkStemSub = 3u * kMkStemW * 64u;  // 7680 B: 512-B aligned (64-B swizzle atoms)
+// stem (mode 2): one task = one pooled output row = 3 conv rows x the full conv width; its A
+// operand is the kMkStemRows padded input rows those conv rows read, staged once (one TMA box),
+// each MMA reading conv column j's 8 pixels x 4 channels at byte 16j of a staged row
+// (overlapping rows of a no-swizzle K-major descriptor: LBO 16 B, SBO 128 B)
+constexpr int kMkStemRows = 11;
 // staging-buffer map: resident stem weights [0, 28 KB) (written by the producer while the
 // input conversion still runs), input-conversion stage [32 KB, 64 KB), stem-pool / split-K
 // scratch at 32 KB, avg-pool scratch at 16 KB

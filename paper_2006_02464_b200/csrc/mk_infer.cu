@@ -227,6 +227,14 @@ __device__ __forceinline__ uint64_t sw64_kmajor_desc(uint32_t smem_addr) {
          (4ull << 61);
 }
 
+// UMMA shared-memory descriptor, K-major, no swizzle: core matrices of 8 rows x 16 B, rows
+// 16 B apart; lbo = byte distance of K-adjacent core matrices, sbo = of M-adjacent ones. Rows
+// may overlap (lbo 16): the stem's implicit im2col (tools/umma_overlap_probe.cu checks it).
+__device__ __forceinline__ uint64_t desc_none(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((smem_addr & 0x3FFFFu) >> 4) | ((uint64_t)(lbo >> 4) << 16) |
+         ((uint64_t)(sbo >> 4) << 32) | (1ull << 46);
+}
+
 __device__ __forceinline__ int first_task(const MkLayer& d, int cta, int G) {
   int t = cta - d.rot % G;
   return t < 0 ? t + G : t;
@@ -998,82 +1006,66 @@ __device__ __forceinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigi
                                            uint32_t ps_addr, const CUtensorMap* tmo, int row,
                                            int grp, int et) {
   const MkLayer& d = *dp;
-#ifdef CW_KB_TRACE
-  const long long s0 = clock64();
-  long long s1 = 0, s2 = 0, s3 = 0;
-#endif
-  {
-    // this thread's row, its group's 32 columns (chunks 4 grp .. 4 grp + 3)
-    uint32_t v[32];
-    tmem_ld16(taddr + 32 * grp, *reinterpret_cast<uint32_t(*)[16]>(v));
-    tmem_ld16(taddr + 32 * grp + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
-    tmem_ld_wait();
-    // (rows >= box_w * box_h of the staged tile are junk the pooling never reads)
-    epi_chunk32<false, true>(v, bias + 32 * grp, pb, row, grp);
-  }
-#ifdef CW_KB_TRACE
-  s1 = clock64();
-#endif
-  if (et == 0) bulk_wait_read<0>();  // the previous tile's store has read the pooled stage
-  named_bar(1, kMkEpiThreads);
-#ifdef CW_KB_TRACE
-  s2 = clock64();
-#endif
-  const int pw0 = (o.ow0 + 1) / 2, ph = (o.oh0 + 1) / 2;
-  // pooled pixels -> staging rows (pool_pw x 128 B, 128-byte swizzle) -> one TMA store
-  // (columns past the image are clipped by the map)
-  const int bw = d.box_w, npix = d.pool_pw * 8;
-  // validity of the tile's 3 conv rows and of its conv columns (image borders = -inf)
-  uint32_t rmask = 0;
+  // 1) vertical max: this thread's conv column (accumulator row) over the task's 3 conv rows
+  // (accumulators 64 columns apart), ReLU folded in (maxima start at 0: post-ReLU values are
+  // >= 0 and a conv row outside the image contributes nothing), its group's 32 channels
+  float mx[32];
 #pragma unroll
-  for (int r = 0; r < 3; ++r)
-    if (o.oh0 + r >= 0 && o.oh0 + r < d.oh) rmask |= 1u << r;
-  const int ow0 = o.ow0, ow = d.ow;
+  for (int k = 0; k < 32; ++k) mx[k] = 0.0f;
+  const float4* bp = reinterpret_cast<const float4*>(__builtin_assume_aligned(bias + 32 * grp, 16));
+  float4 bq[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) bq[i] = bp[i];
+#pragma unroll 1
+  for (int c = 0; c < 3; ++c) {
+    const int cr = o.oh0 + c;
+    if (cr < 0 || cr >= d.oh) continue;  // (uniform over the CTA)
+    uint32_t v[32];
+    tmem_ld16(taddr + 64 * c + 32 * grp, *reinterpret_cast<uint32_t(*)[16]>(v));
+    tmem_ld16(taddr + 64 * c + 32 * grp + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      mx[4 * i] = fmaxf(mx[4 * i], __uint_as_float(v[4 * i]) + bq[i].x);
+      mx[4 * i + 1] = fmaxf(mx[4 * i + 1], __uint_as_float(v[4 * i + 1]) + bq[i].y);
+      mx[4 * i + 2] = fmaxf(mx[4 * i + 2], __uint_as_float(v[4 * i + 2]) + bq[i].z);
+      mx[4 * i + 3] = fmaxf(mx[4 * i + 3], __uint_as_float(v[4 * i + 3]) + bq[i].w);
+    }
+  }
+  // staged as bf16 [conv column][64 channels] (128-byte swizzle); rows >= out_w are junk the
+  // pooling never reads
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk)
+    *reinterpret_cast<uint4*>(pb + row * 128 + (((4 * grp + kk) ^ (row & 7)) << 4)) =
+        make_uint4(pack_bf16x2(mx[8 * kk], mx[8 * kk + 1]), pack_bf16x2(mx[8 * kk + 2], mx[8 * kk + 3]),
+                   pack_bf16x2(mx[8 * kk + 4], mx[8 * kk + 5]), pack_bf16x2(mx[8 * kk + 6], mx[8 * kk + 7]));
+  if (et == 0) bulk_wait_read<0>();  // the previous task's store has read the pooled stage
+  named_bar(1, kMkEpiThreads);
+  // 2) horizontal max over conv columns 2pw-1 .. 2pw+1 (the column left of 0 and right of the
+  // image contribute 0): the staged values are non-negative bf16, whose bit patterns order like
+  // their values: an unsigned 16-bit SIMD max per word is exact
+  const int ow = d.ow, npix = d.pool_pw * 8;
   for (int it = et; it < npix; it += kMkEpiThreads) {
     const int j = it >> 3, k = it & 7;
-    uint4 v[9];
+    uint32_t m4[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int cq = 0; cq < 3; ++cq) {
-        const int prow = r * bw + 2 * j + cq;  // always inside the staged tile
-        v[r * 3 + cq] = *reinterpret_cast<const uint4*>(pb + prow * 128 + ((k ^ (prow & 7)) << 4));
-      }
-    // the staged values are post-ReLU bf16 (>= 0), whose bit patterns order like their
-    // values once the sign bit (a possible -0) is cleared: the window max is an unsigned
-    // 16-bit SIMD max per word, exact; positions outside the image contribute 0 (every
-    // window holds at least one valid position, whose value is >= 0)
-    uint32_t mx[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int cq = 0; cq < 3; ++cq) {
-        const int cc = ow0 + 2 * j + cq;
-        const uint32_t keep = ((rmask >> r & 1) && cc >= 0 && cc < ow) ? 0x7FFF7FFFu : 0u;
-        const uint4 q = v[r * 3 + cq];
-        mx[0] = __vmaxu2(mx[0], q.x & keep);
-        mx[1] = __vmaxu2(mx[1], q.y & keep);
-        mx[2] = __vmaxu2(mx[2], q.z & keep);
-        mx[3] = __vmaxu2(mx[3], q.w & keep);
-      }
-    uint4 w;
-    w.x = mx[0];
-    w.y = mx[1];
-    w.z = mx[2];
-    w.w = mx[3];
-    *reinterpret_cast<uint4*>(ps + j * 128 + ((k ^ (j & 7)) << 4)) = w;
+    for (int dc = -1; dc <= 1; ++dc) {
+      const int cc = 2 * j + dc;
+      if (cc < 0 || cc >= ow) continue;
+      const uint4 q = *reinterpret_cast<const uint4*>(pb + cc * 128 + ((k ^ (cc & 7)) << 4));
+      m4[0] = __vmaxu2(m4[0], q.x & 0x7FFF7FFFu);  // (a -0 from fmaxf orders as +0)
+      m4[1] = __vmaxu2(m4[1], q.y & 0x7FFF7FFFu);
+      m4[2] = __vmaxu2(m4[2], q.z & 0x7FFF7FFFu);
+      m4[3] = __vmaxu2(m4[3], q.w & 0x7FFF7FFFu);
+    }
+    *reinterpret_cast<uint4*>(ps + j * 128 + ((k ^ (j & 7)) << 4)) = make_uint4(m4[0], m4[1], m4[2], m4[3]);
   }
   fence_proxy_async_smem();
   named_bar(1, kMkEpiThreads);
   if (et == 0) {
-    tma_store_4d(tmo, ps_addr, 0, pw0, ph, o.img0);
+    tma_store_4d(tmo, ps_addr, 0, 0, (o.oh0 + 1) / 2, o.img0);
     bulk_commit();
   }
-#ifdef CW_KB_TRACE
-  s3 = clock64();
-  if (blockIdx.x == 0 && et == 0 && o.oh0 < 8)
-    printf("stem epi: stage %lld, bar %lld, pool %lld\n", s1 - s0, s2 - s1, s3 - s2);
-#endif
 }
 // Warps 2-3: the input BatchNorm + ReLU prologue of DenseNet's pre-activation 1x1 convs:
 // relu(x * scale[c] + shift[c]) applied to the A tile of every k-block in place in shared
@@ -1308,7 +1300,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         }
         if (d.mode == 2) {
           // stem: weights once per layer (resident in the staging buffers), then per task ONE
-          // 5D box = the 7 kernel-row sub-tiles of the task's 3 x kMkStemW conv pixels
+          // box = the kMkStemRows padded input rows of the task's 3 conv rows
           if (elect_one()) {
             mbar_arrive_expect_tx(bar_stemb, 7u * 64u * 64u);
             for (int r = 0; r < 7; ++r)
@@ -1326,8 +1318,9 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
               mbar_wait_to<CW_HINT_EMPTY>(bar_empty + 8 * slot, ((par >> slot) & 1) ^ 1, 3);
               par ^= 1u << slot;
               if (elect_one()) {
-                mbar_arrive_expect_tx(bar_full + 8 * slot, 7u * kMkStemSub);
-                tma_load_5d(sbase + slot * sb, ta, bar_full + 8 * slot, 0, o.ow0, o.oh0, 0, o.img0);
+                // padded rows 2*oh0 .. 2*oh0 + 10: conv rows oh0 .. oh0 + 2, kernel rows 0 .. 6
+                mbar_arrive_expect_tx(bar_full + 8 * slot, (uint32_t)(kMkStemRows * d.sub_bytes));
+                tma_load_4d(sbase + slot * sb, ta, bar_full + 8 * slot, 0, 0, 2 * o.oh0, o.img0);
               }
               __syncwarp();
             }
@@ -1579,9 +1572,13 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         int slot = 0;
         bool first = true;
         if (d.mode == 2) {
-          // stem: 7 kernel rows x 2 K=16 steps per task, A sub-tiles kMkStemSub apart in the
-          // slot, B resident (4 KB per kernel row)
+          // stem: per task 3 conv rows (accumulators 64 columns apart) x 7 kernel rows x 2 K=16
+          // steps; A row j (conv column j) = the 64 bytes at 16j of staged row 2c + r: a
+          // no-swizzle K-major view with overlapping rows (LBO 16 B, SBO 128 B); B resident
+          // (4 KB of 64-byte-swizzled weights per kernel row)
           const uint64_t bst = sw64_kmajor_desc(obase + kMkStemB);
+          const uint32_t pitch = (uint32_t)d.sub_bytes;
+          if (first_task(d, cta, G) >= d.tasks) continue;  // (no weights were loaded here)
           mbar_wait_to<CW_HINT_FULL>(bar_stemb, 0, 5);
           for (int t = first_task(d, cta, G); t < d.tasks; t += G) {
             mbar_wait_to<CW_HINT_TEMPTY>(bar_tempty + 8 * acc, acc_phase ^ 1, 4);
@@ -1594,12 +1591,16 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
               first = false;
             }
             tc_fence_after();
-            const uint64_t ad = adesc0 + slot * sdesc;
+            const uint32_t sa = sbase + slot * sb;
             if (elect_one()) {
+#pragma unroll 1
+              for (int c = 0; c < 3; ++c) {
 #pragma unroll
-              for (int r = 0; r < 7; ++r) {
-                mma_bf16(dtm, ad + r * (kMkStemSub >> 4), bst + r * (4096 >> 4), idesc, r != 0);
-                mma_bf16(dtm, ad + r * (kMkStemSub >> 4) + 2, bst + r * (4096 >> 4) + 2, idesc, 1);
+                for (int r = 0; r < 7; ++r) {
+                  const uint32_t ra = sa + (uint32_t)(2 * c + r) * pitch;
+                  mma_bf16(dtm + 64 * c, desc_none(ra, 16, 128), bst + r * (4096 >> 4), idesc, r != 0);
+                  mma_bf16(dtm + 64 * c, desc_none(ra + 32, 16, 128), bst + r * (4096 >> 4) + 2, idesc, 1);
+                }
               }
               mma_commit(bar_empty + 8 * slot);
               mma_commit(bar_tfull + 8 * acc);

@@ -650,21 +650,25 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
           if (!fuse_max || nxt->out_h * 2 != op.out_h || nxt->pad != 1 || nxt->stride != 2)
             return "the stem conv must be followed by a 3x3/s2/p1 max pool";
           if (cout_p != 64 || op.cout != 64) return "the stem conv must have 64 channels";
-          // tiles of 19 pooled columns of one pooled row: 3 x 40 conv pixels (120 rows), all
-          // 7 kernel rows in one slot (sub-tiles kMkStemSub apart), weights resident
-          d.pool_pw = (kMkStemW - 1) / 2;
+          // one task per pooled row: conv rows 2ph-1 .. 2ph+1 over the full width (one
+          // accumulator of op.out_w <= 128 rows each), A = the kMkStemRows padded input rows
+          // they read, staged whole (weights resident in the staging buffers)
+          if (op.out_w > 128 || nxt->out_w > 256) return "stem wider than 128 conv columns";
+          d.pool_pw = nxt->out_w;
           d.OH = nxt->out_h;
           d.OW = nxt->out_w;
-          d.box_w = kMkStemW;
+          d.box_w = op.out_w;
           d.box_h = 3;
           d.box_n = 1;
-          d.tiles_w = (d.OW + d.pool_pw - 1) / d.pool_pw;
+          d.tiles_w = 1;
           d.tiles_h = d.OH;
-          d.m_tiles = d.tiles_w * d.tiles_h * batch;
+          d.m_tiles = d.tiles_h * batch;
           d.out = static_cast<uint8_t*>(a.bufs[nxt->out_buf]) + (size_t)nxt->out_coff * 2;
           d.out_ctot = nxt->out_ctot;
-          if (!make_tmap_stem(&tm, in, batch, op.in_h + 2 * kMkPadH, op.in_w + 2 * kMkPadW,
-                              op.out_w, op.out_h, d.box_w, d.box_h))
+          const int wp = op.in_w + 2 * kMkPadW;
+          d.sub_bytes = wp * 8;  // staged row pitch
+          if (2 * (op.out_w - 1) + 8 > wp) return "stem rows too narrow for the windows";
+          if (!make_tmap_stem_rows(&tm, in, batch, op.in_h + 2 * kMkPadH, wp, kMkStemRows))
             return "tensor map (stem) failed";
         } else if (!fuse_pool && op.kh == 1 && op.kw == 1 && op.stride == 1 && op.pad == 0 &&
                    op.pad_w == 0 && !(sc && sc->stride != 1)) {
@@ -933,11 +937,11 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
   if (const char* e = exp_env("CW_KPACK_MINSLOTS")) min_slots = atoi(e);
   for (auto& d : p.layers) {
     if (d.kind != MK_CONV) continue;
-    if (d.mode == 2) {  // stem: one slot = the 7 kernel-row A sub-tiles (weights resident)
-      d.kpack = 7;
-      d.sub_bytes = (int)kMkStemSub;
+    if (d.mode == 2) {  // stem: one slot = the task's staged input rows (weights resident);
+      // + 256 B: the junk accumulator rows (conv columns >= out_w) read past the last row
+      d.kpack = 1;
       d.b_off = 0;
-      d.slot_bytes = (int)((7 * kMkStemSub + 1023) / 1024 * 1024);
+      d.slot_bytes = (int)((kMkStemRows * d.sub_bytes + 256 + 1023) / 1024 * 1024);
       d.slots = std::min<int>(kMkMaxSlots, p.ring_bytes / d.slot_bytes);
       d.slots -= d.slots % kMkProducers;
       if (d.slots < 2) return "ring too small for the stem";

@@ -78,21 +78,17 @@ bool make_tmap_2d_sw64(CUtensorMap* out, const void* base, uint64_t k, uint64_t 
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Stem windows over NHWC4 rows (bf16 [n][hp][wp][4], hp = H + 6: 3 zero rows above and
-// below). Element (e, p, oh, r, n) is channel e % 4 of padded pixel 2p + e / 4 of padded row
-// 2*oh + r, i.e. window p is the 64 contiguous bytes starting at padded column 2p
-// (consecutive windows overlap: 16-byte stride) and (oh, r) address conv row oh's kernel row
-// r. A box (32, box_w, box_h, 7, 1) lands as 7 kernel-row sub-tiles of box_h x box_w rows.
-bool make_tmap_stem(CUtensorMap* out, const void* base, uint64_t n, uint64_t hp, uint64_t wp,
-                    uint64_t windows, uint64_t conv_rows, uint32_t box_w, uint32_t box_h) {
-  if (!tmap_init()) return false;
+// Whole padded NHWC4 rows (stem): dims (8, wp / 2, hp, n) with strides (16 B, row, image).
+bool make_tmap_stem_rows(CUtensorMap* out, const void* base, uint64_t n, uint64_t hp, uint64_t wp,
+                         uint32_t rows) {
+  if (!tmap_init() || wp % 2 || wp / 2 > 256) return false;
   const uint64_t row = wp * 8;
-  cuuint64_t dims[5] = {32, windows, conv_rows, 7, n};
-  cuuint64_t strides[4] = {16, 2 * row, row, hp * row};
-  cuuint32_t box[5] = {32, box_w, box_h, 7, 1};
-  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  return g_encode(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+  cuuint64_t dims[4] = {8, wp / 2, hp, n};
+  cuuint64_t strides[3] = {16, row, hp * row};
+  cuuint32_t box[4] = {8, (cuuint32_t)(wp / 2), rows, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return g_encode(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }

@@ -31,9 +31,10 @@ bool make_tmap_2d_f32(CUtensorMap* out, const void* base, uint64_t cols, uint64_
 bool make_tmap_2d_sw64(CUtensorMap* out, const void* base, uint64_t k, uint64_t rows,
                        uint32_t box_rows);
 
-// Overlapping 8-pixel windows over NHWC4 rows for the 7x7/s2 stem (see tmap.cpp): a 5D map
-// (window elements, window, conv row, kernel row, image) over rows padded by 3 zero rows.
-bool make_tmap_stem(CUtensorMap* out, const void* base, uint64_t n, uint64_t hp, uint64_t wp,
-                    uint64_t windows, uint64_t conv_rows, uint32_t box_w, uint32_t box_h);
+// Whole padded NHWC4 rows for the 7x7/s2 stem: bf16 [n][hp][wp][4] as a 4D map (8 elements =
+// 2 pixels, wp / 2, hp, n), box = kMkStemRows full rows of one image, no swizzle (rows land
+// contiguous, wp * 8 bytes apart). Rows outside the image are zero-filled.
+bool make_tmap_stem_rows(CUtensorMap* out, const void* base, uint64_t n, uint64_t hp, uint64_t wp,
+                         uint32_t rows);
 
 }  // namespace cw
