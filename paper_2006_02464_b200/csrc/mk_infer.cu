@@ -12,21 +12,27 @@
 //              the per-model tensor map in the model header) and the activation
 //              tile (A): mode 0 a [M][K] matrix box, mode 1 a tap-shifted NHWC
 //              box (implicit GEMM; padding = TMA out-of-bounds zero fill,
-//              stride = TMA element stride), mode 2 the stem's overlapping
-//              8-pixel row windows (one 5D box per task), mode 3 the 3x3/s1
-//              row box shared by the three horizontal taps. Weight tiles of a
-//              layer's first task are issued BEFORE waiting for the layer's inputs.
+//              stride = TMA element stride), mode 2 the stem's 11 padded input
+//              rows of one pooled row (one box per task, read by the MMAs as an
+//              implicit im2col with overlapping no-swizzle rows), mode 3 the
+//              3x3/s1 row box shared by the three horizontal taps; a fused
+//              projection shortcut adds a second K segment (its own A map and
+//              weights). Weight tiles of a layer's first task are issued BEFORE
+//              waiting for the layer's inputs.
 //     warp 1   tcgen05.mma issuer (one elected thread): M=128, N=bn, K=16 steps,
 //              fp32 accumulators in TMEM, two 256-column accumulators so the
 //              epilogue of task i overlaps the MMAs of task i+1.
-//     warps 2-3 idle (their registers go to the epilogue).
+//     warps 2-3 the DenseNet BN+ReLU A-tile prologue and the optional softmax
+//              tail; idle otherwise.
 //   warpgroups 1-2 (setmaxnreg 192): eight epilogue warps, two per TMEM lane
 //              quarter (group g = columns [32g, 32g+32) of every 64-column
 //              chunk): tcgen05.ld -> + bias (folded BatchNorm), + residual,
 //              ReLU -> bf16 into a 128-byte-swizzled staging buffer -> TMA
-//              store; or fp32 split-K partials, or the fused global average
+//              store (branch-free per residual / ReLU variant); or fp32 split-K
+//              partials, the cluster split-K reduction through distributed shared
+//              memory, the stem's 3x3/s2 max pool, or the fused global average
 //              pool. The same warps run the SIMT layers (input conversion, max
-//              pool, avg pool, split-K reduce, FC + logits).
+//              pool, avg pool, BN pool, im2col, split-K reduce, FC + logits).
 //
 // Layer completion: after a layer's stores, one epilogue thread per CTA adds its
 // task count to counter[L]; consumers spin with relaxed loads, then one acquire
