@@ -168,6 +168,12 @@ typedef struct cw_engine_config {
    * ("executor threads ... pinned, real-time priority"). */
   int32_t executor_cpu;
   int32_t executor_rt_prio;
+  /* cuda, gpu_count > 1: 1 = a LOAD of a model that another GPU of
+   * this worker holds resident copies the weights from that GPU's pages over NVLink
+   * (cudaMemcpyPeerAsync) instead of from pinned host memory (worker.py:263-266 copies
+   * host -> device). Off by default: it couples the two GPUs' copy engines and HBM, against
+   * the "no implicit side effects" rule. */
+  int32_t peer_load;
 } cw_engine_config;
 
 typedef struct cw_action {

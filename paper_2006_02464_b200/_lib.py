@@ -49,7 +49,7 @@ class cw_engine_config(C.Structure):
         ("io_capacity", C.c_int64), ("epoch_ns", C.c_int64),
         ("devices", C.POINTER(C.c_int32)), ("models", C.POINTER(cw_model_info)),
         ("io_slots", C.c_int64), ("in_bytes_max", C.c_int64), ("out_bytes_max", C.c_int64),
-        ("executor_cpu", C.c_int32), ("executor_rt_prio", C.c_int32)]
+        ("executor_cpu", C.c_int32), ("executor_rt_prio", C.c_int32), ("peer_load", C.c_int32)]
 
 
 class cw_action(C.Structure):

@@ -44,9 +44,26 @@ std::string Engine::open(const cw_engine_config& cfg) {
       for (int64_t p = 0; p < cfg.pages_per_gpu; ++p)
         gs.free_pages[p] = (int32_t)(cfg.pages_per_gpu - 1 - p);
       gs.page_fence.assign(cfg.pages_per_gpu, -1);
+      gs.page_peer.assign(cfg.pages_per_gpu, {});
       gs.free_slots.resize(cfg.io_slots);
       for (int64_t s = 0; s < cfg.io_slots; ++s) gs.free_slots[s] = (int32_t)(cfg.io_slots - 1 - s);
     }
+  }
+  if (cfg.mode == 1 && cfg.peer_load && cfg.gpu_count > 1) {
+    // peer LOAD: every GPU of the worker may read every other's pages
+    for (int g = 0; g < cfg.gpu_count; ++g)
+      for (int h = 0; h < cfg.gpu_count; ++h) {
+        const int dg = gpus_[g].rt->rt.device(), dh = gpus_[h].rt->rt.device();
+        if (dg == dh) continue;
+        int ok = 0;
+        if (cudaDeviceCanAccessPeer(&ok, dg, dh) != cudaSuccess || !ok)
+          return "peer_load: device " + std::to_string(dg) + " cannot access " + std::to_string(dh);
+        cudaSetDevice(dg);
+        const cudaError_t e = cudaDeviceEnablePeerAccess(dh, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          return std::string("peer_load: ") + cudaGetErrorString(e);
+        cudaGetLastError();  // (clear "already enabled")
+      }
   }
   return "";
 }
@@ -582,10 +599,46 @@ void Engine::device_load(int g, cw_action* a, int64_t now) {
     fence = std::max(fence, gpu.page_fence[pages[i]]);
   }
   // Page-reuse fence: a copy must not overwrite pages an in-flight Exec still reads
-  // (Runtime::load_async waits on the device only if that Exec has not completed).
+  // (Runtime::load_async waits on the device only if that Exec has not completed), nor pages
+  // a peer LOAD of another GPU is still reading.
   const uint64_t tag = ++load_tag_;
   LoadRecord* rec = nullptr;
-  std::string err = rt.load_async(mi.blob_id, pages.data(), n, fence, tag, &rec);
+  std::vector<cudaEvent_t> waits;
+  std::vector<std::shared_ptr<CUevent_st>> keep;  // (alive until the waits are enqueued)
+  for (int32_t p : pages) {
+    for (auto& e : gpu.page_peer[p]) {
+      waits.push_back(e.get());
+      keep.push_back(e);
+    }
+    gpu.page_peer[p].clear();
+  }
+  // Peer source: another GPU of this worker with the model resident
+  // and its own LOAD of it complete.
+  int src = -1;
+  if (cfg_.peer_load)
+    for (int h = 0; h < (int)gpus_.size() && src < 0; ++h) {
+      if (h == g || !gpus_[h].model_pages.count(a->model_id)) continue;
+      bool loading = false;
+      for (const InflightLoad& l : gpus_[h].loads) loading |= l.a->model_id == a->model_id;
+      if (!loading) src = h;
+    }
+  std::shared_ptr<CUevent_st> done;
+  if (src >= 0) {
+    cudaSetDevice(rt.device());
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      fail_device("load: peer event");
+      return;
+    }
+    done.reset(e, [](CUevent_st* x) { cudaEventDestroy(x); });
+  }
+  std::string err =
+      src < 0 ? rt.load_async(mi.blob_id, pages.data(), n, fence, tag, &rec, nullptr, nullptr,
+                              &waits)
+              : rt.load_async(mi.blob_id, pages.data(), n, fence, tag, &rec, &gpus_[src].rt->rt,
+                              gpus_[src].model_pages[a->model_id].data(), &waits, done.get());
+  if (src >= 0)  // the source pages stay readable until this copy completed
+    for (int32_t p : gpus_[src].model_pages[a->model_id]) gpus_[src].page_peer[p].push_back(done);
   gpu.model_pages[a->model_id] = std::move(pages);
   if (!err.empty()) {
     fail_device("load: " + err);

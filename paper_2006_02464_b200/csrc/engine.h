@@ -17,6 +17,7 @@
 #include <condition_variable>
 #include <cstdint>
 #include <deque>
+#include <memory>
 #include <mutex>
 #include <queue>
 #include <string>
@@ -135,6 +136,9 @@ struct GpuState {
   cw_runtime* rt = nullptr;
   std::vector<int32_t> free_pages;
   std::vector<int64_t> page_fence;  // per physical page: last exec seq that read it, -1 none
+  // per physical page: the events of the peer LOADs that copied FROM it to other GPUs since
+  // it was last written (a LOAD into the page on this GPU waits for them)
+  std::vector<std::vector<std::shared_ptr<CUevent_st>>> page_peer;
   std::unordered_map<uint32_t, std::vector<int32_t>> model_pages;
   std::unordered_map<uint32_t, int64_t> model_last_exec;
   std::vector<int32_t> free_slots;

@@ -1084,7 +1084,9 @@ std::string Runtime::build_plans() {
 // ---------------------------------------------------------------- actions
 
 std::string Runtime::load_async(int blob, const int32_t* pages, int npages, int64_t fence_seq,
-                                uint64_t tag, LoadRecord** rec_out) {
+                                uint64_t tag, LoadRecord** rec_out, const Runtime* peer,
+                                const int32_t* peer_pages,
+                                const std::vector<cudaEvent_t>* waits, cudaEvent_t done) {
   CW_TRY(cudaSetDevice(device_));
   auto it = blobs_.find(blob);
   if (it == blobs_.end()) return "unknown blob";
@@ -1125,16 +1127,25 @@ std::string Runtime::load_async(int blob, const int32_t* pages, int npages, int6
     const uint64_t s = exec_seq_ - (uint64_t)fence_seq <= kRing ? (uint64_t)fence_seq : exec_seq_ - 1;
     CW_TRY(cudaStreamWaitEvent(s_load_, exec_events_[s & (kRing - 1)], 0));
   }
+  if (waits)
+    for (cudaEvent_t e : *waits) CW_TRY(cudaStreamWaitEvent(s_load_, e, 0));
+  if (peer && peer->page_bytes_ != page_bytes_) return "peer load: page sizes differ";
   launch_stamp(&rec->t_start, tag, s_load_);
   for (int i = 0; i < b.npages; ++i) {
     const size_t off = (size_t)i * page_bytes_;
     const size_t skip = i == 0 ? kHeaderBytes : 0;
     const size_t n = std::min((size_t)page_bytes_, b.bytes - off);
-    CW_TRY(cudaMemcpyAsync(page_ptr(pages[i]) + skip, b.host + off + skip, n - skip,
-                           cudaMemcpyHostToDevice, s_load_));
+    if (peer)  // the same bytes, resident on the peer GPU (its header differs: skipped)
+      CW_TRY(cudaMemcpyPeerAsync(page_ptr(pages[i]) + skip, device_,
+                                 peer->page_ptr(peer_pages[i]) + skip, peer->device_, n - skip,
+                                 s_load_));
+    else
+      CW_TRY(cudaMemcpyAsync(page_ptr(pages[i]) + skip, b.host + off + skip, n - skip,
+                             cudaMemcpyHostToDevice, s_load_));
   }
   CW_TRY(cudaMemcpyAsync(page_ptr(pages[0]), hdr, kHeaderBytes, cudaMemcpyHostToDevice, s_load_));
   launch_stamp(&rec->t_end, tag, s_load_);
+  if (done) CW_TRY(cudaEventRecord(done, s_load_));
   CW_TRY(cudaGetLastError());
   *rec_out = rec;
   return "";

@@ -128,8 +128,16 @@ class Runtime {
   // Page-reuse fence: when fence_seq >= 0 (the last INFER that read one of these pages)
   // and that INFER has not completed, the copy first waits for it on the device.
   // The record slot is returned; completion when rec->tag_end == tag.
+  // peer: copy the weights from `peer`'s resident pages of the same
+  // blob (cudaMemcpyPeerAsync) instead of from pinned host memory; the header (absolute
+  // addresses of THESE pages) still comes from the host. `waits`: events of earlier peer
+  // copies that read these pages as their source (they must finish before the overwrite);
+  // `done`: recorded on the Load stream after the copies.
   std::string load_async(int blob, const int32_t* pages, int npages, int64_t fence_seq,
-                         uint64_t tag, LoadRecord** rec);
+                         uint64_t tag, LoadRecord** rec, const Runtime* peer = nullptr,
+                         const int32_t* peer_pages = nullptr,
+                         const std::vector<cudaEvent_t>* waits = nullptr,
+                         cudaEvent_t done = nullptr);
 
   // ---- Input stage: copy request inputs into IOCache slots (async, IO stream).
   // Completion when rec->tag == tag.

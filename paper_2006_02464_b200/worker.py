@@ -71,7 +71,7 @@ class Engine:
     def __init__(self, cat: catalog_mod.Catalog, *, mode: str, worker_id: int, gpu_count: int,
                  pages_per_gpu: int, io_capacity: int, epoch_ns: int = 0, devices=None,
                  io_slots: int = 0, in_bytes_max: int = 3 * 224 * 224 * 4,
-                 out_bytes_max: int = 4000):
+                 out_bytes_max: int = 4000, peer_load: bool = False):
         self.cat = cat
         bases = cat.bases()
         self.base_index = {b: i for i, b in enumerate(bases)}
@@ -106,6 +106,7 @@ class Engine:
         cfg.io_capacity = io_capacity
         cfg.epoch_ns = epoch_ns
         cfg.devices = self._devices
+        cfg.peer_load = 1 if peer_load else 0
         cfg.models = models
         cfg.io_slots = io_slots
         cfg.in_bytes_max = in_bytes_max
@@ -293,7 +294,11 @@ class B200Worker:
                  keep_records: bool = True, *, mode: str = "cuda", devices=None,
                  weights_seed: int = 0, input_pool: int = 64, epoch_ns: int | None = None,
                  keep_outputs: bool = False, poll_results: bool = True,
-                 weights_dir: str | None = None, softmax: bool = False):
+                 weights_dir: str | None = None, softmax: bool = False,
+                 peer_load: bool = False):
+        """peer_load (cuda, gpu_count > 1): a LOAD of a model another GPU of this worker holds
+        copies the weights from that GPU over NVLink instead of from host memory (SURVEY.md
+        §8f rank 3; off by default, see include/cw.h cw_engine_config.peer_load)."""
         if mode not in ("cuda", "sim"):
             raise ValueError(f"mode must be 'cuda' or 'sim', not {mode!r}")
         if jitter is not None and getattr(jitter, "kind", "none") != "none" and \
@@ -340,7 +345,7 @@ class B200Worker:
         self.engine = Engine(cat, mode=mode, worker_id=worker_id, gpu_count=gpu_count,
                              pages_per_gpu=pages_per_gpu, io_capacity=io_capacity,
                              epoch_ns=epoch_ns, devices=devices, io_slots=io_slots,
-                             in_bytes_max=in_max, out_bytes_max=out_max)
+                             in_bytes_max=in_max, out_bytes_max=out_max, peer_load=peer_load)
         self.specs = specs
         if mode == "cuda":
             blobs = {}
