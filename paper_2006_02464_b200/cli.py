@@ -50,6 +50,8 @@ def main(argv=None) -> int:
                    help="serve the controller socket from native threads (csrc/net.cpp)")
     p.add_argument("--weights", default="",
                    help="directory of <arch>.cwm model artifacts (default: random-init weights)")
+    p.add_argument("--peer-load", action="store_true",
+                   help="with --gpus > 1: LOAD from another GPU holding the model (NVLink)")
     p.add_argument("--softmax", action="store_true",
                    help="INFER outputs class probabilities (softmax tail) instead of logits")
     k = sub.add_parser("pack", help="fold + pack a torchvision-named state dict (.npz) into a "
@@ -73,7 +75,8 @@ def main(argv=None) -> int:
                  ready_fd=args.ready_fd if args.ready_fd >= 0 else None,
                  worker_id=args.worker_id, devices=devices, mode=args.mode,
                  weights_seed=args.weights_seed, native=args.native_net,
-                 weights_dir=args.weights or None, softmax=args.softmax)
+                 weights_dir=args.weights or None, softmax=args.softmax,
+                 peer_load=args.peer_load)
     return 0
 
 

@@ -40,7 +40,7 @@ def serve(listen: str, catalog, gpu_count: int = 1, pages_per_gpu: int = 500, ji
           io_capacity: int = DEFAULT_IO_CAPACITY, ready_fd: int | None = None, *,
           worker_id: int = 0, devices=None, mode: str = "cuda", weights_seed: int = 0,
           on_ready=None, native: bool = False, weights_dir: str | None = None,
-          softmax: bool = False) -> None:
+          softmax: bool = False, peer_load: bool = False) -> None:
     """native=True: after the accept, the connection is served by cw_net_serve (csrc/net.cpp):
     frames are decoded into the engine and results encoded back in native threads, with no
     Python on the per-action path."""
@@ -74,7 +74,8 @@ def serve(listen: str, catalog, gpu_count: int = 1, pages_per_gpu: int = 500, ji
                         pages_per_gpu=pages_per_gpu, io_capacity=io_capacity, jitter=jitter,
                         seed=seed, keep_records=bool(telemetry_path), mode=mode, devices=devices,
                         weights_seed=weights_seed, epoch_ns=clock.epoch_ns,
-                        poll_results=not native, weights_dir=weights_dir, softmax=softmax)
+                        poll_results=not native, weights_dir=weights_dir, softmax=softmax,
+                        peer_load=peer_load)
     if ready_fd is not None:
         os.write(ready_fd, f"{bound}\n".encode())
         os.close(ready_fd)
