@@ -30,6 +30,10 @@ namespace cw {
 namespace {
 std::mutex g_exec_mu;
 std::map<int, std::pair<cudaStream_t, int>> g_exec_streams;  // device -> (stream, users)
+// device -> uid of the plan whose table the last INFER launched on it copied into the
+// constant bank (launches are serialised on the device's Exec stream, in this order)
+std::map<int, uint64_t> g_bank_plan;
+std::atomic<uint64_t> g_plan_uid{1};
 
 cudaError_t acquire_exec_stream(int device, cudaStream_t* out) {
   std::lock_guard<std::mutex> lk(g_exec_mu);
@@ -69,6 +73,8 @@ Runtime::~Runtime() {
     for (auto& [b, p] : a.plans) {
       if (p.exec) cudaGraphExecDestroy(p.exec);
       if (p.graph) cudaGraphDestroy(p.graph);
+      if (p.exec_nocopy) cudaGraphExecDestroy(p.exec_nocopy);
+      if (p.graph_nocopy) cudaGraphDestroy(p.graph_nocopy);
       cudaFree(p.d_layers);
       cudaFree(p.d_tmaps);
       cudaFree(p.d_counters);
@@ -1036,18 +1042,21 @@ std::string Runtime::capture(Arch& a, Plan& p) {
     if (d.kind == MK_CONV && d.pre_layer >= 0) args.pre_bn = 1;
   args.softmax = p.layers.back().kind == MK_SOFTMAX;
   args.csize = p.csize;
-  CW_TRY(cudaStreamBeginCapture(s_cap_, cudaStreamCaptureModeThreadLocal));
-  cudaError_t ce = copy_plan(p.d_layers, (int)p.layers.size(), s_cap_);
-  launch_gate(ab_, ring_, kRing - 1, ctr_, exec_recs_, s_cap_);
-  cudaError_t le = launch_mk(args, p.grid, p.smem, s_cap_);
-  launch_mk_done(ab_, kRing - 1, exec_recs_, p.d_gen, exec_done_, s_cap_);
-  cudaGraph_t g = nullptr;
-  cudaError_t e = cudaStreamEndCapture(s_cap_, &g);
-  CW_TRY(ce);
-  CW_TRY(le);
-  CW_TRY(e);
-  p.graph = g;
-  CW_TRY(cudaGraphInstantiate(&p.exec, g, 0));
+  for (int copy = 1; copy >= 0; --copy) {
+    CW_TRY(cudaStreamBeginCapture(s_cap_, cudaStreamCaptureModeThreadLocal));
+    cudaError_t ce = copy ? copy_plan(p.d_layers, (int)p.layers.size(), s_cap_) : cudaSuccess;
+    launch_gate(ab_, ring_, kRing - 1, ctr_, exec_recs_, s_cap_);
+    cudaError_t le = launch_mk(args, p.grid, p.smem, s_cap_);
+    launch_mk_done(ab_, kRing - 1, exec_recs_, p.d_gen, exec_done_, s_cap_);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s_cap_, &g);
+    CW_TRY(ce);
+    CW_TRY(le);
+    CW_TRY(e);
+    (copy ? p.graph : p.graph_nocopy) = g;
+    CW_TRY(cudaGraphInstantiate(copy ? &p.exec : &p.exec_nocopy, g, 0));
+  }
+  p.uid = g_plan_uid.fetch_add(1);
   p.launches = 3;
   return "";
 }
@@ -1205,7 +1214,14 @@ std::string Runtime::exec_async(int arch, int batch, int32_t hdr_page, const int
   d.batch = batch;
   std::atomic_thread_fence(std::memory_order_seq_cst);
   if (input_seq >= 0) CW_TRY(cudaStreamWaitEvent(s_exec_, in_events_[input_seq & (kRing - 1)], 0));
-  CW_TRY(cudaGraphLaunch(pit->second.exec, s_exec_));
+  {
+    // the plan-table copy only when the device's constant bank holds another plan
+    std::lock_guard<std::mutex> lk(g_exec_mu);
+    uint64_t& bank = g_bank_plan[device_];
+    const Plan& p = pit->second;
+    CW_TRY(cudaGraphLaunch(bank == p.uid ? p.exec_nocopy : p.exec, s_exec_));
+    bank = p.uid;
+  }
   exec_seq_ = seq + 1;  // the gate consumed ring entry seq: host and device stay aligned
   CW_TRY(cudaEventRecord(exec_events_[seq & (kRing - 1)], s_exec_));
   *seq_out = seq;

@@ -66,6 +66,11 @@ struct Plan {
   int csize = 1;  // thread-block cluster size of the megakernel launch (cluster split-K)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  // the same INFER without the plan-table copy into the constant bank: launched when the
+  // previous INFER on this device ran this very plan (its table is still there)
+  cudaGraph_t graph_nocopy = nullptr;
+  cudaGraphExec_t exec_nocopy = nullptr;
+  uint64_t uid = 0;  // process-unique plan id (what the device's constant bank holds)
   int launches = 0;  // kernels per INFER (gate + megakernel + done)
 };
 
