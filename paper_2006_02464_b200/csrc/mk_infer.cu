@@ -815,8 +815,9 @@ __device__ __forceinline__ void mbar_wait_cluster_to(uint32_t bar, uint32_t pari
 // Cluster split-K epilogue (d.csplit): split z of a tile runs on cluster rank z (planner:
 // tasks = tiles x C, rotation a multiple of C, bn = 64). Rank z stages its fp32 partial tile
 // [128][64] in the upper half of its staging buffers (16-byte chunks XOR-swizzled by row),
-// then ONE bulk DSMEM copy per rank j moves row block j (rows [j*rpc, (j+1)*rpc), rpc = 128/C)
-// into slot z of rank j's receive buffer (the lower half); each rank then sums the C partial
+// then ONE bulk DSMEM copy per other rank j moves row block j (rows [j*rpc, (j+1)*rpc),
+// rpc = 128/C) into slot z of rank j's receive buffer (the lower half; block z itself stays in
+// this rank's staging half and is read there); each rank then sums the C partial
 // blocks of its own rows + bias (+ residual) (+ ReLU) -> bf16 rows -> bulk stores. Per task
 // (the ranks of a cluster run the same task sequence): bar_crdy completes once all C ranks'
 // buffers are free (each rank arrives on every rank's), bar_crx once this rank's C blocks
@@ -845,7 +846,7 @@ __device__ __noinline__ void epi_csplit(const MkLayer& d, const TileOrigin& o, i
   named_bar(1, kMkEpiThreads);
   // (relaxed signals: this rank's reads of its receive buffer are complete, their values were
   // consumed before the barrier; the copies into it are ordered by the transaction count)
-  if (et == 0) mbar_arrive_expect_tx(bar_crx, kTile);
+  if (et == 0) mbar_arrive_expect_tx(bar_crx, kTile - blk);
   if ((et & 31) == 0)
     for (int j = et >> 5; j < C; j += kMkEpiThreads / 32)
       mbar_arrive_remote(mapa_shared(bar_crdy, (uint32_t)j));
@@ -898,8 +899,9 @@ __device__ __noinline__ void epi_csplit(const MkLayer& d, const TileOrigin& o, i
   named_bar(1, kMkEpiThreads);
   if ((et & 31) == 0)  // (one issuing lane per warp: the copies leave in parallel)
     for (uint32_t j = (uint32_t)(et >> 5); j < (uint32_t)C; j += kMkEpiThreads / 32)
-      bulk_s2cluster(mapa_shared(obase + (uint32_t)z * blk, j), obase + kTile + j * blk, blk,
-                     mapa_shared(bar_crx, j));
+      if (j != (uint32_t)z)  // (this rank's own block is read from its staging half)
+        bulk_s2cluster(mapa_shared(obase + (uint32_t)z * blk, j), obase + kTile + j * blk, blk,
+                       mapa_shared(bar_crx, j));
   CW_CST(4);
   mbar_wait_cluster_to(bar_crx, cpar, 17);
   CW_CST(5);
@@ -910,7 +912,8 @@ __device__ __noinline__ void epi_csplit(const MkLayer& d, const TileOrigin& o, i
     float4 a4 = acc[k];
     const int pc = c4[k] ^ (li[k] & 7);  // (row & 7 == li & 7: rpc is a multiple of 8)
     for (int s = 0; s < C; ++s) {
-      const float4 p = src[(s * rpc + li[k]) * c4n + pc];
+      // (summed in rank order 0..C-1: every rank's rows see the same association)
+      const float4 p = s == z ? src[(C * rpc + r0 + li[k]) * c4n + pc] : src[(s * rpc + li[k]) * c4n + pc];
       a4.x += p.x;
       a4.y += p.y;
       a4.z += p.z;
