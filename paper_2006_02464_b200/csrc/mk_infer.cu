@@ -1186,9 +1186,15 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   __shared__ uint64_t kbt[4][64];  // debug: producer acquire / A issued, MMA full / committed
   __shared__ uint64_t ket[2][64];  // debug: epilogue events (clock, tag)
   int kbp = 0, kbm = 0, kbe = 0;
+#ifndef CW_KB_LAYER
+#define CW_KB_LAYER -1  // trace one plan layer only (-1: from the first)
+#endif
+#ifndef CW_KB_ET
+#define CW_KB_ET 0  // the traced epilogue thread
+#endif
 #define CW_KET(tag_)                                                   \
   do {                                                                 \
-    if (cta == 0 && et == 0 && kbe < 64) {                             \
+    if (cta == 0 && et == CW_KB_ET && kbe < 64 && (CW_KB_LAYER < 0 || L == CW_KB_LAYER)) { \
       ket[0][kbe] = clock64();                                         \
       ket[1][kbe++] = (tag_);                                          \
     }                                                                  \
@@ -1771,6 +1777,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
           const int z = t - tile * d.splits;
           const TileOrigin o = tile_origin(d, tile);
           const uint32_t taddr = tmem + acc * 256 + ((uint32_t)(q * 32) << 16);
+          CW_KET(62);
           if (d.csplit) {
             const uint32_t bar_acc = bar_tfull + 8 * acc;
             if (args.csize == 8)
@@ -1952,10 +1959,12 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
             }
           }
           // accumulator drained: hand it back to the MMA warp
+          CW_KET(60);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_tempty + 8 * acc);
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          CW_KET(61);
         }
         if (d.csplit) {  // (this CTA had tasks: the cluster's ranks all did)
           csplit_drain(args.csize, et, bar_cdone, cdpar);
@@ -2033,7 +2042,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
   tc_fence_before();
   __syncthreads();
 #ifdef CW_KB_TRACE
-  if (cta == 0 && threadIdx.x == kMkEpiWarp0 * 32) {
+  if (cta == 0 && threadIdx.x == kMkEpiWarp0 * 32 + CW_KB_ET) {
     for (int i = 0; i < kbe; ++i)
       printf("ep %2d tag %3d t %6lld\n", i, (int)ket[1][i], (long long)(ket[0][i] - ket[0][0]));
   }

@@ -6,6 +6,9 @@
 //   mode 1: st.global.v4 by 8 warps, coalesced (each warp instruction: 4 rows x 128 B)
 //   mode 2: st.global.v4 by 8 warps, row per thread (the accumulator layout: a warp
 //           instruction touches 32 rows x 16 B)
+//   mode 3: per-warp TMA stores: each of the 8 warps' lane 0 stores its own 32 rows x 32
+//           columns (a 2 KB box, 64-byte swizzle) of every chunk, no CTA barrier
+// Also reports the issuing thread's cycles per store instruction + commit (issue cost).
 // Reports bytes per clock per SM and the aggregate bandwidth.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -14,15 +17,18 @@
 
 #include "../paper_2006_02464_b200/csrc/ptx.cuh"
 
-__global__ void __launch_bounds__(256) probe(const __grid_constant__ CUtensorMap tm, uint4* out,
+__global__ void __launch_bounds__(256) probe(const __grid_constant__ CUtensorMap tm,
+                                              const __grid_constant__ CUtensorMap tm32, uint4* out,
                                               int mode, int issuers, int reps, int tiles,
-                                              unsigned long long* cyc) {
+                                              unsigned long long* cyc, unsigned long long* icyc) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t base = (cw::smem_u32(smem) + 1023u) & ~1023u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __syncthreads();
   const long long t0 = clock64();
   const int chunks = tiles * 4;
+  long long issue = 0;
+  int nissue = 0;
   if (mode == 0) {
     if (lane == 0 && warp < issuers) {
       int n = 0;
@@ -31,12 +37,34 @@ __global__ void __launch_bounds__(256) probe(const __grid_constant__ CUtensorMap
           const int nb = issuers == 1 ? 4 : 12 / issuers;
           const uint32_t src = base + (warp * nb + n % nb) * 16384u;
           const int row = (blockIdx.x * tiles + i / 4) * 128, col = (i % 4) * 64;
+          cw::bulk_wait_read_n(nb - 1);
+          const long long q0 = clock64();
           cw::tma_store_2d(&tm, src, col, row);
           cw::bulk_commit();
-          cw::bulk_wait_read_n(nb - 1);
+          issue += clock64() - q0;
+          ++nissue;
         }
       cw::bulk_wait_all();
     }
+  } else if (mode == 3) {
+    // warp w: rows 32 (w & 3) .. +31, columns 32 (w >> 2) .. +31 of each 64-column chunk
+    if (lane == 0) {
+      int n = 0;
+      for (int r = 0; r < reps; ++r)
+        for (int i = 0; i < chunks; ++i, ++n) {
+          const uint32_t src = base + (uint32_t)(warp * 6 + n % 6) * 2048u;
+          const int row = (blockIdx.x * tiles + i / 4) * 128 + 32 * (warp & 3);
+          const int col = (i % 4) * 64 + 32 * (warp >> 2);
+          cw::bulk_wait_read_n(5);
+          const long long q0 = clock64();
+          cw::tma_store_2d(&tm32, src, col, row);
+          cw::bulk_commit();
+          issue += clock64() - q0;
+          ++nissue;
+        }
+      cw::bulk_wait_all();
+    }
+    __syncwarp();
   } else {
     const uint4 v = make_uint4(threadIdx.x, 1, 2, 3);
     for (int r = 0; r < reps; ++r)
@@ -60,6 +88,7 @@ __global__ void __launch_bounds__(256) probe(const __grid_constant__ CUtensorMap
   }
   __syncthreads();
   if (threadIdx.x == 0) cyc[blockIdx.x] = clock64() - t0;
+  if (threadIdx.x == 0) icyc[blockIdx.x] = nissue ? issue / nissue : 0;
 }
 
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -78,12 +107,17 @@ int main() {
   cudaMalloc(&buf, rows * 512);
   unsigned long long* cyc;
   cudaMalloc(&cyc, 148 * 8);
-  CUtensorMap tm;
+  unsigned long long* icyc;
+  cudaMalloc(&icyc, 148 * 8);
+  CUtensorMap tm, tm32;
   cuuint64_t d[2] = {256, (cuuint64_t)rows};
   cuuint64_t s[1] = {512};
   cuuint32_t b[2] = {64, 128}, e[2] = {1, 1};
   enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, d, s, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint32_t b32[2] = {32, 32};
+  enc(&tm32, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, d, s, b32, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaEvent_t a, z;
   cudaEventCreate(&a);
@@ -92,12 +126,14 @@ int main() {
   struct Case { int mode, issuers; const char* name; } cases[] = {
       {0, 1, "TMA store, 1 issuer   "}, {0, 2, "TMA store, 2 issuers  "},
       {0, 3, "TMA store, 3 issuers  "}, {0, 6, "TMA store, 6 issuers  "},
+      {3, 8, "TMA store, per warp   "},
       {1, 0, "st.global coalesced   "}, {2, 0, "st.global row/thread  "}};
   for (const Case& c : cases) {
     float best = 1e9;
     for (int r = 0; r < 4; ++r) {
       cudaEventRecord(a);
-      probe<<<148, 256, 12 * 16384 + 1024>>>(tm, (uint4*)buf, c.mode, c.issuers, reps, tiles, cyc);
+      probe<<<148, 256, 12 * 16384 + 1024>>>(tm, tm32, (uint4*)buf, c.mode, c.issuers, reps, tiles,
+                                             cyc, icyc);
       cudaEventRecord(z);
       cudaEventSynchronize(z);
       float ms;
@@ -106,11 +142,14 @@ int main() {
     }
     unsigned long long h[148];
     cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
-    double mc = 0;
-    for (int i = 0; i < 148; ++i) mc += (double)h[i] / 148;
+    unsigned long long hi[148];
+    cudaMemcpy(hi, icyc, sizeof(hi), cudaMemcpyDeviceToHost);
+    double mc = 0, mi = 0;
+    for (int i = 0; i < 148; ++i) mc += (double)h[i] / 148, mi += (double)hi[i] / 148;
     const double per_sm = (double)reps * tiles * 4 * 16384;
-    printf("%s %7.1f us  %6.0f GB/s  %5.1f B/clk/SM  (%5.0f cycles per 16 KB chunk)\n", c.name,
-           best * 1e3, 148 * per_sm / (best * 1e-3) / 1e9, per_sm / mc, mc / (reps * tiles * 4));
+    printf("%s %7.1f us  %6.0f GB/s  %5.1f B/clk/SM  (%5.0f cycles per 16 KB chunk, issue %4.0f "
+           "cycles per store)\n", c.name, best * 1e3, 148 * per_sm / (best * 1e-3) / 1e9,
+           per_sm / mc, mc / (reps * tiles * 4), mi);
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
