@@ -371,46 +371,47 @@ __device__ __forceinline__ void simt_input(const MkLayer& d, const ActionBlock* 
 }
 
 // 3x3 max pool, stride / padding from the plan (padding = -inf: skipped), input channel
-// stride in_ctot, output at the layer's channel slice of a buffer of stride out_ctot.
+// stride in_ctot, output at the layer's channel slice of a buffer of stride out_ctot. One
+// thread per (output pixel, 8-channel chunk); the maxima on packed bf16 pairs (exact: the
+// max of bf16 values is one of them, as it was through fp32).
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&a),
+                             *reinterpret_cast<const __nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
 __device__ __forceinline__ void simt_maxpool(const MkLayer& d, int cta, int G, int et) {
   const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(d.in);
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(d.out);
   const int chunks = d.C / 8;
   const int total = d.batch * d.OH * d.OW * chunks;
-  const int st = d.stride, pd = d.pad;
+  const int st = d.stride, pd = d.pad, H = d.H, W = d.W, OW = d.OW, OH = d.OH;
+  const long long ct = d.in_ctot;
   for (int t = cta * kMkEpiThreads + et; t < total; t += G * kMkEpiThreads) {
-    const int j = t % chunks;
     const int p = t / chunks;
-    const int ow = p % d.OW;
-    const int oh = (p / d.OW) % d.OH;
-    const int n = p / (d.OW * d.OH);
-    uint4 v[9];
+    const int j = t - p * chunks;
+    const int q = p / OW;
+    const int ow = p - q * OW;
+    const int n = q / OH;
+    const int oh = q - n * OH;
+    const int ih0 = oh * st - pd, iw0 = ow * st - pd;
+    const __nv_bfloat16* base = in + ((long long)n * H * W) * ct + j * 8;
+    uint4 m = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);  // -inf
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
+      const int ih = ih0 + r;
+      if (ih < 0 || ih >= H) continue;
 #pragma unroll
       for (int s = 0; s < 3; ++s) {
-        const int ih = oh * st - pd + r, iw = ow * st - pd + s;
-        if (ih >= 0 && ih < d.H && iw >= 0 && iw < d.W)
-          v[r * 3 + s] = __ldcg(reinterpret_cast<const uint4*>(
-              in + (((long long)n * d.H + ih) * d.W + iw) * d.in_ctot + j * 8));
-        else
-          v[r * 3 + s] = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);  // -inf
+        const int iw = iw0 + s;
+        if (iw < 0 || iw >= W) continue;
+        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(base + ((long long)ih * W + iw) * ct));
+        m.x = bmax2(m.x, v.x);
+        m.y = bmax2(m.y, v.y);
+        m.z = bmax2(m.z, v.z);
+        m.w = bmax2(m.w, v.w);
       }
     }
-    float m[8], f[8];
-    bf16x8_to_f32(v[0], m);
-#pragma unroll
-    for (int i = 1; i < 9; ++i) {
-      bf16x8_to_f32(v[i], f);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) m[e] = fmaxf(m[e], f[e]);
-    }
-    uint4 o;
-    o.x = pack_bf16x2(m[0], m[1]);
-    o.y = pack_bf16x2(m[2], m[3]);
-    o.z = pack_bf16x2(m[4], m[5]);
-    o.w = pack_bf16x2(m[6], m[7]);
-    *reinterpret_cast<uint4*>(out + (long long)p * d.out_ctot + j * 8) = o;
+    *reinterpret_cast<uint4*>(out + (long long)p * d.out_ctot + j * 8) = m;
   }
 }
 
@@ -516,28 +517,51 @@ __device__ __forceinline__ void simt_bnpool(const MkLayer& d, const uint8_t* hdr
 // 299x299, 3x3/s2 valid): patches of the fp32 NCHW request images -> bf16 [M][64] rows
 // (k = (r*KW + s)*C + c, zero past KH*KW*C), the A operand of a 1x1-shaped GEMM. One
 // thread per output pixel: consecutive threads read stride-2 columns of the same rows.
+// The layer is load-latency bound (8 warps per SM): 3x3 kernels over 3 channels (the only
+// user) issue all 27 loads of a pixel at once, (c, r, s) of every k resolved at compile
+// time; other shapes take the generic loop.
 __device__ __forceinline__ void simt_im2col(const MkLayer& d, const ActionBlock* ab, int cta,
                                             int G, int et) {
   uint4* out = reinterpret_cast<uint4*>(d.out);
-  const int K = d.kw, C = d.C, st = d.stride, pd = d.pad;
-  const int total = d.batch * d.OH * d.OW;
-  const long long plane = (long long)d.H * d.W;
+  const int K = d.kw, C = d.C, st = d.stride, pd = d.pad, OW = d.OW, OH = d.OH, H = d.H, W = d.W;
+  const int total = d.batch * OH * OW;
+  const long long plane = (long long)H * W;
   for (int m = cta * kMkEpiThreads + et; m < total; m += G * kMkEpiThreads) {
-    const int ow = m % d.OW;
-    const int oh = (m / d.OW) % d.OH;
-    const int n = m / (d.OW * d.OH);
+    const int t = m / OW;
+    const int ow = m - t * OW;
+    const int n = t / OH;
+    const int oh = t - n * OH;
+    const int ih0 = oh * st - pd, iw0 = ow * st - pd;
     const float* img = ab->in[n];
-    const int kkc = K * K * C;
     uint4* o = out + (long long)m * 8;
+    if (K == 3 && C == 3) {
+      float f[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const int c = k % 3, r = (k / 3) / 3, s = (k / 3) % 3;
+        const int ih = ih0 + r, iw = iw0 + s;
+        f[k] = (k < 27 && ih >= 0 && ih < H && iw >= 0 && iw < W)
+                   ? __ldg(img + c * plane + (long long)ih * W + iw) : 0.0f;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        o[q] = make_uint4(pack_bf16x2(f[8 * q], f[8 * q + 1]), pack_bf16x2(f[8 * q + 2], f[8 * q + 3]),
+                          pack_bf16x2(f[8 * q + 4], f[8 * q + 5]),
+                          pack_bf16x2(f[8 * q + 6], f[8 * q + 7]));
+#pragma unroll
+      for (int q = 4; q < 8; ++q) o[q] = make_uint4(0u, 0u, 0u, 0u);
+      continue;
+    }
+    const int kkc = K * K * C;
     for (int q = 0; q < 8; ++q) {
       float f[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int k = 8 * q + e;
         const int c = k % C, rs = k / C, s = rs % K, r = rs / K;
-        const int ih = oh * st - pd + r, iw = ow * st - pd + s;
-        f[e] = (k < kkc && ih >= 0 && ih < d.H && iw >= 0 && iw < d.W)
-                   ? __ldg(img + c * plane + ih * d.W + iw) : 0.0f;
+        const int ih = ih0 + r, iw = iw0 + s;
+        f[e] = (k < kkc && ih >= 0 && ih < H && iw >= 0 && iw < W)
+                   ? __ldg(img + c * plane + (long long)ih * W + iw) : 0.0f;
       }
       o[q] = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]),
                         pack_bf16x2(f[4], f[5]), pack_bf16x2(f[6], f[7]));

@@ -15,7 +15,8 @@ batches = [int(b) for b in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1,
 spec = arch.build_arch(name)
 blob = arch.pack_blob(spec, arch.fold(spec, arch.make_params(spec, 0)))
 names = {1: "conv", 2: "input", 3: "maxpool", 4: "avgpool", 5: "fc", 6: "reduce"}
-with DeviceRuntime(pages_total=8 * blob.pages, io_slots=16) as rt:
+with DeviceRuntime(pages_total=8 * blob.pages, io_slots=16,
+                   in_bytes_max=spec.in_c * spec.in_h * spec.in_w * 4) as rt:
     rt.register_arch(0, spec)
     rt.register_blob(0, 0, blob)
     rt.build()
