@@ -1109,6 +1109,10 @@ __device__ __forceinline__ void epi_stem_pool(const MkLayer* dp, const TileOrigi
 // owns physical 16-byte chunk t & 7 of rows (t >> 3) + 8i: under the 128-byte swizzle (chunk
 // j of row r at j ^ (r & 7)) that is ONE logical chunk, i.e. the same 8 channels, for all
 // its rows, so the k-block's scale/shift of those channels stay in registers.
+#ifndef CW_PRE_UNROLL
+#define CW_PRE_UNROLL 4
+#endif
+constexpr int kPreUnroll = CW_PRE_UNROLL;
 __device__ __noinline__ void bn_prologue(const MkLayer* sl, int nl, int cta, int G,
                                          const uint8_t* hdr, uint8_t* smem, uint32_t bar_fpre,
                                          uint32_t bar_xf, int t64) {
@@ -1126,18 +1130,25 @@ __device__ __noinline__ void bn_prologue(const MkLayer* sl, int nl, int cta, int
       int kb0, kb1;
       split_range(d, t % d.splits, kb0, kb1);
       const int n = kb1 - kb0;  // kpack = 1: a k-block per slot
+      // this thread's 8 channels' scale / shift, one k-block ahead (an L2 round trip per
+      // k-block otherwise sits between the tile landing and its rewrite)
+      float4 s0, s1, h0, h1;
+      auto load_tab = [&](int kb) {
+        const int c0 = kb * 64 + lc * 8;
+        s0 = __ldg(reinterpret_cast<const float4*>(ptab + c0));
+        s1 = __ldg(reinterpret_cast<const float4*>(ptab + c0 + 4));
+        h0 = __ldg(reinterpret_cast<const float4*>(ptab + cpad + c0));
+        h1 = __ldg(reinterpret_cast<const float4*>(ptab + cpad + c0 + 4));
+      };
+      if (n > 0) load_tab(kb0);
       for (int i = 0; i < n; ++i) {
-        const int c0 = (kb0 + i) * 64 + lc * 8;
-        const float4 s0 = __ldg(reinterpret_cast<const float4*>(ptab + c0));
-        const float4 s1 = __ldg(reinterpret_cast<const float4*>(ptab + c0 + 4));
-        const float4 h0 = __ldg(reinterpret_cast<const float4*>(ptab + cpad + c0));
-        const float4 h1 = __ldg(reinterpret_cast<const float4*>(ptab + cpad + c0 + 4));
         const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
         const float sh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        if (i + 1 < n) load_tab(kb0 + i + 1);
         mbar_wait_to<64>(bar_fpre + 8 * slot, (par >> slot) & 1, 13);
         par ^= 1u << slot;
         uint8_t* tile = smem + slot * sb;
-#pragma unroll 4
+#pragma unroll kPreUnroll
         for (int r = rg; r < 128; r += 8) {
           uint4* q = reinterpret_cast<uint4*>(tile + r * 128 + pc * 16);
           float f[8];

@@ -428,7 +428,11 @@ static void plan_conv(MkLayer& d, int cout, int G, bool allow_split, bool groupe
     if ((d.mode == 2 || grouped) && bn != 64) continue;  // grouped: one 64-channel block per tile
     const int tiles = d.m_tiles * (cout / bn);
     const int n_tma = 1 + ((bn == std::min(256, cout) && d.kblk == 64) ? 1 : bn / 64);
-    const double t_kb = std::max({0.30, 0.08 * n_tma + 0.1, (a_bytes + bn * d.kblk * 2.0) / 140e3});
+    // (an input-BatchNorm layer: warps 2-3 rewrite every A k-block in shared memory before
+    // its MMAs, ~1.25 us per k-block measured on DenseNet-121's 1x1 convs)
+    static const double pre_us = exp_env("CW_PRE_KB_US") ? atof(exp_env("CW_PRE_KB_US")) : 1.25;
+    const double t_kb = std::max({d.pre_layer >= 0 ? pre_us : 0.30, 0.08 * n_tma + 0.1,
+                                  (a_bytes + bn * d.kblk * 2.0) / 140e3});
     for (int s = 1; s <= 32; ++s) {
       int per;
       if (csize > 1) {
