@@ -640,6 +640,18 @@ __device__ __forceinline__ void fc_mac(const float* const (&pn)[NI], const __nv_
 // thread 8 classes x its K chunks, warp reduce-scatter, then the image's warps through
 // shared memory. Batch 9..16: a warp per image pair (images w and w+8), 2 x 8 sums per
 // thread: half the shared-memory weight reads per FMA.
+// The CTA's first weight block does not depend on the previous layers: requested (with the
+// transaction bytes of the pooled block too) before the dependency wait.
+__device__ __forceinline__ void simt_fc_prefetch(const MkLayer& d, const uint8_t* hdr, int cta,
+                                                 uint32_t sw_addr, uint32_t bar) {
+  if (cta >= (d.classes + 7) / 8) return;
+  const __nv_bfloat16* wbase =
+      reinterpret_cast<const __nv_bfloat16* const*>(hdr + kHdrWeightOff)[d.wlayer];
+  const int j0 = cta * 8, nj = min(8, d.classes - j0);
+  const uint32_t wbytes = (uint32_t)(nj * d.C * 2);
+  mbar_arrive_expect_tx(bar, wbytes + (uint32_t)(d.batch * d.C * 4));
+  bulk_g2s(sw_addr, wbase + (size_t)j0 * d.C, wbytes, bar);
+}
 __device__ __forceinline__ void simt_fc(const MkLayer& d, const ActionBlock* ab, const uint8_t* hdr,
                                      int cta, int G, int et, float* sp, uint32_t sp_addr,
                                      const __nv_bfloat16* sw, uint32_t sw_addr, float* sred,
@@ -660,9 +672,12 @@ __device__ __forceinline__ void simt_fc(const MkLayer& d, const ActionBlock* ab,
       fence_proxy_async();  // pooled was written by generic stores of other CTAs
       const uint32_t wbytes = (uint32_t)(nj * C * 2);
       const uint32_t pbytes = pooled_in ? 0u : (uint32_t)(d.batch * C * 4);
-      mbar_arrive_expect_tx(bar, wbytes + pbytes);
-      if (!pooled_in) bulk_g2s(sp_addr, d.in, pbytes, bar);
-      bulk_g2s(sw_addr, wbase + (size_t)j0 * C, wbytes, bar);
+      if (pooled_in) {
+        mbar_arrive_expect_tx(bar, wbytes);
+        bulk_g2s(sw_addr, wbase + (size_t)j0 * C, wbytes, bar);
+      } else {  // first block: its weights were requested by simt_fc_prefetch
+        bulk_g2s(sp_addr, d.in, pbytes, bar);
+      }
     }
     pooled_in = true;
 #ifdef CW_KB_TRACE
@@ -1154,7 +1169,7 @@ __device__ __noinline__ void bn_prologue(const MkLayer* sl, int nl, int cta, int
           float f[8];
           bf16x8_to_f32(*q, f);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) f[e] = fmaf(f[e], sc[e], sh[e]);
+          for (int e = 0; e < 8; e += 2) ffma2(f[e], f[e + 1], sc[e], sc[e + 1], sh[e], sh[e + 1]);
           uint4 o;
           o.x = pack_bf16x2_relu(f[0], f[1]);
           o.y = pack_bf16x2_relu(f[2], f[3]);
@@ -2024,6 +2039,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) mk_infer_kernel(const __grid_co
         const MkLayer& d = sl[L];
         if (d.kind == MK_SOFTMAX) continue;  // run by warps 2-3 (softmax_tail)
         if (d.kind == MK_REDUCE && first_task(d, cta, G) >= d.tasks) continue;
+        if (d.kind == MK_FC && et == 0) simt_fc_prefetch(d, hdr, cta, obase, bar_simt);
         if (et == 0) wait_deps(sl, L, counters, gen1, 9);
         named_bar(1, kMkEpiThreads);
         if (args.trace && et == 0) args.trace[((size_t)L * G + cta) * 4 + 1] = globaltimer();

@@ -323,6 +323,15 @@ __device__ __forceinline__ void fadd2(float& a0, float& a1, float b0, float b1) 
   a0 = __uint_as_float((uint32_t)x);
   a1 = __uint_as_float((uint32_t)(x >> 32));
 }
+// a = a * s + h on a pair (one FFMA2; each lane the IEEE fp32 fma)
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float s0, float s1, float h0, float h1) {
+  uint64_t x = (uint64_t)__float_as_uint(a0) | ((uint64_t)__float_as_uint(a1) << 32);
+  const uint64_t y = (uint64_t)__float_as_uint(s0) | ((uint64_t)__float_as_uint(s1) << 32);
+  const uint64_t z = (uint64_t)__float_as_uint(h0) | ((uint64_t)__float_as_uint(h1) << 32);
+  asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x) : "l"(y), "l"(z));
+  a0 = __uint_as_float((uint32_t)x);
+  a1 = __uint_as_float((uint32_t)(x >> 32));
+}
 // bf16x2 {lo = a, hi = b} with ReLU fused into the conversion (max(round(x), 0) == round(max(x, 0)))
 __device__ __forceinline__ uint32_t pack_bf16x2_relu(float a, float b) {
   uint32_t d;
