@@ -463,7 +463,11 @@ static void plan_conv(MkLayer& d, int cout, int G, bool allow_split, bool groupe
       }
     }
   }
-  // experiment overrides (profiling only): CW_FORCE_BN, CW_FORCE_SPLIT
+  // experiment overrides (profiling only): CW_BN_CAP, CW_FORCE_BN, CW_FORCE_SPLIT
+  if (const char* e = exp_env("CW_BN_CAP")) {
+    const int cap = atoi(e);
+    if (cap >= 64 && best_bn > cap && cout % cap == 0 && best_s == 1) best_bn = cap;
+  }
   if (const char* e = exp_env("CW_FORCE_BN")) {
     const int bn = atoi(e);
     if (bn > 0 && cout % bn == 0 && ((d.mode != 2 && !grouped) || bn == 64)) best_bn = bn;
@@ -561,7 +565,13 @@ std::string Runtime::build_plan(Arch& a, int batch, bool allow_split) {
   // (B200: 120 CTAs in clusters of 8, 132 in clusters of 4, all 148 in pairs). Measured
   // (ResNet-50 Exec p50 without -> with, tools/ab_quick.py): b=1 275 -> 248 us (8), b=2 305 ->
   // 279 (4), b=4 346 -> 309 (4), b=8 422 -> 400 (2), b=16 551 -> 524 (2).
-  int csize = batch == 1 ? 8 : batch <= 4 ? 4 : 2;
+  // Nets with input-BatchNorm layers (DenseNet: long-K 1x1 bottlenecks whose k-blocks cost
+  // ~4x an MMA's) gain from one size larger: DenseNet-121 b=4 777 -> 744 us, b=8 951 -> 843;
+  // DenseNet-169 b=2 1093 -> 1029, b=4 1139 -> 1057, b=8 1451 -> 1209.
+  bool has_pre_bn = false;
+  for (const CwOp& op : a.ops) has_pre_bn |= (op.flags & OPF_PRE_BN) != 0;
+  int csize = has_pre_bn ? (batch <= 4 ? 8 : batch <= 8 ? 4 : 2)
+                         : (batch == 1 ? 8 : batch <= 4 ? 4 : 2);
   if (const char* e = exp_env("CW_CSIZE")) csize = atoi(e);
   if (csize != 1 && csize != 2 && csize != 4 && csize != 8) return "cluster size must be 1, 2, 4 or 8";
   int G = num_sms_;
