@@ -379,39 +379,58 @@ __device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
                              *reinterpret_cast<const __nv_bfloat162*>(&b));
   return *reinterpret_cast<uint32_t*>(&r);
 }
+// Issue the 9 window loads of item t (padding taps read a clamped in-bounds pixel and are
+// masked to -inf afterwards: no branches between the loads).
+__device__ __forceinline__ void maxpool_loads(const MkLayer& d, const __nv_bfloat16* in, int t,
+                                              int chunks, uint4 (&v)[9], uint32_t& valid,
+                                              long long& out_off) {
+  const int H = d.H, W = d.W, OW = d.OW, OH = d.OH;
+  const long long ct = d.in_ctot;
+  const int p = t / chunks;
+  const int j = t - p * chunks;
+  const int q = p / OW;
+  const int ow = p - q * OW;
+  const int n = q / OH;
+  const int oh = q - n * OH;
+  const int ih0 = oh * d.stride - d.pad, iw0 = ow * d.stride - d.pad;
+  const __nv_bfloat16* base = in + ((long long)n * H * W) * ct + j * 8;
+  valid = 0;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int ih = ih0 + r, iw = iw0 + s;
+      const bool ok = ih >= 0 && ih < H && iw >= 0 && iw < W;
+      valid |= (ok ? 1u : 0u) << (r * 3 + s);
+      const int ihc = min(max(ih, 0), H - 1), iwc = min(max(iw, 0), W - 1);
+      v[r * 3 + s] = __ldcg(reinterpret_cast<const uint4*>(base + ((long long)ihc * W + iwc) * ct));
+    }
+  }
+  out_off = (long long)p * d.out_ctot + j * 8;
+}
+__device__ __forceinline__ uint4 maxpool_reduce(const uint4 (&v)[9], uint32_t valid) {
+  uint4 m = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);  // -inf
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    if (!((valid >> i) & 1u)) continue;
+    m.x = bmax2(m.x, v[i].x);
+    m.y = bmax2(m.y, v[i].y);
+    m.z = bmax2(m.z, v[i].z);
+    m.w = bmax2(m.w, v[i].w);
+  }
+  return m;
+}
 __device__ __forceinline__ void simt_maxpool(const MkLayer& d, int cta, int G, int et) {
   const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(d.in);
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(d.out);
   const int chunks = d.C / 8;
   const int total = d.batch * d.OH * d.OW * chunks;
-  const int st = d.stride, pd = d.pad, H = d.H, W = d.W, OW = d.OW, OH = d.OH;
-  const long long ct = d.in_ctot;
   for (int t = cta * kMkEpiThreads + et; t < total; t += G * kMkEpiThreads) {
-    const int p = t / chunks;
-    const int j = t - p * chunks;
-    const int q = p / OW;
-    const int ow = p - q * OW;
-    const int n = q / OH;
-    const int oh = q - n * OH;
-    const int ih0 = oh * st - pd, iw0 = ow * st - pd;
-    const __nv_bfloat16* base = in + ((long long)n * H * W) * ct + j * 8;
-    uint4 m = make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);  // -inf
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const int ih = ih0 + r;
-      if (ih < 0 || ih >= H) continue;
-#pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        const int iw = iw0 + s;
-        if (iw < 0 || iw >= W) continue;
-        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(base + ((long long)ih * W + iw) * ct));
-        m.x = bmax2(m.x, v.x);
-        m.y = bmax2(m.y, v.y);
-        m.z = bmax2(m.z, v.z);
-        m.w = bmax2(m.w, v.w);
-      }
-    }
-    *reinterpret_cast<uint4*>(out + (long long)p * d.out_ctot + j * 8) = m;
+    uint4 v[9];
+    uint32_t valid;
+    long long o;
+    maxpool_loads(d, in, t, chunks, v, valid, o);
+    *reinterpret_cast<uint4*>(out + o) = maxpool_reduce(v, valid);
   }
 }
 
@@ -519,14 +538,52 @@ __device__ __forceinline__ void simt_bnpool(const MkLayer& d, const uint8_t* hdr
 // thread per output pixel: consecutive threads read stride-2 columns of the same rows.
 // The layer is load-latency bound (8 warps per SM): 3x3 kernels over 3 channels (the only
 // user) issue all 27 loads of a pixel at once, (c, r, s) of every k resolved at compile
-// time; other shapes take the generic loop.
+// time; other shapes take the generic loop (two pixels per round spill the epilogue warps'
+// registers: measured slower).
+// 3x3 x 3-channel patch of output pixel m: its 27 loads issued together (k >= 27 zero).
+__device__ __forceinline__ void im2col_33_loads(const MkLayer& d, const ActionBlock* ab, int m,
+                                                float (&f)[32]) {
+  const int OW = d.OW, OH = d.OH, H = d.H, W = d.W;
+  const long long plane = (long long)H * W;
+  const int t = m / OW;
+  const int ow = m - t * OW;
+  const int n = t / OH;
+  const int oh = t - n * OH;
+  const int ih0 = oh * d.stride - d.pad, iw0 = ow * d.stride - d.pad;
+  const float* img = ab->in[n];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const int c = k % 3, r = (k / 3) / 3, s = (k / 3) % 3;
+    const int ih = ih0 + r, iw = iw0 + s;
+    f[k] = (k < 27 && ih >= 0 && ih < H && iw >= 0 && iw < W)
+               ? __ldg(img + c * plane + (long long)ih * W + iw) : 0.0f;
+  }
+}
+__device__ __forceinline__ void im2col_33_store(uint4* o, const float (&f)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    o[q] = make_uint4(pack_bf16x2(f[8 * q], f[8 * q + 1]), pack_bf16x2(f[8 * q + 2], f[8 * q + 3]),
+                      pack_bf16x2(f[8 * q + 4], f[8 * q + 5]), pack_bf16x2(f[8 * q + 6], f[8 * q + 7]));
+#pragma unroll
+  for (int q = 4; q < 8; ++q) o[q] = make_uint4(0u, 0u, 0u, 0u);
+}
 __device__ __forceinline__ void simt_im2col(const MkLayer& d, const ActionBlock* ab, int cta,
                                             int G, int et) {
   uint4* out = reinterpret_cast<uint4*>(d.out);
   const int K = d.kw, C = d.C, st = d.stride, pd = d.pad, OW = d.OW, OH = d.OH, H = d.H, W = d.W;
   const int total = d.batch * OH * OW;
+  const int step = G * kMkEpiThreads;
+  if (K == 3 && C == 3) {
+    for (int m = cta * kMkEpiThreads + et; m < total; m += step) {
+      float f[32];
+      im2col_33_loads(d, ab, m, f);
+      im2col_33_store(out + (long long)m * 8, f);
+    }
+    return;
+  }
   const long long plane = (long long)H * W;
-  for (int m = cta * kMkEpiThreads + et; m < total; m += G * kMkEpiThreads) {
+  const int kkc = K * K * C;
+  for (int m = cta * kMkEpiThreads + et; m < total; m += step) {
     const int t = m / OW;
     const int ow = m - t * OW;
     const int n = t / OH;
@@ -534,25 +591,6 @@ __device__ __forceinline__ void simt_im2col(const MkLayer& d, const ActionBlock*
     const int ih0 = oh * st - pd, iw0 = ow * st - pd;
     const float* img = ab->in[n];
     uint4* o = out + (long long)m * 8;
-    if (K == 3 && C == 3) {
-      float f[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const int c = k % 3, r = (k / 3) / 3, s = (k / 3) % 3;
-        const int ih = ih0 + r, iw = iw0 + s;
-        f[k] = (k < 27 && ih >= 0 && ih < H && iw >= 0 && iw < W)
-                   ? __ldg(img + c * plane + (long long)ih * W + iw) : 0.0f;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        o[q] = make_uint4(pack_bf16x2(f[8 * q], f[8 * q + 1]), pack_bf16x2(f[8 * q + 2], f[8 * q + 3]),
-                          pack_bf16x2(f[8 * q + 4], f[8 * q + 5]),
-                          pack_bf16x2(f[8 * q + 6], f[8 * q + 7]));
-#pragma unroll
-      for (int q = 4; q < 8; ++q) o[q] = make_uint4(0u, 0u, 0u, 0u);
-      continue;
-    }
-    const int kkc = K * K * C;
     for (int q = 0; q < 8; ++q) {
       float f[8];
 #pragma unroll
