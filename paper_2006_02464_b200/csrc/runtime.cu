@@ -375,7 +375,8 @@ static void box_dims_dense(int nimg, int oh, int ow, int* bw, int* bh, int* bn) 
     return (double)ow * oh * nimg / (tiles * 128.0);
   };
   const double base = util(*bw, *bh, *bn);
-  if (base >= 0.7) return;
+  static const double thresh = exp_env("CW_DENSE_BELOW") ? atof(exp_env("CW_DENSE_BELOW")) : 0.7;
+  if (base >= thresh) return;
   double best = -1.0;
   int bw2 = *bw, bh2 = *bh, bn2 = *bn;
   for (int w = 1; w <= std::min(ow, 128); ++w)
