@@ -1201,6 +1201,9 @@ __device__ __noinline__ void bn_prologue(const MkLayer* sl, int nl, int cta, int
         mbar_wait_to<64>(bar_fpre + 8 * slot, (par >> slot) & 1, 13);
         par ^= 1u << slot;
         uint8_t* tile = smem + slot * sb;
+#ifdef CW_PRE_NOOP  // experiments: the hand-off without the rewrite (wrong logits; timing only)
+        if (sb != 0u) { fence_proxy_async_smem(); mbar_arrive(bar_xf + 8 * slot); if (++slot == ns) slot = 0; continue; }
+#endif
 #pragma unroll kPreUnroll
         for (int r = rg; r < 128; r += 8) {
           uint4* q = reinterpret_cast<uint4*>(tile + r * 128 + pc * 16);
