@@ -226,7 +226,7 @@ def ncu_traffic(b: int):
     """DRAM bytes (read + write) per launch of the INFER megakernel at batch b, from the
     newest committed `ncu --set full` capture summary (tools/ncu_capture.sh +
     tools/ncu_summary.py) under profiles/."""
-    for name in ("r2c_ncu_full_mk_infer_summary.json", "r2b_ncu_full_mk_infer_summary.json",
+    for name in ("r2d_ncu_full_mk_infer_summary.json", "r2c_ncu_full_mk_infer_summary.json", "r2b_ncu_full_mk_infer_summary.json",
                  "r2_ncu_full_mk_infer_summary.json",
                  "r1_ncu_full_mk_infer_summary.json"):
         path = os.path.join(REPO, "profiles", name)
